@@ -1,0 +1,173 @@
+"""The whole hot path, step by step (oracle, fp64).  Test infrastructure only.
+
+Follows SURVEY §8(c) "Oracle algorithm": field B'(m, t) (step 3), torque (4), RK4 (5),
+memory update after the step on the new state (6), relax (7).  Inputs come in as the
+CUDA path receives them (fp32 m, B_rms), widened to fp64.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from .constants import GAMMA, HBAR
+from . import fields as F
+from . import tensor as T
+from .cavity import CavityMemory
+from .llg import torque, relax_torque, normalize, rk4_step
+
+ZEEMAN, EXCHANGE, ANIS, DEMAG, CAVITY, EXCITATION = 1, 2, 4, 8, 16, 32
+ALL = ZEEMAN | EXCHANGE | ANIS | DEMAG | CAVITY | EXCITATION
+RELAX_CHECK_EVERY = 50
+
+
+class Simulation:
+    def __init__(self, grid, cell, Ms, Aex, alpha, m0, mask=None, bext=(0.0, 0.0, 0.0),
+                 brms_map=None, brms_uniform=(0.0, 0.0, 0.0), f_c=1e9, kappa=0.0, x0=0.0, p0=0.0,
+                 exc_amp=0.0, exc_omega=0.0, aniso=None, demag="auto", octant=None, hbar=HBAR,
+                 gamma=GAMMA, terms=ALL):
+        self.grid = tuple(int(g) for g in grid)
+        nx, ny, nz = self.grid
+        self.shape = (nz, ny, nx)
+        self.cell = tuple(float(c) for c in cell)
+        self.vcell = self.cell[0] * self.cell[1] * self.cell[2]
+        self.Ms, self.Aex, self.alpha = float(Ms), float(Aex), float(alpha)
+        self.gamma = gamma
+        self.mag = np.ones(self.shape, bool) if mask is None else np.asarray(mask).reshape(self.shape).astype(bool)
+        self.m = np.asarray(m0, dtype=np.float64).reshape(self.shape + (3,)) * self.mag[..., None]
+        self.m = normalize(self.m)
+        self.bext = np.asarray(bext, dtype=np.float64)
+        if brms_map is not None:
+            self.brms = np.asarray(brms_map, dtype=np.float64).reshape(self.shape + (3,))
+        else:
+            self.brms = F.zeeman(self.shape, brms_uniform)
+        self.aniso = aniso or {}
+        self.exc_amp, self.exc_omega = float(exc_amp), float(exc_omega)
+        self.mem = CavityMemory(2 * math.pi * f_c, kappa, x0, p0, self.vcell, hbar)
+        n = nx * ny * nz
+        self.demag_mode = ("brute" if n <= 4096 else "dft") if demag == "auto" else demag
+        self._octant = octant
+        self._padded = None
+        self.terms = terms          # enabled field terms (e.g. the Dicke mapping uses B_ext + cavity only)
+
+    # ---------------------------------------------------------------- state
+    @property
+    def cavity_enabled(self):
+        """CavityFeatureStatus: 1 iff B_rms set and nonzero (reading C14)."""
+        return bool(np.any(self.brms != 0))
+
+    def octant(self):
+        if self._octant is None:
+            nx, ny, nz = self.grid
+            self._octant = T.tensor_octant((nx, ny, nz), self.cell)
+        return self._octant
+
+    # ---------------------------------------------------------------- field (step 3)
+    def demag(self, m):
+        if self.demag_mode == "brute":
+            return F.demag_bruteforce(m, self.mag, self.cell, self.Ms, self.octant())
+        if self.demag_mode == "dft":
+            if self._padded is None:
+                self._padded = T.padded_tensor(self.grid, self.cell, self.octant())
+            return F.demag_dft(m, self.mag, self.cell, self.Ms, self._padded)
+        return np.zeros_like(m)
+
+    def field(self, m, t, terms=ALL):
+        """B'(m, t) summed in the fixed order Zeeman, exchange, anisotropy, demag, excitation,
+        cavity; vacuum cells get 0.  Gamma uses the S_n, C_n of the last completed step (C3)."""
+        B = np.zeros_like(m)
+        terms &= self.terms
+        if terms & ZEEMAN:
+            B += F.zeeman(self.shape, self.bext)
+        if terms & EXCHANGE and self.Aex != 0.0:
+            B += F.exchange(m, self.mag, self.cell, self.Aex, self.Ms)
+        if terms & ANIS:
+            a = self.aniso
+            if a.get("ku1", 0.0):
+                B += F.uniaxial(m, self.mag, a["ku1"], a["u"], self.Ms)
+            if a.get("kc1", 0.0):
+                B += F.cubic(m, self.mag, a["kc1"], a["c1"], a["c2"], self.Ms)
+        if terms & DEMAG and self.demag_mode != "off":
+            B += self.demag(m)
+        if terms & EXCITATION and self.exc_amp != 0.0:
+            B += self.exc_amp * float(F.sinc(self.exc_omega * t)) * self.brms
+        if terms & CAVITY and self.cavity_enabled:
+            B += self.brms * self.mem.gamma(t)
+        return np.where(self.mag[..., None], B, 0.0)
+
+    def W(self, m):
+        """Overlap W = sum_i M_s,i m_i . B_rms(r_i)."""
+        return float(np.sum(self.Ms * np.sum(m * self.brms, axis=-1) * self.mag))
+
+    # ---------------------------------------------------------------- stepping (steps 4-6)
+    def rhs(self, m, t):
+        return torque(m, self.field(m, t), self.alpha, self.gamma)
+
+    def step(self, dt):
+        self.m = rk4_step(self.rhs, self.m, self.mem.t, dt)
+        W = self.W(self.m) if self.cavity_enabled else 0.0
+        self.mem.update(W, dt)
+
+    def run(self, dt, steps):
+        for _ in range(int(steps)):
+            self.step(dt)
+        return self.m
+
+    # ---------------------------------------------------------------- relax (step 7)
+    def max_torque(self, m=None):
+        m = self.m if m is None else m
+        B = self.field(m, self.mem.t, ALL & ~(CAVITY | EXCITATION))
+        return float(np.max(np.linalg.norm(np.cross(m, B), axis=-1)))
+
+    def relax(self, dt, tol, max_steps, check_every=RELAX_CHECK_EVERY):
+        """RK4 on -gamma m x (m x B') with cavity and excitation off and t frozen; every
+        ``check_every`` steps stop if max_i |m_i x B'_i| < tol; then reset memory (C15)."""
+        t0 = self.mem.t
+        terms = ALL & ~(CAVITY | EXCITATION)
+
+        def f(m, t):
+            return relax_torque(m, self.field(m, t0, terms), self.gamma)
+
+        steps = 0
+        while steps < max_steps:
+            k = min(check_every, max_steps - steps)
+            for _ in range(k):
+                self.m = rk4_step(f, self.m, t0, dt)
+            steps += k
+            if self.max_torque() < tol:
+                break
+        self.mem.reset()
+        return steps
+
+    def reset_memory(self):
+        self.mem.reset()
+
+    # ---------------------------------------------------------------- diagnostics (pins)
+    def energy(self, m=None):
+        """E = Vc sum_i [-M_s m.B_ext - 1/2 M_s m.(B_exch + B_demag) + e_anis]
+        - Vc W Gamma + hbar w_c |alpha|^2  (P:214 with S = -M_s Vc m / gamma; reading C22)."""
+        m = self.m if m is None else m
+        Ms = self.Ms * self.mag
+        e = -Ms * np.sum(m * self.bext, -1)
+        e = e - 0.5 * Ms * np.sum(m * F.exchange(m, self.mag, self.cell, self.Aex, self.Ms), -1)
+        if self.demag_mode != "off":
+            e = e - 0.5 * Ms * np.sum(m * self.demag(m), -1)
+        a = self.aniso
+        if a.get("ku1", 0.0):
+            u = np.asarray(a["u"], float)
+            u = u / np.linalg.norm(u)
+            e = e - a["ku1"] * (m @ u) ** 2 * self.mag
+        if a.get("kc1", 0.0):
+            c1 = np.asarray(a["c1"], float); c1 /= np.linalg.norm(c1)
+            c2 = np.asarray(a["c2"], float); c2 /= np.linalg.norm(c2)
+            c3 = np.cross(c1, c2)
+            m1, m2, m3 = m @ c1, m @ c2, m @ c3
+            e = e + a["kc1"] * (m1**2 * m2**2 + m2**2 * m3**2 + m3**2 * m1**2) * self.mag
+        E = self.vcell * float(np.sum(e))
+        if self.cavity_enabled:
+            al = self.mem.alpha()
+            E += -self.vcell * self.W(m) * 2 * al.real + self.mem.hbar * self.mem.omega_c * abs(al) ** 2
+        return E
+
+    def mean_m(self):
+        return (self.m * self.mag[..., None]).sum(axis=(0, 1, 2)) / self.mag.sum()
