@@ -1,0 +1,186 @@
+/*
+ * mcq.h — C ABI of the B200-native Mumax3-cQED hot path (arXiv 2410.00966).
+ *
+ * One context = one ferromagnet on an nx*ny*nz finite-difference grid coupled to one damped
+ * cavity mode.  Each mcq_run step integrates the LLG equation with the cavity field
+ *     dm_i/dt = -gamma/(1+alpha^2) [m_i x B'_i + alpha m_i x (m_i x B'_i)]            (eq:llg)
+ *     B'_i = B_ext + B_exch + B_anis + B_demag + a sinc(w_cut t) B_rms,i + B_rms,i Gamma(t)
+ *                                                     (eq:bcav P:239, excitation P:165)
+ * with classical RK4 at fixed dt (reading C1), stage renormalisation (C2), the cavity memory
+ * frozen inside a step (C3) and advanced once per step on the new state from the overlap
+ *     W = sum_i M_s m_i . B_rms(r_i)
+ * through the recursion of eq:Sdiscrete/eq:Cdiscrete/eq:gammadiscretefinal, kept on
+ * the device in the algebraically identical complex form
+ *     alpha_{n+1} = e^{-(kappa + i w_c) dt} alpha_n + i (V_c/hbar) W_{n+1} dt,  Gamma = 2 Re alpha
+ * (reading C5; alpha_0 = (x0 - i p0)/2, reading C6).  Constants: gamma = 1.7595e11 rad/(s T),
+ * mu0 = 4 pi 1e-7, hbar = 1.05457182e-34 J s (reading C8).
+ *
+ * Conventions (all calls):
+ *  - SI units; B in tesla; f_c in Hz (w_c = 2 pi f_c); kappa in rad/s (cavity FWHM = 2 kappa).
+ *  - Host vector arrays are interleaved (vx, vy, vz) per cell, cell index i = x + nx (y + ny z)
+ *    (x fastest).  Arrays are copied in/out before the call returns; no pointer is retained.
+ *    The caller owns every host array; the library owns the context and all device memory.
+ *  - Every call returns 0 (MCQ_OK) on success or a negative MCQ_E* code; mcq_last_error()
+ *    holds the message.  No C++ exception crosses the ABI.  A failing call leaves the
+ *    simulation state unchanged (except MCQ_ECUDA, after which the context must be destroyed).
+ *  - Device work is enqueued on the context's stream (mcq_set_stream; default: a library-owned
+ *    stream).  mcq_run / mcq_relax / setters are stream-ordered; getters synchronise.
+ *  - Single GPU in this build (dist == NULL or world == 1); z-slab decomposition is planned
+ *     and rejected with MCQ_EINVAL for world > 1.  Multi-GPU runs use replicas.
+ */
+#ifndef MCQ_H
+#define MCQ_H
+
+#if defined(__GNUC__)
+#define MCQ_API __attribute__((visibility("default")))
+#else
+#define MCQ_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MCQ_OK 0
+#define MCQ_EINVAL (-1)  /* invalid argument (values below) */
+#define MCQ_ESTATE (-2)  /* call not valid in the current state (e.g. run before set_m) */
+#define MCQ_ENOMEM (-3)  /* device allocation failed */
+#define MCQ_ECUDA (-4)   /* CUDA runtime / kernel error */
+#define MCQ_ENCCL (-5)   /* reserved for the multi-GPU build */
+
+/* field-term bitmask for mcq_get_field */
+#define MCQ_TERM_ZEEMAN 1u
+#define MCQ_TERM_EXCHANGE 2u
+#define MCQ_TERM_ANIS 4u
+#define MCQ_TERM_DEMAG 8u
+#define MCQ_TERM_CAVITY 16u     /* B_rms * Gamma(t) */
+#define MCQ_TERM_EXCITATION 32u /* a sinc(w_cut t) B_rms */
+#define MCQ_TERM_ALL 63u
+
+/* kernel classes reported by mcq_profile_run */
+#define MCQ_K_YFWD 0   /* y-forward FFT pass (3D)                        */
+#define MCQ_K_ZCONV 1  /* z-forward * Khat * z-inverse pass (3D)          */
+#define MCQ_K_YINV 2   /* y-inverse FFT pass (3D)                        */
+#define MCQ_K_Y2D 3    /* y-forward * Khat * y-inverse pass (nz == 1)     */
+#define MCQ_K_UPDATE 4 /* fused x-C2R + fields + torque + RK4 + x-R2C     */
+#define MCQ_K_CAVITY 5 /* overlap finalize + cavity state update          */
+#define MCQ_NKCLASS 6
+
+typedef struct mcq_ctx mcq_ctx; /* opaque, library-owned */
+
+/* Anisotropy (reading C10).  Energy densities -K_u1 (m.u)^2 and
+ * K_c1 (m1^2 m2^2 + m2^2 m3^2 + m3^2 m1^2) with m_k = m.c_k, c3 = c1 x c2.  J/m^3; axes are
+ * normalised by the library; ku1 == 0 / kc1 == 0 disables the term. */
+typedef struct {
+  double ku1, u[3];
+  double kc1, c1[3], c2[3];
+} mcq_aniso;
+
+/* Distribution descriptor.  This build: world must be 1 (or pass NULL). */
+typedef struct {
+  int rank, world, device;
+  const unsigned char *nccl_id; /* 128 bytes or NULL */
+  void *cuda_stream;            /* cudaStream_t or NULL */
+} mcq_dist;
+
+/* Cavity state at t_n (all ranks identical).  S, C are the paper's accumulators,
+ * reconstructed from alpha: S - i C = (hbar/V_c)(alpha_0 - e^{(kappa + i w_c) t} alpha). */
+typedef struct {
+  double t;                  /* cavity clock since the last reset (s)                   */
+  double re_alpha, im_alpha; /* alpha(t_n) = <a>                             */
+  double gamma;              /* Gamma(t_n) = 2 Re alpha = x(t_n) (eq:gammadiscretefinal) */
+  double W;                  /* overlap of the last completed step, A/m * T      */
+  double S, C;               /* literal accumulators (overflow beyond kappa t ~ 700)     */
+  double n_photon;           /* |alpha|^2                                        */
+  long long step;            /* completed steps since the last reset                    */
+} mcq_cavity_state;
+
+/* Create a context.  grid[3] = (nx, ny, nz) with 2 <= nx, ny <= 512 and 1 <= nz <= 512;
+ * cell[3] = (dx, dy, dz) > 0 metres; Ms > 0 (A/m; single material, vacuum via the geometry
+ * mask); Aex >= 0 (J/m); alpha >= 0 (Gilbert); K may be NULL; dist may be NULL.
+ * Precomputes the demag kernel (Newell near field, Gauss-Legendre far field, reading C11) on
+ * the device in fp64.  EINVAL on bad sizes/values; ENOMEM if HBM is insufficient. */
+MCQ_API int mcq_create(mcq_ctx **out, const int grid[3], const double cell[3], double Ms, double Aex,
+               double alpha, const mcq_aniso *K, const mcq_dist *dist);
+
+/* Use `stream` (a cudaStream_t, e.g. torch.cuda.current_stream().cuda_stream) for all work. */
+MCQ_API int mcq_set_stream(mcq_ctx *, void *stream);
+
+/* Geometry mask, N bytes, x fastest, 0 = vacuum (M_s = 0, m = 0).  NULL = full box.
+ * Applies to subsequent mcq_set_m calls and zeroes m in vacuum now. */
+MCQ_API int mcq_set_geometry(mcq_ctx *, const unsigned char *mask);
+
+/* Magnetisation, 3N floats interleaved (host).  Normalised on entry; vacuum cells are set to 0.
+ * EINVAL if a magnetic cell has a zero vector.  Does not touch the cavity state. */
+MCQ_API int mcq_set_m(mcq_ctx *, const float *m);
+/* Same from a device pointer (3N floats interleaved, device memory of this context's GPU). */
+MCQ_API int mcq_set_m_device(mcq_ctx *, const float *d_m);
+
+/* Uniform external field B_ext (T). */
+MCQ_API int mcq_set_bext(mcq_ctx *, const double B[3]);
+
+/* Cavity vacuum field B_rms: a per-cell map (3N floats interleaved, T) or, if map is
+ * NULL, the uniform vector `uniform` (T).  The cavity is enabled iff B_rms is nonzero (C14). */
+MCQ_API int mcq_set_brms(mcq_ctx *, const float *map, const double uniform[3]);
+
+/* Cavity parameters: f_c (Hz, > 0), kappa (rad/s, >= 0), x0 = 2 Re alpha_0, p0 = -2 Im alpha_0
+ * (P:362-368).  Resets the memory term (alpha <- alpha_0, t <- 0). */
+MCQ_API int mcq_set_cavity(mcq_ctx *, double f_c, double kappa, double x0, double p0);
+
+/* Excitation a * sinc(w_cut t) * B_rms, unnormalised sinc, t = cavity clock (C13). */
+MCQ_API int mcq_set_excitation(mcq_ctx *, double amplitude, double omega_cut);
+
+/* ResetMemoryTerm(): alpha <- alpha_0, t <- 0, step <- 0. */
+MCQ_API int mcq_reset_memory(mcq_ctx *);
+
+/* Relax (reading C15): RK4 with step dt (s) on dm/dt = -gamma m x (m x B'), cavity and
+ * excitation off, t frozen; every 50 steps stop if max_i |m_i x B'_i| < torque_tol (T); at
+ * most max_steps steps.  Then resets the memory term.  *steps_taken may be NULL. */
+MCQ_API int mcq_relax(mcq_ctx *, double dt, double torque_tol, long long max_steps, long long *steps_taken);
+
+/* Advance `steps` RK4 steps of size dt (s > 0), replaying a captured CUDA graph.  Enqueued on
+ * the context stream; returns without synchronising.  ESTATE before the first set_m. */
+MCQ_API int mcq_run(mcq_ctx *, double dt, long long steps);
+
+/* Block until all enqueued work is done; reports asynchronous kernel errors (ECUDA). */
+MCQ_API int mcq_synchronize(mcq_ctx *);
+
+/* Magnetisation out, 3N floats interleaved (host / device pointer). */
+MCQ_API int mcq_get_m(mcq_ctx *, float *m_out);
+MCQ_API int mcq_get_m_device(mcq_ctx *, float *d_out);
+
+/* Parity hook: B' (selected terms, MCQ_TERM_* bitmask) of the current m at the current cavity
+ * time (stage 1 of the next step), 3N floats interleaved, T; vacuum cells get 0. */
+MCQ_API int mcq_get_field(mcq_ctx *, float *b_out, unsigned terms);
+
+MCQ_API int mcq_get_cavity(mcq_ctx *, mcq_cavity_state *out);
+/* Resume: sets t, alpha (re/im) and step from `in` (other fields ignored). */
+MCQ_API int mcq_set_cavity_state(mcq_ctx *, const mcq_cavity_state *in);
+
+/* CavityFeatureStatus: 1 iff B_rms is set and nonzero, else 0; <0 on error. */
+MCQ_API int mcq_cavity_status(const mcq_ctx *);
+
+/* Number of library kernels launched so far (graph replays count every kernel node). */
+MCQ_API long long mcq_kernel_launches(const mcq_ctx *);
+
+/* Measurement hook: runs `steps` steps with CUDA events around every kernel (no graph) and
+ * writes the mean device time (ms) per launch of each MCQ_K_* class to kernel_ms[MCQ_NKCLASS]
+ * (0 for classes not launched) and launches per step to per_step[MCQ_NKCLASS] (may be NULL). */
+MCQ_API int mcq_profile_run(mcq_ctx *, double dt, long long steps, double *kernel_ms, int *per_step);
+
+/* Padded layout: out[0..5] = Lx, Ly, Lz (zero-padded FFT lengths), NKX = Lx/2+1 (x-spectrum
+ * columns), P (row pitch of the spectrum, complex elements), n_partials. */
+MCQ_API int mcq_debug_layout(const mcq_ctx *, long long out[6]);
+/* Real-space demag tensor octant, fp64 (6, Lz/2+1, Ly/2+1, Lx/2+1) in XX,YY,ZZ,XY,XZ,YZ
+ * order, for index offsets (i, j, k); zero where i >= nx, j >= ny or k >= nz. */
+MCQ_API int mcq_debug_tensor_octant(mcq_ctx *, double *out);
+/* Folded kernel spectrum, fp32 (6, Lz/2+1, Ly/2+1, P): Khat = -mu0 Ms/(Lx Ly Lz) DFT(N). */
+MCQ_API int mcq_debug_khat(mcq_ctx *, float *out);
+
+MCQ_API const char *mcq_last_error(const mcq_ctx *);
+MCQ_API void mcq_destroy(mcq_ctx *);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MCQ_H */

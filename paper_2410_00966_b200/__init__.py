@@ -1,0 +1,254 @@
+"""B200-native Mumax3-cQED hot path (arXiv 2410.00966): LLG + single damped cavity mode.
+
+Thin Python binding of the C ABI in ``include/mcq.h`` — the functions below carry the ABI's
+names and only marshal arguments (numpy host arrays, or integer device pointers such as
+``torch.Tensor.data_ptr()``).  All computation happens in ``libmcq.so`` (sm_100a CUDA).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import (lib, MCQError, mcq_aniso, mcq_dist, mcq_cavity_state, EXPORTED,  # noqa: F401
+                   TERM_ZEEMAN, TERM_EXCHANGE, TERM_ANIS, TERM_DEMAG, TERM_CAVITY, TERM_EXCITATION,
+                   TERM_ALL, NKCLASS, KCLASS_NAMES, K_YFWD, K_ZCONV, K_YINV, K_Y2D, K_UPDATE, K_CAVITY)
+
+__all__ = [n for n in EXPORTED] + ["Solver", "MCQError"]
+
+
+def _check(ctx, rc):
+    if rc != 0:
+        msg = lib.mcq_last_error(ctx)
+        raise MCQError(rc, msg.decode() if msg else "")
+
+
+def _vec(a, n=None, dtype=np.float32):
+    arr = np.ascontiguousarray(a, dtype=dtype).reshape(-1)
+    if n is not None and arr.size != n:
+        raise ValueError(f"expected {n} values, got {arr.size}")
+    return arr
+
+
+def _d3(v):
+    return (C.c_double * 3)(*[float(x) for x in v])
+
+
+# ---------------------------------------------------------------- ABI-named functions
+
+def mcq_create(grid, cell, Ms, Aex, alpha, K=None, dist=None):
+    h = C.c_void_p()
+    g = (C.c_int * 3)(*[int(x) for x in grid])
+    c = (C.c_double * 3)(*[float(x) for x in cell])
+    kp = None
+    if K:
+        k = mcq_aniso()
+        k.ku1 = float(K.get("ku1", 0.0))
+        k.u = _d3(K.get("u", (0, 0, 1)))
+        k.kc1 = float(K.get("kc1", 0.0))
+        k.c1 = _d3(K.get("c1", (1, 0, 0)))
+        k.c2 = _d3(K.get("c2", (0, 1, 0)))
+        kp = C.pointer(k)
+    dp = None
+    if dist is not None:
+        d = mcq_dist(int(dist.get("rank", 0)), int(dist.get("world", 1)), int(dist.get("device", -1)), None,
+                     dist.get("stream"))
+        dp = C.pointer(d)
+    rc = lib.mcq_create(C.byref(h), g, c, float(Ms), float(Aex), float(alpha), kp, dp)
+    if rc != 0:
+        raise MCQError(rc, "mcq_create failed (invalid arguments, no device or out of memory)")
+    return h
+
+
+def mcq_set_stream(ctx, stream):
+    _check(ctx, lib.mcq_set_stream(ctx, C.c_void_p(stream) if stream else None))
+
+
+def mcq_set_geometry(ctx, mask):
+    if mask is None:
+        _check(ctx, lib.mcq_set_geometry(ctx, None))
+        return
+    m = np.ascontiguousarray(mask, dtype=np.uint8).reshape(-1)
+    _check(ctx, lib.mcq_set_geometry(ctx, m.ctypes.data))
+
+
+def mcq_set_m(ctx, m):
+    a = _vec(m)
+    _check(ctx, lib.mcq_set_m(ctx, a.ctypes.data))
+
+
+def mcq_set_m_device(ctx, dptr):
+    _check(ctx, lib.mcq_set_m_device(ctx, C.c_void_p(int(dptr))))
+
+
+def mcq_set_bext(ctx, B):
+    _check(ctx, lib.mcq_set_bext(ctx, _d3(B)))
+
+
+def mcq_set_brms(ctx, map=None, uniform=(0.0, 0.0, 0.0)):
+    if map is not None:
+        a = _vec(map)
+        _check(ctx, lib.mcq_set_brms(ctx, a.ctypes.data, _d3(uniform)))
+    else:
+        _check(ctx, lib.mcq_set_brms(ctx, None, _d3(uniform)))
+
+
+def mcq_set_cavity(ctx, f_c, kappa, x0=0.0, p0=0.0):
+    _check(ctx, lib.mcq_set_cavity(ctx, float(f_c), float(kappa), float(x0), float(p0)))
+
+
+def mcq_set_excitation(ctx, amplitude, omega_cut):
+    _check(ctx, lib.mcq_set_excitation(ctx, float(amplitude), float(omega_cut)))
+
+
+def mcq_reset_memory(ctx):
+    _check(ctx, lib.mcq_reset_memory(ctx))
+
+
+def mcq_relax(ctx, dt, torque_tol, max_steps):
+    n = C.c_longlong(0)
+    _check(ctx, lib.mcq_relax(ctx, float(dt), float(torque_tol), int(max_steps), C.byref(n)))
+    return n.value
+
+
+def mcq_run(ctx, dt, steps):
+    _check(ctx, lib.mcq_run(ctx, float(dt), int(steps)))
+
+
+def mcq_synchronize(ctx):
+    _check(ctx, lib.mcq_synchronize(ctx))
+
+
+def mcq_get_m(ctx, n_cells, out=None):
+    out = np.empty(3 * n_cells, np.float32) if out is None else out
+    _check(ctx, lib.mcq_get_m(ctx, out.ctypes.data))
+    return out.reshape(n_cells, 3)
+
+
+def mcq_get_m_device(ctx, dptr):
+    _check(ctx, lib.mcq_get_m_device(ctx, C.c_void_p(int(dptr))))
+
+
+def mcq_get_field(ctx, n_cells, terms=TERM_ALL):
+    out = np.empty(3 * n_cells, np.float32)
+    _check(ctx, lib.mcq_get_field(ctx, out.ctypes.data, C.c_uint(terms)))
+    return out.reshape(n_cells, 3)
+
+
+def mcq_get_cavity(ctx):
+    s = mcq_cavity_state()
+    _check(ctx, lib.mcq_get_cavity(ctx, C.byref(s)))
+    return s.as_dict()
+
+
+def mcq_set_cavity_state(ctx, state):
+    s = mcq_cavity_state()
+    s.t = float(state["t"])
+    s.re_alpha = float(state["re_alpha"])
+    s.im_alpha = float(state["im_alpha"])
+    s.step = int(state.get("step", 0))
+    _check(ctx, lib.mcq_set_cavity_state(ctx, C.byref(s)))
+
+
+def mcq_cavity_status(ctx):
+    rc = lib.mcq_cavity_status(ctx)
+    if rc < 0:
+        _check(ctx, rc)
+    return rc
+
+
+def mcq_kernel_launches(ctx):
+    return int(lib.mcq_kernel_launches(ctx))
+
+
+def mcq_profile_run(ctx, dt, steps):
+    ms = (C.c_double * NKCLASS)()
+    per = (C.c_int * NKCLASS)()
+    _check(ctx, lib.mcq_profile_run(ctx, float(dt), int(steps), ms, per))
+    return {KCLASS_NAMES[k]: (ms[k], per[k]) for k in range(NKCLASS)}
+
+
+def mcq_debug_layout(ctx):
+    out = (C.c_longlong * 6)()
+    _check(ctx, lib.mcq_debug_layout(ctx, out))
+    return dict(zip(("Lx", "Ly", "Lz", "NKX", "P", "n_partials"), list(out)))
+
+
+def mcq_debug_tensor_octant(ctx):
+    L = mcq_debug_layout(ctx)
+    shape = (6, L["Lz"] // 2 + 1, L["Ly"] // 2 + 1, L["Lx"] // 2 + 1)
+    out = np.empty(shape, np.float64)
+    _check(ctx, lib.mcq_debug_tensor_octant(ctx, out.ctypes.data))
+    return out
+
+
+def mcq_debug_khat(ctx):
+    L = mcq_debug_layout(ctx)
+    shape = (6, L["Lz"] // 2 + 1, L["Ly"] // 2 + 1, L["P"])
+    out = np.empty(shape, np.float32)
+    _check(ctx, lib.mcq_debug_khat(ctx, out.ctypes.data))
+    return out[..., :L["NKX"]]
+
+
+def mcq_last_error(ctx):
+    return lib.mcq_last_error(ctx).decode()
+
+
+def mcq_destroy(ctx):
+    lib.mcq_destroy(ctx)
+
+
+# ---------------------------------------------------------------- convenience wrapper
+
+class Solver:
+    """Owns one context; methods forward to the ABI functions above."""
+
+    def __init__(self, grid, cell, Ms, Aex, alpha, aniso=None, stream=None):
+        self.grid = tuple(int(g) for g in grid)
+        self.n = self.grid[0] * self.grid[1] * self.grid[2]
+        self.ctx = mcq_create(grid, cell, Ms, Aex, alpha, aniso, {"stream": stream} if stream else None)
+
+    @classmethod
+    def from_config(cls, cfg, stream=None, set_state=True):
+        s = cls(cfg.grid, cfg.cell, cfg.Ms, cfg.Aex, cfg.alpha, cfg.aniso, stream)
+        if cfg.mask is not None:
+            mcq_set_geometry(s.ctx, cfg.mask)
+        mcq_set_bext(s.ctx, cfg.bext)
+        mcq_set_brms(s.ctx, cfg.brms_map, cfg.brms_uniform)
+        mcq_set_cavity(s.ctx, cfg.f_c, cfg.kappa, cfg.x0, cfg.p0)
+        mcq_set_excitation(s.ctx, cfg.exc_amp, cfg.exc_omega)
+        if set_state:
+            mcq_set_m(s.ctx, cfg.m0)
+        return s
+
+    def set_m(self, m):
+        mcq_set_m(self.ctx, m)
+
+    def run(self, dt, steps):
+        mcq_run(self.ctx, dt, steps)
+
+    def relax(self, dt, tol, max_steps):
+        return mcq_relax(self.ctx, dt, tol, max_steps)
+
+    def m(self):
+        return mcq_get_m(self.ctx, self.n)
+
+    def field(self, terms=TERM_ALL):
+        return mcq_get_field(self.ctx, self.n, terms)
+
+    def cavity(self):
+        return mcq_get_cavity(self.ctx)
+
+    def sync(self):
+        mcq_synchronize(self.ctx)
+
+    def close(self):
+        if getattr(self, "ctx", None) is not None:
+            mcq_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,99 @@
+// common.cuh — shared device-side structures of the mcq library (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace mcq {
+
+constexpr double kGamma = 1.7595e11;             // rad s^-1 T^-1 (reading C8)
+constexpr double kMu0 = 4e-7 * 3.14159265358979323846;
+constexpr double kHbar = 1.05457182e-34;         // J s
+constexpr int kTwMax = 1024;                     // global twiddle table length (max FFT length)
+
+// Sizes of one context's padded spectral layout.
+struct Dims {
+  int nx, ny, nz;     // grid
+  int Lx, Ly, Lz;     // zero-padded FFT lengths (next pow2 >= 2n; 1 if n == 1)
+  int N2;             // Lx / 2: complex length of the packed real x-transform
+  int NKX;            // Lx / 2 + 1: x-spectrum columns (Hermitian half)
+  int P;              // row pitch of the spectra (complex elements), >= NKX
+  long long N;        // nx * ny * nz
+};
+
+// Cavity state on the device (fp64), advanced once per step by k_cavity (a13).
+struct CavState {
+  double re, im;      // alpha_n
+  double t;           // cavity clock t_n
+  double W;           // overlap of the last completed step
+  long long step;
+  float gc[4];        // Gamma(t_n + c_s dt) = 2 Re(e^{-(kappa+iw) c_s dt} alpha_n), s = 0..3
+  float ge[4];        // a sinc(w_cut (t_n + c_s dt))
+};
+
+// Scalars the cavity kernels need (host precomputed in fp64 for a given dt).
+struct CavParams {
+  double ec_re[3], ec_im[3];  // e^{-(kappa + i w) c dt} for c = 0, 1/2, 1
+  double vc_over_hbar;        // V_c / hbar
+  double Ms;
+  double dt;
+  double exc_amp, exc_omega;
+  int cav_on;                 // B_rms nonzero (C14)
+};
+
+enum UpdateMode : int { MODE_LLG = 0, MODE_RELAX = 1, MODE_FIELD = 2, MODE_MAXTORQUE = 3, MODE_X0 = 4 };
+
+// Arguments of the fused update kernel K-U.
+struct UpdateArgs {
+  Dims d;
+  int stage;          // 1..4 (MODE_LLG / MODE_RELAX)
+  int mode;
+  unsigned terms;     // MCQ_TERM_* mask
+  const float* mS;    // stage state (SoA [3][N])
+  const float* mN;    // m_n (SoA)
+  float* mOut;        // m_{s+1} (stages 1-3) or m_{n+1} (stage 4, may alias mN)
+  float* acc;         // RK4 accumulator k1 + 2k2 + 2k3 (SoA)
+  float2* X;          // x-spectrum rows [3][nz][ny][P]: demag in, FFT(m_{s+1}) out
+  const float* brms;  // SoA map or nullptr
+  float brms_u[3];
+  float bext[3];
+  float ex[3];        // 2A / (Ms d_axis^2)
+  float ku, u[3];     // 2 K_u1 / Ms, axis
+  float kc, c1[3], c2[3], c3[3];  // 2 K_c1 / Ms, axes
+  float gl;           // gamma / (1 + alpha^2)
+  float alpha;
+  float gamma;
+  float h;            // c_{s+1} dt for stages 1..3
+  float dt6;          // dt / 6
+  const CavState* cav;
+  double* partials;   // per-CTA overlap partials (stage 4)
+  float* bout;        // MODE_FIELD output (SoA)
+  unsigned* maxbits;  // MODE_MAXTORQUE output (float bits, >= 0)
+  int demag;          // run the x-C2R demag phase
+};
+
+// ---------------------------------------------------------------- launchers
+// passes.cu
+void configure_pass_kernels();
+void launch_yfwd(const Dims& d, const float2* X, float2* Y, const float2* tw, cudaStream_t s);
+void launch_zconv(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t s);
+void launch_yinv(const Dims& d, const float2* Y, float2* X, const float2* tw, cudaStream_t s);
+void launch_y2d(const Dims& d, float2* X, const float* khat, const float2* tw, cudaStream_t s);
+// update.cu
+void configure_update_kernels();
+void launch_update(const UpdateArgs& a, const float2* tw, cudaStream_t s);
+int update_grid_blocks(const Dims& d);
+void launch_cavity(const CavParams& p, CavState* st, const double* partials, int n, cudaStream_t s);
+void launch_cav_prepare(const CavParams& p, CavState* st, cudaStream_t s);
+void launch_aos_to_soa(const float* in, float* out, const uint8_t* mask, long long N, int* bad,
+                       cudaStream_t s);
+void launch_soa_to_aos(const float* in, float* out, long long N, cudaStream_t s);
+void launch_deinterleave(const float* in, float* out, long long N, cudaStream_t s);
+// tensor.cu
+void launch_tensor_octant(double* oct, const Dims& d, double dx, double dy, double dz,
+                          cudaStream_t s);
+void launch_axis_transform(const double* in, double* out, int m0, int m1, int m2, int axis,
+                           const double* Tcos, const double* Tsin, cudaStream_t s);
+void launch_khat_finalize(const double* in, float* khat, const Dims& d, double scale,
+                          cudaStream_t s);
+
+}  // namespace mcq

@@ -1,0 +1,430 @@
+// update.cu — the fused per-stage update kernel K-U, the cavity kernel K-CAV and layout helpers.
+//
+// K-U (one launch per RK4 stage), one CTA = RY full x-rows at one z:
+//   A. demag x-C2R: rows of the y/z-processed spectrum X'[3][z][y][0..Lx/2] -> real B_demag
+//      rows in shared memory (packed half-length complex IFFT, reading C11);
+//   B. per cell: B' = demag + B_ext + exchange (6-neighbour, C9) + anisotropy (C10)
+//      + B_rms (Gamma(t_s) + a sinc(w t_s)) (eq:bcav P:239), LLG torque (eq:llg P:184),
+//      RK4 stage combine + renormalisation (C1, C2); at stage 4 the overlap
+//      W partial = sum B_rms . m_{n+1} in fp64;
+//   C. x-R2C of m_{s+1} rows -> X[3][z][y][0..Lx/2] for the next stage's y/z passes.
+// Ms is folded into the kernel spectrum, so the transforms act on m directly.
+#include "common.cuh"
+#include "fft.cuh"
+#include "../../include/mcq.h"
+
+namespace mcq {
+
+template <int N2>
+struct UCfg {
+  static constexpr int RY = (1024 / N2) < 1 ? 1 : ((1024 / N2) > 16 ? 16 : (1024 / N2));
+  static constexpr int E = N2 < 16 ? N2 : 16;
+  static constexpr int NT = 3 * RY * N2 / E;
+};
+
+__device__ __forceinline__ float3 cross3(float3 a, float3 b) {
+  return make_float3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ float dot3(float3 a, float3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ float3 nrm3(float3 v) {
+  const float n2 = dot3(v, v);
+  if (n2 > 0.f) {
+    const float r = rsqrtf(n2);
+    return make_float3(v.x * r, v.y * r, v.z * r);
+  }
+  return make_float3(0.f, 0.f, 0.f);
+}
+__device__ __forceinline__ float3 ld3(const float* __restrict__ p, long long N, long long i) {
+  return make_float3(__ldg(p + i), __ldg(p + N + i), __ldg(p + 2 * N + i));
+}
+
+template <int N2>
+__global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const float2* __restrict__ gtw) {
+  constexpr int RY = UCfg<N2>::RY, NT = UCfg<N2>::NT, LX = 2 * N2;
+  constexpr int NL = 3 * RY;  // lines: comp * RY + yl
+  using Lay = RowLayout<N2>;
+  extern __shared__ float2 sm[];
+  float2* tw = sm;        // w_Lx^m, m < Lx
+  float2* s = sm + LX;
+  __shared__ double red[32];
+  __shared__ float redf[32];
+
+  const Dims& d = a.d;
+  const int y0 = blockIdx.x * RY, z = blockIdx.y;
+  const int nrow = min(RY, d.ny - y0);
+  const long long N = d.N;
+  for (int m = threadIdx.x; m < LX; m += NT) tw[m] = gtw[m * (kTwMax / LX)];
+
+  // ---------------- A: demag rows (x-C2R) ----------------
+  const bool use_demag = a.demag && (a.terms & MCQ_TERM_DEMAG) && a.mode != MODE_X0;
+  if (use_demag) {
+    __syncthreads();  // tw ready
+    for (int e = threadIdx.x; e < NL * N2; e += NT) {
+      const int line = e / N2, k = e - line * N2;
+      const int comp = line / RY, yl = line - comp * RY;
+      float2 zk = make_float2(0.f, 0.f);
+      if (yl < nrow) {
+        const float2* row = a.X + ((size_t)(comp * d.nz + z) * d.ny + y0 + yl) * d.P;
+        const float2 xk = row[k], xn = cconj(row[N2 - k]);
+        const float2 ev = cadd(xk, xn);
+        const float2 od = cmul(csub(xk, xn), cconj(tw[k]));  // * w^{-k}
+        zk = make_float2(ev.x - od.y, ev.y + od.x);           // E + i O
+      }
+      s[Lay::addr(k, line)] = zk;
+    }
+    __syncthreads();
+    block_fft<N2, NL, NT, true, Lay, 2>(s, tw);
+  } else {
+    __syncthreads();
+  }
+
+  // ---------------- B: per-cell fields, torque, RK4 ----------------
+  float* sf = reinterpret_cast<float*>(s);
+  const int stage = a.stage;
+  float gc = 0.f, ge = 0.f;
+  if (a.mode == MODE_LLG || a.mode == MODE_FIELD) {
+    const int si = (a.mode == MODE_FIELD) ? 0 : stage - 1;
+    gc = (a.terms & MCQ_TERM_CAVITY) ? a.cav->gc[si] : 0.f;
+    ge = (a.terms & MCQ_TERM_EXCITATION) ? a.cav->ge[si] : 0.f;
+  }
+  const float gsum = gc + ge;
+  double wacc = 0.0;
+  float tmax = 0.f;
+  const int ncell = nrow * d.nx;
+  for (int e = threadIdx.x; e < ncell; e += NT) {
+    const int yl = e / d.nx, x = e - yl * d.nx, y = y0 + yl;
+    const long long idx = x + (long long)d.nx * (y + (long long)d.ny * z);
+    const float3 m = ld3(a.mS, N, idx);
+    float3 out = m;  // value that goes into the x-R2C rows
+    if (a.mode != MODE_X0) {
+      const bool mag = dot3(m, m) > 0.f;
+      float3 B = make_float3(0.f, 0.f, 0.f);
+      if (mag) {
+        if (use_demag) {
+          const int n = x >> 1, lo = x & 1;
+          B.x = sf[2 * Lay::addr(n, 0 * RY + yl) + lo];
+          B.y = sf[2 * Lay::addr(n, 1 * RY + yl) + lo];
+          B.z = sf[2 * Lay::addr(n, 2 * RY + yl) + lo];
+        }
+        if (a.terms & MCQ_TERM_ZEEMAN) {
+          B.x += a.bext[0];
+          B.y += a.bext[1];
+          B.z += a.bext[2];
+        }
+        if (a.terms & MCQ_TERM_EXCHANGE) {
+          float3 acc = make_float3(0.f, 0.f, 0.f);
+#define MCQ_NB(COND, OFF, COEF)                                      \
+  if (COND) {                                                        \
+    const float3 mj = ld3(a.mS, N, idx + (OFF));                     \
+    if (dot3(mj, mj) > 0.f) {                                        \
+      acc.x += (COEF) * (mj.x - m.x);                                \
+      acc.y += (COEF) * (mj.y - m.y);                                \
+      acc.z += (COEF) * (mj.z - m.z);                                \
+    }                                                                \
+  }
+          MCQ_NB(x > 0, -1, a.ex[0])
+          MCQ_NB(x < d.nx - 1, +1, a.ex[0])
+          MCQ_NB(y > 0, -(long long)d.nx, a.ex[1])
+          MCQ_NB(y < d.ny - 1, +(long long)d.nx, a.ex[1])
+          MCQ_NB(z > 0, -(long long)d.nx * d.ny, a.ex[2])
+          MCQ_NB(z < d.nz - 1, +(long long)d.nx * d.ny, a.ex[2])
+#undef MCQ_NB
+          B.x += acc.x;
+          B.y += acc.y;
+          B.z += acc.z;
+        }
+        if (a.terms & MCQ_TERM_ANIS) {
+          if (a.ku != 0.f) {
+            const float mu = m.x * a.u[0] + m.y * a.u[1] + m.z * a.u[2];
+            B.x += a.ku * mu * a.u[0];
+            B.y += a.ku * mu * a.u[1];
+            B.z += a.ku * mu * a.u[2];
+          }
+          if (a.kc != 0.f) {
+            const float m1 = m.x * a.c1[0] + m.y * a.c1[1] + m.z * a.c1[2];
+            const float m2 = m.x * a.c2[0] + m.y * a.c2[1] + m.z * a.c2[2];
+            const float m3 = m.x * a.c3[0] + m.y * a.c3[1] + m.z * a.c3[2];
+            const float f1 = -a.kc * m1 * (m2 * m2 + m3 * m3);
+            const float f2 = -a.kc * m2 * (m1 * m1 + m3 * m3);
+            const float f3 = -a.kc * m3 * (m1 * m1 + m2 * m2);
+            B.x += f1 * a.c1[0] + f2 * a.c2[0] + f3 * a.c3[0];
+            B.y += f1 * a.c1[1] + f2 * a.c2[1] + f3 * a.c3[1];
+            B.z += f1 * a.c1[2] + f2 * a.c2[2] + f3 * a.c3[2];
+          }
+        }
+        if (gsum != 0.f) {
+          const float3 br = a.brms ? ld3(a.brms, N, idx) : make_float3(a.brms_u[0], a.brms_u[1], a.brms_u[2]);
+          B.x += br.x * gsum;
+          B.y += br.y * gsum;
+          B.z += br.z * gsum;
+        }
+      }
+      if (a.mode == MODE_FIELD) {
+        a.bout[idx] = B.x;
+        a.bout[N + idx] = B.y;
+        a.bout[2 * N + idx] = B.z;
+        continue;
+      }
+      const float3 mxB = cross3(m, B);
+      if (a.mode == MODE_MAXTORQUE) {
+        tmax = fmaxf(tmax, sqrtf(dot3(mxB, mxB)));
+        continue;
+      }
+      float3 k;
+      const float3 mmxB = cross3(m, mxB);
+      if (a.mode == MODE_LLG) {
+        k = make_float3(-a.gl * (mxB.x + a.alpha * mmxB.x), -a.gl * (mxB.y + a.alpha * mmxB.y),
+                        -a.gl * (mxB.z + a.alpha * mmxB.z));
+      } else {  // MODE_RELAX: -gamma m x (m x B)
+        k = make_float3(-a.gamma * mmxB.x, -a.gamma * mmxB.y, -a.gamma * mmxB.z);
+      }
+      const float3 mn = (stage == 1) ? m : ld3(a.mN, N, idx);
+      if (stage < 4) {
+        float3 acc;
+        if (stage == 1) {
+          acc = k;
+        } else {
+          const float3 ap = ld3(a.acc, N, idx);
+          acc = make_float3(ap.x + 2.f * k.x, ap.y + 2.f * k.y, ap.z + 2.f * k.z);
+        }
+        a.acc[idx] = acc.x;
+        a.acc[N + idx] = acc.y;
+        a.acc[2 * N + idx] = acc.z;
+        out = nrm3(make_float3(mn.x + a.h * k.x, mn.y + a.h * k.y, mn.z + a.h * k.z));
+      } else {
+        const float3 ap = ld3(a.acc, N, idx);
+        out = nrm3(make_float3(mn.x + a.dt6 * (ap.x + k.x), mn.y + a.dt6 * (ap.y + k.y),
+                               mn.z + a.dt6 * (ap.z + k.z)));
+        if (a.mode == MODE_LLG) {
+          const float3 br = a.brms ? ld3(a.brms, N, idx) : make_float3(a.brms_u[0], a.brms_u[1], a.brms_u[2]);
+          wacc += (double)(br.x * out.x) + (double)(br.y * out.y) + (double)(br.z * out.z);
+        }
+      }
+      a.mOut[idx] = out.x;
+      a.mOut[N + idx] = out.y;
+      a.mOut[2 * N + idx] = out.z;
+    }
+    // stash m_{s+1} (or m for MODE_X0) as real rows for the x-R2C
+    const int n = x >> 1, lo = x & 1;
+    sf[2 * Lay::addr(n, 0 * RY + yl) + lo] = out.x;
+    sf[2 * Lay::addr(n, 1 * RY + yl) + lo] = out.y;
+    sf[2 * Lay::addr(n, 2 * RY + yl) + lo] = out.z;
+  }
+
+  // ---------------- reductions ----------------
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (NT + 31) / 32;
+  if (a.mode == MODE_LLG && stage == 4) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wacc += __shfl_down_sync(0xffffffffu, wacc, o);
+    if (lane == 0) red[warp] = wacc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < nw; ++w) t += red[w];
+      a.partials[blockIdx.y * gridDim.x + blockIdx.x] = t;
+    }
+  }
+  if (a.mode == MODE_MAXTORQUE) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_down_sync(0xffffffffu, tmax, o));
+    if (lane == 0) redf[warp] = tmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float t = 0.f;
+      for (int w = 0; w < nw; ++w) t = fmaxf(t, redf[w]);
+      atomicMax(a.maxbits, __float_as_uint(t));
+    }
+    return;
+  }
+  if (a.mode == MODE_FIELD) return;
+
+  // ---------------- C: x-R2C of the new rows ----------------
+  // zero the padding: real positions x in [nx, Lx) of each valid row
+  for (int e = threadIdx.x; e < NL * (LX - d.nx); e += NT) {
+    const int line = e / (LX - d.nx), x = d.nx + (e - line * (LX - d.nx));
+    sf[2 * Lay::addr(x >> 1, line) + (x & 1)] = 0.f;
+  }
+  if (nrow < RY) {  // ragged tail rows: keep them finite (never stored)
+    for (int e = threadIdx.x; e < NL * d.nx; e += NT) {
+      const int line = e / d.nx, x = e - line * d.nx;
+      if (line % RY >= nrow) sf[2 * Lay::addr(x >> 1, line) + (x & 1)] = 0.f;
+    }
+  }
+  __syncthreads();
+  block_fft<N2, NL, NT, false, Lay, 2>(s, tw);
+  for (int e = threadIdx.x; e < NL * (N2 + 1); e += NT) {
+    const int line = e / (N2 + 1), k = e - line * (N2 + 1);
+    const int comp = line / RY, yl = line - comp * RY;
+    if (yl >= nrow) continue;
+    const float2 zk = s[Lay::addr(k & (N2 - 1), line)];
+    const float2 zn = cconj(s[Lay::addr((N2 - k) & (N2 - 1), line)]);
+    const float2 ev = cadd(zk, zn);                         // 2 A_k
+    const float2 df = csub(zk, zn);                         // 2 i B_k
+    const float2 wd = cmul(tw[k], df);                      // w^k (Z_k - conj Z_{N-k})
+    // X_k = (Z_k + conj Z_{N-k})/2 - i/2 w^k (Z_k - conj Z_{N-k})
+    const float2 xk = make_float2(0.5f * (ev.x + wd.y), 0.5f * (ev.y - wd.x));
+    a.X[((size_t)(comp * d.nz + z) * d.ny + y0 + yl) * d.P + k] = xk;
+  }
+}
+
+int update_grid_blocks(const Dims& d) {
+  int ry = 1;
+  switch (d.N2) {
+#define C_(n) case n: ry = UCfg<n>::RY; break;
+    C_(2) C_(4) C_(8) C_(16) C_(32) C_(64) C_(128) C_(256) C_(512)
+#undef C_
+    default: break;
+  }
+  return ((d.ny + ry - 1) / ry) * d.nz;
+}
+
+#define MCQ_DISPATCH_N2(Nv, ...)                        \
+  switch (Nv) {                                          \
+    case 2: { constexpr int N2 = 2; __VA_ARGS__; } break;       \
+    case 4: { constexpr int N2 = 4; __VA_ARGS__; } break;       \
+    case 8: { constexpr int N2 = 8; __VA_ARGS__; } break;       \
+    case 16: { constexpr int N2 = 16; __VA_ARGS__; } break;     \
+    case 32: { constexpr int N2 = 32; __VA_ARGS__; } break;     \
+    case 64: { constexpr int N2 = 64; __VA_ARGS__; } break;     \
+    case 128: { constexpr int N2 = 128; __VA_ARGS__; } break;   \
+    case 256: { constexpr int N2 = 256; __VA_ARGS__; } break;   \
+    case 512: { constexpr int N2 = 512; __VA_ARGS__; } break;   \
+    default: break;                                      \
+  }
+
+template <int N2>
+static size_t update_smem() {
+  return (size_t)(2 * N2 + RowLayout<N2>::size(3 * UCfg<N2>::RY)) * sizeof(float2);
+}
+
+void launch_update(const UpdateArgs& a, const float2* tw, cudaStream_t st) {
+  MCQ_DISPATCH_N2(a.d.N2, {
+    using Cf = UCfg<N2>;
+    dim3 grid((a.d.ny + Cf::RY - 1) / Cf::RY, a.d.nz);
+    k_update<N2><<<grid, Cf::NT, update_smem<N2>(), st>>>(a, tw);
+  })
+}
+
+void configure_update_kernels() {
+  for (int n = 2; n <= 512; n *= 2) {
+    MCQ_DISPATCH_N2(n, {
+      cudaFuncSetAttribute(k_update<N2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)update_smem<N2>());
+    })
+  }
+}
+
+// ---------------------------------------------------------------- K-CAV
+// Stage factors for the step that starts at (alpha, t): Gamma(t + c dt) = 2 Re(e_c alpha)
+// (P:343 with S_n, C_n frozen, reading C3/C5), excitation a sinc(w_cut (t + c dt)) (C13).
+__device__ void cav_prepare(const CavParams& p, CavState* st) {
+  const double c[4] = {0.0, 0.5, 0.5, 1.0};
+  const int ci[4] = {0, 1, 1, 2};
+  for (int s = 0; s < 4; ++s) {
+    const double er = p.ec_re[ci[s]], ei = p.ec_im[ci[s]];
+    const double g = 2.0 * (er * st->re - ei * st->im);
+    const double x = p.exc_omega * (st->t + c[s] * p.dt);
+    const double sc = (x == 0.0) ? 1.0 : sin(x) / x;
+    st->gc[s] = (float)(p.cav_on ? g : 0.0);
+    st->ge[s] = (float)(p.exc_amp * sc);
+  }
+}
+
+__global__ void k_cav_prepare(CavParams p, CavState* st) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) cav_prepare(p, st);
+}
+
+// Fixed-order reduction of the per-CTA partials (deterministic), then
+// alpha_{n+1} = e^{-(kappa + i w) dt} alpha_n + i (V_c/hbar) W_{n+1} dt, t += dt (a13).
+__global__ void __launch_bounds__(1024) k_cavity(CavParams p, CavState* st, const double* __restrict__ partials,
+                                                 int n) {
+  __shared__ double red[1024];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += 1024) s += partials[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double W = p.cav_on ? p.Ms * red[0] : 0.0;
+    const double er = p.ec_re[2], ei = p.ec_im[2];
+    const double re = er * st->re - ei * st->im;
+    const double im = er * st->im + ei * st->re + p.vc_over_hbar * W * p.dt;
+    st->re = re;
+    st->im = im;
+    st->t += p.dt;
+    st->W = W;
+    st->step += 1;
+    cav_prepare(p, st);
+  }
+}
+
+void launch_cavity(const CavParams& p, CavState* st, const double* partials, int n, cudaStream_t s) {
+  k_cavity<<<1, 1024, 0, s>>>(p, st, partials, n);
+}
+
+void launch_cav_prepare(const CavParams& p, CavState* st, cudaStream_t s) {
+  k_cav_prepare<<<1, 32, 0, s>>>(p, st);
+}
+
+// ---------------------------------------------------------------- K-IO
+// interleaved (AoS) -> SoA, normalise, apply the geometry mask; *bad counts magnetic cells
+// with a zero vector (EINVAL).
+__global__ void k_aos_to_soa(const float* __restrict__ in, float* __restrict__ out, const uint8_t* __restrict__ mask,
+                             long long N, int* bad) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+    float3 v = make_float3(in[3 * i], in[3 * i + 1], in[3 * i + 2]);
+    const bool mag = mask ? (mask[i] != 0) : true;
+    if (!mag) {
+      v = make_float3(0.f, 0.f, 0.f);
+    } else {
+      const float n2 = dot3(v, v);
+      if (!(n2 > 0.f) || !isfinite(n2)) {
+        atomicAdd(bad, 1);
+        v = make_float3(0.f, 0.f, 0.f);
+      } else {
+        const float r = 1.0f / sqrtf(n2);
+        v = make_float3(v.x * r, v.y * r, v.z * r);
+      }
+    }
+    out[i] = v.x;
+    out[N + i] = v.y;
+    out[2 * N + i] = v.z;
+  }
+}
+
+__global__ void k_soa_to_aos(const float* __restrict__ in, float* __restrict__ out, long long N) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+    out[3 * i] = in[i];
+    out[3 * i + 1] = in[N + i];
+    out[3 * i + 2] = in[2 * N + i];
+  }
+}
+
+__global__ void k_deinterleave(const float* __restrict__ in, float* __restrict__ out, long long N) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+    out[i] = in[3 * i];
+    out[N + i] = in[3 * i + 1];
+    out[2 * N + i] = in[3 * i + 2];
+  }
+}
+
+static int io_blocks(long long N) {
+  long long b = (N + 255) / 256;
+  return (int)(b < 148 * 16 ? (b < 1 ? 1 : b) : 148 * 16);
+}
+
+void launch_aos_to_soa(const float* in, float* out, const uint8_t* mask, long long N, int* bad, cudaStream_t s) {
+  k_aos_to_soa<<<io_blocks(N), 256, 0, s>>>(in, out, mask, N, bad);
+}
+
+void launch_soa_to_aos(const float* in, float* out, long long N, cudaStream_t s) {
+  k_soa_to_aos<<<io_blocks(N), 256, 0, s>>>(in, out, N);
+}
+
+void launch_deinterleave(const float* in, float* out, long long N, cudaStream_t s) {
+  k_deinterleave<<<io_blocks(N), 256, 0, s>>>(in, out, N);
+}
+
+}  // namespace mcq
