@@ -108,19 +108,25 @@ def step_alg_bytes(L, grid, has_map):
 
 
 # ---------------------------------------------------------------- oracle timing
-def cpu_baseline(cfg, sample_steps=1):
-    """Oracle (fp64 NumPy, as it stands) on the same workload: `sample_steps` full RK4 steps."""
-    from tests.helpers import oracle_from
+def cpu_baseline(cfg, rhs_evals=1):
+    """Oracle (fp64 NumPy, as it stands) on the same workload, bounded sample: `rhs_evals`
+    right-hand-side evaluations (one RK4 step = 4), scaled to cell-updates/s = N * evals/4 / t."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from helpers import oracle_from
     t0 = time.perf_counter()
     ref = oracle_from(cfg)
-    ref.rhs(ref.m, 0.0)            # builds the tensor + its DFT (setup, untimed)
+    ref.octant()
+    if ref.demag_mode == "dft":
+        from oracle import tensor as T
+        ref._padded = T.padded_tensor(ref.grid, ref.cell, ref.octant())
     setup = time.perf_counter() - t0
     t0 = time.perf_counter()
-    ref.run(cfg.dt, sample_steps)
+    for _ in range(rhs_evals):
+        ref.rhs(ref.m, 0.0)
     dt = time.perf_counter() - t0
-    return {"value": cfg.n * sample_steps / dt, "unit": "cell-updates/s", "cores": len(os.sched_getaffinity(0)),
-            "kind": "oracle", "sample": f"{sample_steps} full RK4 step(s) of {cfg.name} {cfg.grid} "
-            f"(direct-DFT demag, fp64); setup {setup:.1f} s untimed", "seconds": dt}
+    return {"value": cfg.n * rhs_evals / 4 / dt, "unit": "cell-updates/s", "cores": len(os.sched_getaffinity(0)),
+            "kind": "oracle", "sample": f"{rhs_evals} RHS evaluation(s) (1/4 RK4 step each) of {cfg.name} "
+            f"{tuple(cfg.grid)}, direct-DFT demag in fp64; tensor setup {setup:.1f} s untimed", "seconds": dt}
 
 
 def run_reference(args):
@@ -129,7 +135,8 @@ def run_reference(args):
     if rank != 0:
         return
     from synth import make_config
-    from tests.helpers import oracle_from
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from helpers import oracle_from
     full = make_config(args.config)
     sample_grid = {0: (64, 64, 1), 1: (32, 32, 32), 2: (32, 32, 32), 3: (64, 64, 8), 4: (64, 64, 32)}[args.config]
     cfg = make_config(args.config, grid=sample_grid) if args.config in (1, 2, 3) else full
@@ -192,7 +199,8 @@ def main():
         if nrm > 0:
             pts = bias_sweep(nrm, n=world, rel=0.1) if world > 1 else [nrm]
             cfg.bext = tuple(b / nrm * pts[rank])
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()          # a real stream: the library's kernels and our events share it
+    torch.cuda.set_stream(stream)
     solver = mcq.Solver.from_config(cfg, stream=stream.cuda_stream)
     if cfg.relax_first:
         solver.relax(cfg.dt * 0.5, 1e-3, 2000)

@@ -110,7 +110,9 @@ MCQ_API int mcq_set_stream(mcq_ctx *, void *stream);
  * Applies to subsequent mcq_set_m calls and zeroes m in vacuum now. */
 MCQ_API int mcq_set_geometry(mcq_ctx *, const unsigned char *mask);
 
-/* Magnetisation, 3N floats interleaved (host).  Normalised on entry; vacuum cells are set to 0.
+/* Magnetisation, 3N floats interleaved (host).  Normalised on entry (vectors already unit to
+ * within 1e-6 in |m|^2 are kept as given, so a state saved with mcq_get_m resumes bit-exactly);
+ * vacuum cells are set to 0.
  * EINVAL if a magnetic cell has a zero vector.  Does not touch the cavity state. */
 MCQ_API int mcq_set_m(mcq_ctx *, const float *m);
 /* Same from a device pointer (3N floats interleaved, device memory of this context's GPU). */

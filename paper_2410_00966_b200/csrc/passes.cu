@@ -7,49 +7,72 @@
 //                   symmetric 3x3 multiply by the real folded Khat, inverse along z, keep nz
 //   K-YI (k_yinv):  Y -> X, inverse along y, keep the first ny rows
 //   K-Y2D(k_y2d):   nz == 1: forward y, Khat multiply, inverse y in one pass, in place on X
-// Each CTA owns C adjacent kx columns (contiguous in memory, so every global access of a warp
-// is a contiguous C*8-byte segment) and the full padded line in shared memory.
+// A CTA owns C adjacent kx columns (a warp's global accesses are contiguous C*8-byte row
+// segments).  Lines are transformed with the register-resident FFT of regfft.cuh: data go
+// HBM -> registers -> (S-1 smem exchanges) -> registers -> HBM, and K-Z/K-Y2D multiply by Khat
+// in registers between the forward and the inverse transform.
 #include "common.cuh"
-#include "fft.cuh"
+#include "regfft.cuh"
 
 namespace mcq {
 
 template <int L>
-struct PassCfg {
-  static constexpr int C = L >= 512 ? 8 : 16;          // columns per CTA
-  static constexpr int E = L < 16 ? L : 16;            // complex values per thread
-  static constexpr int NT = L * C / E;                 // threads (single-component passes)
+struct PassCfg {  // single-line passes (K-Y, K-YI)
+  static constexpr int E = L < 16 ? L : 16;
+  static constexpr int TL = L / E;
+  static constexpr int C0 = 256 / TL;
+  static constexpr int C = C0 < 8 ? 8 : (C0 > 64 ? 64 : C0);
+  static constexpr int NT = C * TL;
+  static constexpr size_t SMEM = (size_t)(L + (TL > 1 ? L * C : 0)) * sizeof(float2);
+};
+
+template <int L>
+struct ZCfg {  // three-line passes with the Khat multiply (K-Z, K-Y2D)
+  static constexpr int E = L < 16 ? L : 16;
+  static constexpr int TL = L / E;
+  static constexpr int C0 = 128 / TL;
+  static constexpr int C = C0 < 4 ? 4 : (C0 > 64 ? 64 : C0);
+  static constexpr int NT = C * TL;
+  static constexpr size_t SMEM = (size_t)(L + (TL > 1 ? 3 * L * C : 0)) * sizeof(float2);
 };
 
 template <int L>
 __device__ __forceinline__ void load_tw(float2* tw, const float2* __restrict__ gtw, int nt) {
   for (int m = threadIdx.x; m < L; m += nt) tw[m] = gtw[m * (kTwMax / L)];
+  __syncthreads();
 }
+
+// shared-memory address of (line l, position pos) for column c: [l][pos][c]
+template <int L, int C>
+struct ColAddr {
+  int c;
+  __device__ __forceinline__ int operator()(int l, int pos) const { return (l * L + pos) * C + c; }
+};
 
 // ---------------------------------------------------------------- K-Y forward
 template <int L>
 __global__ void __launch_bounds__(PassCfg<L>::NT) k_yfwd(const float2* __restrict__ X, float2* __restrict__ Y,
                                                          Dims d, const float2* __restrict__ gtw) {
-  constexpr int C = PassCfg<L>::C, NT = PassCfg<L>::NT;
-  using Lay = ColLayout<L, C>;
+  using Cf = PassCfg<L>;
+  constexpr int E = Cf::E, TL = Cf::TL, C = Cf::C, NT = Cf::NT;
   extern __shared__ float2 sm[];
   float2* tw = sm;
-  float2* s = sm + L;
   load_tw<L>(tw, gtw, NT);
-  const int kx0 = blockIdx.x * C, z = blockIdx.y, comp = blockIdx.z;
-  const float2* src = X + ((size_t)(comp * d.nz + z) * d.ny) * d.P;
-  for (int e = threadIdx.x; e < L * C; e += NT) {
-    const int i = e / C, c = e - i * C, kx = kx0 + c;
-    float2 v = make_float2(0.f, 0.f);
-    if (i < d.ny && kx < d.NKX) v = src[(size_t)i * d.P + kx];
-    s[Lay::addr(i, c)] = v;
+  const int c = threadIdx.x % C, t = threadIdx.x / C;
+  const int kx = blockIdx.x * C + c, z = blockIdx.y, comp = blockIdx.z;
+  const bool ok = kx < d.NKX;
+  const float2* src = X + ((size_t)(comp * d.nz + z) * d.ny) * d.P + kx;
+  float2 v[1][E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const int p = t + TL * i;
+    v[0][i] = (ok && p < d.ny) ? src[(size_t)p * d.P] : make_float2(0.f, 0.f);
   }
-  __syncthreads();
-  block_fft<L, C, NT, false, Lay>(s, tw);
-  float2* dst = Y + ((size_t)(comp * d.nz + z) * L) * d.P;
-  for (int e = threadIdx.x; e < L * C; e += NT) {
-    const int i = e / C, c = e - i * C, kx = kx0 + c;
-    if (kx < d.NKX) dst[(size_t)i * d.P + kx] = s[Lay::addr(i, c)];
+  reg_fft<L, E, 1, false>(v, sm + L, ColAddr<L, C>{c}, tw, t);
+  if (ok) {
+    float2* dst = Y + ((size_t)(comp * d.nz + z) * L) * d.P + kx;
+#pragma unroll
+    for (int i = 0; i < E; ++i) dst[(size_t)(t + TL * i) * d.P] = v[0][i];
   }
 }
 
@@ -57,26 +80,26 @@ __global__ void __launch_bounds__(PassCfg<L>::NT) k_yfwd(const float2* __restric
 template <int L>
 __global__ void __launch_bounds__(PassCfg<L>::NT) k_yinv(const float2* __restrict__ Y, float2* __restrict__ X,
                                                          Dims d, const float2* __restrict__ gtw) {
-  constexpr int C = PassCfg<L>::C, NT = PassCfg<L>::NT;
-  using Lay = ColLayout<L, C>;
+  using Cf = PassCfg<L>;
+  constexpr int E = Cf::E, TL = Cf::TL, C = Cf::C, NT = Cf::NT;
   extern __shared__ float2 sm[];
   float2* tw = sm;
-  float2* s = sm + L;
   load_tw<L>(tw, gtw, NT);
-  const int kx0 = blockIdx.x * C, z = blockIdx.y, comp = blockIdx.z;
-  const float2* src = Y + ((size_t)(comp * d.nz + z) * L) * d.P;
-  for (int e = threadIdx.x; e < L * C; e += NT) {
-    const int i = e / C, c = e - i * C, kx = kx0 + c;
-    float2 v = make_float2(0.f, 0.f);
-    if (kx < d.NKX) v = src[(size_t)i * d.P + kx];
-    s[Lay::addr(i, c)] = v;
-  }
-  __syncthreads();
-  block_fft<L, C, NT, true, Lay>(s, tw);
-  float2* dst = X + ((size_t)(comp * d.nz + z) * d.ny) * d.P;
-  for (int e = threadIdx.x; e < d.ny * C; e += NT) {
-    const int i = e / C, c = e - i * C, kx = kx0 + c;
-    if (kx < d.NKX) dst[(size_t)i * d.P + kx] = s[Lay::addr(i, c)];
+  const int c = threadIdx.x % C, t = threadIdx.x / C;
+  const int kx = blockIdx.x * C + c, z = blockIdx.y, comp = blockIdx.z;
+  const bool ok = kx < d.NKX;
+  const float2* src = Y + ((size_t)(comp * d.nz + z) * L) * d.P + kx;
+  float2 v[1][E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) v[0][i] = ok ? src[(size_t)(t + TL * i) * d.P] : make_float2(0.f, 0.f);
+  reg_fft<L, E, 1, true>(v, sm + L, ColAddr<L, C>{c}, tw, t);
+  if (ok) {
+    float2* dst = X + ((size_t)(comp * d.nz + z) * d.ny) * d.P + kx;
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int p = t + TL * i;
+      if (p < d.ny) dst[(size_t)p * d.P] = v[0][i];
+    }
   }
 }
 
@@ -106,48 +129,42 @@ __device__ __forceinline__ void khat_apply(const float* __restrict__ khat, const
 
 // ---------------------------------------------------------------- K-Z: z fwd * Khat * z inv
 template <int L>
-struct ZCfg {
-  static constexpr int C = L >= 512 ? 4 : (L >= 256 ? 8 : 16);
-  static constexpr int E = L < 16 ? L : 16;
-  static constexpr int NT = 3 * L * C / E;
-};
-
-template <int L>
 __global__ void __launch_bounds__(ZCfg<L>::NT) k_zconv(float2* __restrict__ Y, const float* __restrict__ khat, Dims d,
                                                        const float2* __restrict__ gtw) {
-  constexpr int C = ZCfg<L>::C, NT = ZCfg<L>::NT;
-  using Lay = ColLayout<L, C>;
+  using Cf = ZCfg<L>;
+  constexpr int E = Cf::E, TL = Cf::TL, C = Cf::C, NT = Cf::NT;
   extern __shared__ float2 sm[];
   float2* tw = sm;
-  float2* s = sm + L;
   load_tw<L>(tw, gtw, NT);
-  const int kx0 = blockIdx.x * C, ky = blockIdx.y;
-  const size_t plane = (size_t)d.Ly * d.P;                 // stride between z planes of one comp
-  const size_t comp_stride = (size_t)d.nz * plane;
-  float2* base = Y + (size_t)ky * d.P;
-  for (int e = threadIdx.x; e < 3 * L * C; e += NT) {
-    const int g = e / (L * C), rem = e - g * (L * C), i = rem / C, c = rem - i * C, kx = kx0 + c;
-    float2 v = make_float2(0.f, 0.f);
-    if (i < d.nz && kx < d.NKX) v = base[g * comp_stride + i * plane + kx];
-    s[Lay::addr(i, g * C + c)] = v;
-  }
-  __syncthreads();
-  block_fft<L, 3 * C, NT, false, Lay>(s, tw);
-  for (int e = threadIdx.x; e < L * C; e += NT) {
-    const int i = e / C, c = e - i * C, kx = kx0 + c;
-    if (kx < d.NKX) {
-      float2 mx = s[Lay::addr(i, c)], my = s[Lay::addr(i, C + c)], mz = s[Lay::addr(i, 2 * C + c)];
-      khat_apply(khat, d, kx, ky, i, mx, my, mz);
-      s[Lay::addr(i, c)] = mx;
-      s[Lay::addr(i, C + c)] = my;
-      s[Lay::addr(i, 2 * C + c)] = mz;
+  const int c = threadIdx.x % C, t = threadIdx.x / C;
+  const int kx = blockIdx.x * C + c, ky = blockIdx.y;
+  const bool ok = kx < d.NKX;
+  const size_t plane = (size_t)d.Ly * d.P;    // stride between z planes of one component
+  const size_t cstr = (size_t)d.nz * plane;
+  float2* base = Y + (size_t)ky * d.P + kx;
+  float2 v[3][E];
+#pragma unroll
+  for (int g = 0; g < 3; ++g)
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int p = t + TL * i;
+      v[g][i] = (ok && p < d.nz) ? base[g * cstr + p * plane] : make_float2(0.f, 0.f);
     }
+  const ColAddr<L, C> A{c};
+  reg_fft<L, E, 3, false>(v, sm + L, A, tw, t);
+  if (ok) {
+#pragma unroll
+    for (int i = 0; i < E; ++i) khat_apply(khat, d, kx, ky, t + TL * i, v[0][i], v[1][i], v[2][i]);
   }
-  __syncthreads();
-  block_fft<L, 3 * C, NT, true, Lay>(s, tw);
-  for (int e = threadIdx.x; e < 3 * d.nz * C; e += NT) {
-    const int g = e / (d.nz * C), rem = e - g * (d.nz * C), i = rem / C, c = rem - i * C, kx = kx0 + c;
-    if (kx < d.NKX) base[g * comp_stride + i * plane + kx] = s[Lay::addr(i, g * C + c)];
+  reg_fft<L, E, 3, true>(v, sm + L, A, tw, t);
+  if (ok) {
+#pragma unroll
+    for (int g = 0; g < 3; ++g)
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int p = t + TL * i;
+        if (p < d.nz) base[g * cstr + p * plane] = v[g][i];
+      }
   }
 }
 
@@ -155,43 +172,45 @@ __global__ void __launch_bounds__(ZCfg<L>::NT) k_zconv(float2* __restrict__ Y, c
 template <int L>
 __global__ void __launch_bounds__(ZCfg<L>::NT) k_y2d(float2* __restrict__ X, const float* __restrict__ khat, Dims d,
                                                      const float2* __restrict__ gtw) {
-  constexpr int C = ZCfg<L>::C, NT = ZCfg<L>::NT;
-  using Lay = ColLayout<L, C>;
+  using Cf = ZCfg<L>;
+  constexpr int E = Cf::E, TL = Cf::TL, C = Cf::C, NT = Cf::NT;
   extern __shared__ float2 sm[];
   float2* tw = sm;
-  float2* s = sm + L;
   load_tw<L>(tw, gtw, NT);
-  const int kx0 = blockIdx.x * C;
-  const size_t comp_stride = (size_t)d.ny * d.P;
-  for (int e = threadIdx.x; e < 3 * L * C; e += NT) {
-    const int g = e / (L * C), rem = e - g * (L * C), i = rem / C, c = rem - i * C, kx = kx0 + c;
-    float2 v = make_float2(0.f, 0.f);
-    if (i < d.ny && kx < d.NKX) v = X[g * comp_stride + (size_t)i * d.P + kx];
-    s[Lay::addr(i, g * C + c)] = v;
-  }
-  __syncthreads();
-  block_fft<L, 3 * C, NT, false, Lay>(s, tw);
-  for (int e = threadIdx.x; e < L * C; e += NT) {
-    const int i = e / C, c = e - i * C, kx = kx0 + c;
-    if (kx < d.NKX) {
-      float2 mx = s[Lay::addr(i, c)], my = s[Lay::addr(i, C + c)], mz = s[Lay::addr(i, 2 * C + c)];
-      khat_apply(khat, d, kx, i, 0, mx, my, mz);
-      s[Lay::addr(i, c)] = mx;
-      s[Lay::addr(i, C + c)] = my;
-      s[Lay::addr(i, 2 * C + c)] = mz;
+  const int c = threadIdx.x % C, t = threadIdx.x / C;
+  const int kx = blockIdx.x * C + c;
+  const bool ok = kx < d.NKX;
+  const size_t cstr = (size_t)d.ny * d.P;
+  float2* base = X + kx;
+  float2 v[3][E];
+#pragma unroll
+  for (int g = 0; g < 3; ++g)
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int p = t + TL * i;
+      v[g][i] = (ok && p < d.ny) ? base[g * cstr + (size_t)p * d.P] : make_float2(0.f, 0.f);
     }
+  const ColAddr<L, C> A{c};
+  reg_fft<L, E, 3, false>(v, sm + L, A, tw, t);
+  if (ok) {
+#pragma unroll
+    for (int i = 0; i < E; ++i) khat_apply(khat, d, kx, t + TL * i, 0, v[0][i], v[1][i], v[2][i]);
   }
-  __syncthreads();
-  block_fft<L, 3 * C, NT, true, Lay>(s, tw);
-  for (int e = threadIdx.x; e < 3 * d.ny * C; e += NT) {
-    const int g = e / (d.ny * C), rem = e - g * (d.ny * C), i = rem / C, c = rem - i * C, kx = kx0 + c;
-    if (kx < d.NKX) X[g * comp_stride + (size_t)i * d.P + kx] = s[Lay::addr(i, g * C + c)];
+  reg_fft<L, E, 3, true>(v, sm + L, A, tw, t);
+  if (ok) {
+#pragma unroll
+    for (int g = 0; g < 3; ++g)
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int p = t + TL * i;
+        if (p < d.ny) base[g * cstr + (size_t)p * d.P] = v[g][i];
+      }
   }
 }
 
 // ---------------------------------------------------------------- dispatch
-#define MCQ_DISPATCH_L(Lval, ...)          \
-  switch (Lval) {                           \
+#define MCQ_DISPATCH_L(Lval, ...)                              \
+  switch (Lval) {                                              \
     case 2: { constexpr int L = 2; __VA_ARGS__; } break;       \
     case 4: { constexpr int L = 4; __VA_ARGS__; } break;       \
     case 8: { constexpr int L = 8; __VA_ARGS__; } break;       \
@@ -202,42 +221,38 @@ __global__ void __launch_bounds__(ZCfg<L>::NT) k_y2d(float2* __restrict__ X, con
     case 256: { constexpr int L = 256; __VA_ARGS__; } break;   \
     case 512: { constexpr int L = 512; __VA_ARGS__; } break;   \
     case 1024: { constexpr int L = 1024; __VA_ARGS__; } break; \
-    default: break;                         \
+    default: break;                                            \
   }
 
 void launch_yfwd(const Dims& d, const float2* X, float2* Y, const float2* tw, cudaStream_t st) {
   MCQ_DISPATCH_L(d.Ly, {
     using Cf = PassCfg<L>;
-    const size_t sm = (size_t)(L + L * Cf::C) * sizeof(float2);
     dim3 grid((d.NKX + Cf::C - 1) / Cf::C, d.nz, 3);
-    k_yfwd<L><<<grid, Cf::NT, sm, st>>>(X, Y, d, tw);
+    k_yfwd<L><<<grid, Cf::NT, Cf::SMEM, st>>>(X, Y, d, tw);
   })
 }
 
 void launch_yinv(const Dims& d, const float2* Y, float2* X, const float2* tw, cudaStream_t st) {
   MCQ_DISPATCH_L(d.Ly, {
     using Cf = PassCfg<L>;
-    const size_t sm = (size_t)(L + L * Cf::C) * sizeof(float2);
     dim3 grid((d.NKX + Cf::C - 1) / Cf::C, d.nz, 3);
-    k_yinv<L><<<grid, Cf::NT, sm, st>>>(Y, X, d, tw);
+    k_yinv<L><<<grid, Cf::NT, Cf::SMEM, st>>>(Y, X, d, tw);
   })
 }
 
 void launch_zconv(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t st) {
   MCQ_DISPATCH_L(d.Lz, {
     using Cf = ZCfg<L>;
-    const size_t sm = (size_t)(L + 3 * L * Cf::C) * sizeof(float2);
     dim3 grid((d.NKX + Cf::C - 1) / Cf::C, d.Ly);
-    k_zconv<L><<<grid, Cf::NT, sm, st>>>(Y, khat, d, tw);
+    k_zconv<L><<<grid, Cf::NT, Cf::SMEM, st>>>(Y, khat, d, tw);
   })
 }
 
 void launch_y2d(const Dims& d, float2* X, const float* khat, const float2* tw, cudaStream_t st) {
   MCQ_DISPATCH_L(d.Ly, {
     using Cf = ZCfg<L>;
-    const size_t sm = (size_t)(L + 3 * L * Cf::C) * sizeof(float2);
     dim3 grid((d.NKX + Cf::C - 1) / Cf::C);
-    k_y2d<L><<<grid, Cf::NT, sm, st>>>(X, khat, d, tw);
+    k_y2d<L><<<grid, Cf::NT, Cf::SMEM, st>>>(X, khat, d, tw);
   })
 }
 
@@ -245,12 +260,10 @@ void launch_y2d(const Dims& d, float2* X, const float* khat, const float2* tw, c
 void configure_pass_kernels() {
   for (int Lv = 2; Lv <= 1024; Lv *= 2) {
     MCQ_DISPATCH_L(Lv, {
-      const int a = (int)((L + L * PassCfg<L>::C) * sizeof(float2));
-      const int b = (int)((L + 3 * L * ZCfg<L>::C) * sizeof(float2));
-      cudaFuncSetAttribute(k_yfwd<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, a);
-      cudaFuncSetAttribute(k_yinv<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, a);
-      cudaFuncSetAttribute(k_zconv<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-      cudaFuncSetAttribute(k_y2d<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+      cudaFuncSetAttribute(k_yfwd<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PassCfg<L>::SMEM);
+      cudaFuncSetAttribute(k_yinv<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PassCfg<L>::SMEM);
+      cudaFuncSetAttribute(k_zconv<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZCfg<L>::SMEM);
+      cudaFuncSetAttribute(k_y2d<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZCfg<L>::SMEM);
     })
   }
 }

@@ -1,0 +1,83 @@
+// regfft.cuh — register-resident Stockham FFT stages for sm_100a.
+//
+// A line of length L (power of two) is spread over TL = L/E threads of a CTA; thread t owns the
+// E positions  p_i = t + TL*i  (i < E)  before the first stage and after the last one.  Every
+// radix-R stage (R <= E, R in {2,4,8,16}) is a register codelet; consecutive stages exchange
+// data through shared memory once, so an FFT of S stages costs S-1 smem round trips and the
+// input/output stay in registers, ready to be loaded from / stored to HBM or fused with the
+// next operation (the Khat multiply, the LLG update).  Stage (Ns = product of earlier radices):
+//     butterfly b in [0, L/R), k = b mod Ns:
+//     v[r] = x[b + r L/R] * w_{Ns R}^{r k},  v = DFT_R(v),  y[(b - k) R + k + r Ns] = v[r]
+// Thread t runs butterflies b = t + q*TL (q < E/R) whose inputs are exactly its positions
+// p_{q + r E/R}; in the last stage (Ns R = L) the outputs land on the same positions.
+#pragma once
+#include "fft.cuh"
+
+namespace mcq {
+
+template <int L, int E>
+__host__ __device__ constexpr int reg_radix(int Ns) {
+  constexpr int RMAX = cmin(16, cmin(E, L));
+  constexpr int lm = ilog2c(RMAX);
+  constexpr int lr = ilog2c(L);
+  constexpr int first = (lr % lm) ? (1 << (lr % lm)) : RMAX;
+  return Ns == 1 ? first : RMAX;
+}
+
+// v[l][i]: NLT lines per thread.  A(l, pos): shared-memory index of element pos of the
+// thread's line l.  tw[m * TWS] = exp(-2 pi i m / L).
+template <int L, int E, int NLT, bool INV, int TWS, int Ns, class Addr>
+__device__ __forceinline__ void reg_stage(float2 (&v)[NLT][E], float2* __restrict__ sm, const Addr& A,
+                                          const float2* __restrict__ tw, int t) {
+  if constexpr (Ns < L) {
+    constexpr int R = reg_radix<L, E>(Ns);
+    constexpr int TL = L / E;
+    constexpr int NB = E / R;
+    constexpr bool LAST = (Ns * R == L);
+#pragma unroll
+    for (int l = 0; l < NLT; ++l) {
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
+        const int b = t + q * TL;
+        const int k = b & (Ns - 1);
+        float2 x[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          x[r] = v[l][q + r * NB];
+          if (Ns > 1 && r > 0) {
+            float2 w = tw[(r * k * (L / (Ns * R))) * TWS];
+            if (INV) w.y = -w.y;
+            x[r] = cmul(x[r], w);
+          }
+        }
+        dft<R, INV>(x);
+        if (LAST) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) v[l][q + r * NB] = x[r];
+        } else {
+          const int base = (b - k) * R + k;
+#pragma unroll
+          for (int r = 0; r < R; ++r) sm[A(l, base + r * Ns)] = x[r];
+        }
+      }
+    }
+    if constexpr (!LAST) {
+      __syncthreads();
+#pragma unroll
+      for (int l = 0; l < NLT; ++l)
+#pragma unroll
+        for (int i = 0; i < E; ++i) v[l][i] = sm[A(l, t + TL * i)];
+      __syncthreads();  // the next stage stores into the same buffer
+      reg_stage<L, E, NLT, INV, TWS, Ns * R, Addr>(v, sm, A, tw, t);
+    }
+  }
+}
+
+template <int L, int E, int NLT, bool INV, int TWS = 1, class Addr>
+__device__ __forceinline__ void reg_fft(float2 (&v)[NLT][E], float2* __restrict__ sm, const Addr& A,
+                                        const float2* __restrict__ tw, int t) {
+  static_assert((L & (L - 1)) == 0 && E <= L && L % E == 0, "plan");
+  reg_stage<L, E, NLT, INV, TWS, 1, Addr>(v, sm, A, tw, t);
+}
+
+}  // namespace mcq

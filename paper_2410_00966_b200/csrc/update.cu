@@ -1,25 +1,32 @@
 // update.cu — the fused per-stage update kernel K-U, the cavity kernel K-CAV and layout helpers.
 //
-// K-U (one launch per RK4 stage), one CTA = RY full x-rows at one z:
-//   A. demag x-C2R: rows of the y/z-processed spectrum X'[3][z][y][0..Lx/2] -> real B_demag
-//      rows in shared memory (packed half-length complex IFFT, reading C11);
+// K-U (one launch per RK4 stage), one CTA = RY full x-rows at one z,
+// TL = N2/E threads per row; thread t of a row owns the packed positions n = t + TL*i (i < E),
+// i.e. the cell pairs x = 2n, 2n+1:
+//   A. demag x-C2R: Z_n = E_n + i O_n from the y/z-processed spectrum row X'[0..N2] (packed
+//      half-length real transform), register-resident inverse FFT -> z_n = B(2n) + i B(2n+1);
 //   B. per cell: B' = demag + B_ext + exchange (6-neighbour, C9) + anisotropy (C10)
 //      + B_rms (Gamma(t_s) + a sinc(w t_s)) (eq:bcav P:239), LLG torque (eq:llg P:184),
-//      RK4 stage combine + renormalisation (C1, C2); at stage 4 the overlap
-//      W partial = sum B_rms . m_{n+1} in fp64;
-//   C. x-R2C of m_{s+1} rows -> X[3][z][y][0..Lx/2] for the next stage's y/z passes.
+//      RK4 stage combine + renormalisation (C1, C2); at stage 4 the overlap partial
+//      sum B_rms . m_{n+1} in fp64;
+//   C. packed forward FFT of m_{s+1} rows (still in registers) and the real-to-half-complex
+//      post-processing -> X[3][z][y][0..N2] for the next stage's y/z passes.
 // Ms is folded into the kernel spectrum, so the transforms act on m directly.
 #include "common.cuh"
-#include "fft.cuh"
+#include "regfft.cuh"
 #include "../../include/mcq.h"
 
 namespace mcq {
 
 template <int N2>
 struct UCfg {
-  static constexpr int RY = (1024 / N2) < 1 ? 1 : ((1024 / N2) > 16 ? 16 : (1024 / N2));
   static constexpr int E = N2 < 16 ? N2 : 16;
-  static constexpr int NT = 3 * RY * N2 / E;
+  static constexpr int TL = N2 / E;                       // threads per row
+  static constexpr int RY0 = 128 / TL;
+  static constexpr int RY = RY0 < 1 ? 1 : (RY0 > 16 ? 16 : RY0);
+  static constexpr int NT = RY * TL;
+  static constexpr int PITCH = N2 + (N2 >= 16 ? N2 / 16 : 1);
+  static constexpr size_t SMEM = (size_t)(2 * N2 + 3 * RY * PITCH) * sizeof(float2);
 };
 
 __device__ __forceinline__ float3 cross3(float3 a, float3 b) {
@@ -39,189 +46,216 @@ __device__ __forceinline__ float3 ld3(const float* __restrict__ p, long long N, 
 }
 
 template <int N2>
+struct RowAddr {  // shared-memory address of element pos of component-line l of row yl
+  int yl;
+  __device__ __forceinline__ int operator()(int l, int pos) const {
+    return (l * UCfg<N2>::RY + yl) * UCfg<N2>::PITCH + pos + (N2 >= 16 ? (pos >> 4) : 0);
+  }
+};
+
+// One cell: effective field, then (by mode) field output / max torque / RK4 stage update.
+// Returns the value that enters the x-R2C rows (m_{s+1}, or m for MODE_X0).
+__device__ __forceinline__ float3 cell_update(const UpdateArgs& a, long long idx, int x, int y, int z, float3 Bd,
+                                              float gsum, double& wacc, float& tmax) {
+  const Dims& d = a.d;
+  const long long N = d.N;
+  const float3 m = ld3(a.mS, N, idx);
+  if (a.mode == MODE_X0) return m;
+  float3 B = make_float3(0.f, 0.f, 0.f);
+  if (dot3(m, m) > 0.f) {
+    B = Bd;
+    if (a.terms & MCQ_TERM_ZEEMAN) {
+      B.x += a.bext[0];
+      B.y += a.bext[1];
+      B.z += a.bext[2];
+    }
+    if (a.terms & MCQ_TERM_EXCHANGE) {
+      float3 acc = make_float3(0.f, 0.f, 0.f);
+#define MCQ_NB(COND, OFF, COEF)                  \
+  if (COND) {                                    \
+    const float3 mj = ld3(a.mS, N, idx + (OFF)); \
+    if (dot3(mj, mj) > 0.f) {                    \
+      acc.x += (COEF) * (mj.x - m.x);            \
+      acc.y += (COEF) * (mj.y - m.y);            \
+      acc.z += (COEF) * (mj.z - m.z);            \
+    }                                            \
+  }
+      MCQ_NB(x > 0, -1, a.ex[0])
+      MCQ_NB(x < d.nx - 1, +1, a.ex[0])
+      MCQ_NB(y > 0, -(long long)d.nx, a.ex[1])
+      MCQ_NB(y < d.ny - 1, +(long long)d.nx, a.ex[1])
+      MCQ_NB(z > 0, -(long long)d.nx * d.ny, a.ex[2])
+      MCQ_NB(z < d.nz - 1, +(long long)d.nx * d.ny, a.ex[2])
+#undef MCQ_NB
+      B.x += acc.x;
+      B.y += acc.y;
+      B.z += acc.z;
+    }
+    if (a.terms & MCQ_TERM_ANIS) {
+      if (a.ku != 0.f) {
+        const float mu = m.x * a.u[0] + m.y * a.u[1] + m.z * a.u[2];
+        B.x += a.ku * mu * a.u[0];
+        B.y += a.ku * mu * a.u[1];
+        B.z += a.ku * mu * a.u[2];
+      }
+      if (a.kc != 0.f) {
+        const float m1 = m.x * a.c1[0] + m.y * a.c1[1] + m.z * a.c1[2];
+        const float m2 = m.x * a.c2[0] + m.y * a.c2[1] + m.z * a.c2[2];
+        const float m3 = m.x * a.c3[0] + m.y * a.c3[1] + m.z * a.c3[2];
+        const float f1 = -a.kc * m1 * (m2 * m2 + m3 * m3);
+        const float f2 = -a.kc * m2 * (m1 * m1 + m3 * m3);
+        const float f3 = -a.kc * m3 * (m1 * m1 + m2 * m2);
+        B.x += f1 * a.c1[0] + f2 * a.c2[0] + f3 * a.c3[0];
+        B.y += f1 * a.c1[1] + f2 * a.c2[1] + f3 * a.c3[1];
+        B.z += f1 * a.c1[2] + f2 * a.c2[2] + f3 * a.c3[2];
+      }
+    }
+    if (gsum != 0.f) {
+      const float3 br = a.brms ? ld3(a.brms, N, idx) : make_float3(a.brms_u[0], a.brms_u[1], a.brms_u[2]);
+      B.x += br.x * gsum;
+      B.y += br.y * gsum;
+      B.z += br.z * gsum;
+    }
+  }
+  if (a.mode == MODE_FIELD) {
+    a.bout[idx] = B.x;
+    a.bout[N + idx] = B.y;
+    a.bout[2 * N + idx] = B.z;
+    return m;
+  }
+  const float3 mxB = cross3(m, B);
+  if (a.mode == MODE_MAXTORQUE) {
+    tmax = fmaxf(tmax, sqrtf(dot3(mxB, mxB)));
+    return m;
+  }
+  const float3 mmxB = cross3(m, mxB);
+  float3 k;
+  if (a.mode == MODE_LLG) {
+    k = make_float3(-a.gl * (mxB.x + a.alpha * mmxB.x), -a.gl * (mxB.y + a.alpha * mmxB.y),
+                    -a.gl * (mxB.z + a.alpha * mmxB.z));
+  } else {  // MODE_RELAX: -gamma m x (m x B)
+    k = make_float3(-a.gamma * mmxB.x, -a.gamma * mmxB.y, -a.gamma * mmxB.z);
+  }
+  const int stage = a.stage;
+  const float3 mn = (stage == 1) ? m : ld3(a.mN, N, idx);
+  float3 out;
+  if (stage < 4) {
+    float3 acc;
+    if (stage == 1) {
+      acc = k;
+    } else {
+      const float3 ap = ld3(a.acc, N, idx);
+      acc = make_float3(ap.x + 2.f * k.x, ap.y + 2.f * k.y, ap.z + 2.f * k.z);
+    }
+    a.acc[idx] = acc.x;
+    a.acc[N + idx] = acc.y;
+    a.acc[2 * N + idx] = acc.z;
+    out = nrm3(make_float3(mn.x + a.h * k.x, mn.y + a.h * k.y, mn.z + a.h * k.z));
+  } else {
+    const float3 ap = ld3(a.acc, N, idx);
+    out = nrm3(make_float3(mn.x + a.dt6 * (ap.x + k.x), mn.y + a.dt6 * (ap.y + k.y), mn.z + a.dt6 * (ap.z + k.z)));
+    if (a.mode == MODE_LLG) {
+      const float3 br = a.brms ? ld3(a.brms, N, idx) : make_float3(a.brms_u[0], a.brms_u[1], a.brms_u[2]);
+      wacc += (double)(br.x * out.x) + (double)(br.y * out.y) + (double)(br.z * out.z);
+    }
+  }
+  a.mOut[idx] = out.x;
+  a.mOut[N + idx] = out.y;
+  a.mOut[2 * N + idx] = out.z;
+  return out;
+}
+
+template <int N2>
 __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const float2* __restrict__ gtw) {
-  constexpr int RY = UCfg<N2>::RY, NT = UCfg<N2>::NT, LX = 2 * N2;
-  constexpr int NL = 3 * RY;  // lines: comp * RY + yl
-  using Lay = RowLayout<N2>;
+  using Cf = UCfg<N2>;
+  constexpr int E = Cf::E, TL = Cf::TL, RY = Cf::RY, NT = Cf::NT, LX = 2 * N2;
   extern __shared__ float2 sm[];
-  float2* tw = sm;        // w_Lx^m, m < Lx
-  float2* s = sm + LX;
+  float2* tw = sm;  // w_Lx^m, m < Lx
+  float2* xs = sm + LX;
   __shared__ double red[32];
   __shared__ float redf[32];
 
   const Dims& d = a.d;
-  const int y0 = blockIdx.x * RY, z = blockIdx.y;
-  const int nrow = min(RY, d.ny - y0);
-  const long long N = d.N;
+  const int yl = threadIdx.x / TL, t = threadIdx.x - yl * TL;
+  const int y0 = blockIdx.x * RY, z = blockIdx.y, y = y0 + yl;
+  const bool rowok = y < d.ny;
   for (int m = threadIdx.x; m < LX; m += NT) tw[m] = gtw[m * (kTwMax / LX)];
+  __syncthreads();
+  const RowAddr<N2> A{yl};
+  float2 v[3][E];
 
-  // ---------------- A: demag rows (x-C2R) ----------------
+  // ---------------- A: demag rows (packed x-C2R) ----------------
   const bool use_demag = a.demag && (a.terms & MCQ_TERM_DEMAG) && a.mode != MODE_X0;
   if (use_demag) {
-    __syncthreads();  // tw ready
-    for (int e = threadIdx.x; e < NL * N2; e += NT) {
-      const int line = e / N2, k = e - line * N2;
-      const int comp = line / RY, yl = line - comp * RY;
-      float2 zk = make_float2(0.f, 0.f);
-      if (yl < nrow) {
-        const float2* row = a.X + ((size_t)(comp * d.nz + z) * d.ny + y0 + yl) * d.P;
-        const float2 xk = row[k], xn = cconj(row[N2 - k]);
-        const float2 ev = cadd(xk, xn);
-        const float2 od = cmul(csub(xk, xn), cconj(tw[k]));  // * w^{-k}
-        zk = make_float2(ev.x - od.y, ev.y + od.x);           // E + i O
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float2* row = a.X + ((size_t)(c * d.nz + z) * d.ny + (rowok ? y : 0)) * d.P;
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int n = t + TL * i;
+        float2 zn = make_float2(0.f, 0.f);
+        if (rowok) {
+          const float2 xk = row[n], xn = cconj(row[N2 - n]);
+          const float2 ev = cadd(xk, xn);
+          const float2 od = cmul(csub(xk, xn), cconj(tw[n]));  // * w^{-n}
+          zn = make_float2(ev.x - od.y, ev.y + od.x);           // E + i O
+        }
+        v[c][i] = zn;
       }
-      s[Lay::addr(k, line)] = zk;
     }
-    __syncthreads();
-    block_fft<N2, NL, NT, true, Lay, 2>(s, tw);
+    reg_fft<N2, E, 3, true, 2>(v, xs, A, tw, t);
   } else {
-    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int i = 0; i < E; ++i) v[c][i] = make_float2(0.f, 0.f);
   }
 
   // ---------------- B: per-cell fields, torque, RK4 ----------------
-  float* sf = reinterpret_cast<float*>(s);
-  const int stage = a.stage;
   float gc = 0.f, ge = 0.f;
   if (a.mode == MODE_LLG || a.mode == MODE_FIELD) {
-    const int si = (a.mode == MODE_FIELD) ? 0 : stage - 1;
+    const int si = (a.mode == MODE_FIELD) ? 0 : a.stage - 1;
     gc = (a.terms & MCQ_TERM_CAVITY) ? a.cav->gc[si] : 0.f;
     ge = (a.terms & MCQ_TERM_EXCITATION) ? a.cav->ge[si] : 0.f;
   }
   const float gsum = gc + ge;
   double wacc = 0.0;
   float tmax = 0.f;
-  const int ncell = nrow * d.nx;
-  for (int e = threadIdx.x; e < ncell; e += NT) {
-    const int yl = e / d.nx, x = e - yl * d.nx, y = y0 + yl;
-    const long long idx = x + (long long)d.nx * (y + (long long)d.ny * z);
-    const float3 m = ld3(a.mS, N, idx);
-    float3 out = m;  // value that goes into the x-R2C rows
-    if (a.mode != MODE_X0) {
-      const bool mag = dot3(m, m) > 0.f;
-      float3 B = make_float3(0.f, 0.f, 0.f);
-      if (mag) {
-        if (use_demag) {
-          const int n = x >> 1, lo = x & 1;
-          B.x = sf[2 * Lay::addr(n, 0 * RY + yl) + lo];
-          B.y = sf[2 * Lay::addr(n, 1 * RY + yl) + lo];
-          B.z = sf[2 * Lay::addr(n, 2 * RY + yl) + lo];
-        }
-        if (a.terms & MCQ_TERM_ZEEMAN) {
-          B.x += a.bext[0];
-          B.y += a.bext[1];
-          B.z += a.bext[2];
-        }
-        if (a.terms & MCQ_TERM_EXCHANGE) {
-          float3 acc = make_float3(0.f, 0.f, 0.f);
-#define MCQ_NB(COND, OFF, COEF)                                      \
-  if (COND) {                                                        \
-    const float3 mj = ld3(a.mS, N, idx + (OFF));                     \
-    if (dot3(mj, mj) > 0.f) {                                        \
-      acc.x += (COEF) * (mj.x - m.x);                                \
-      acc.y += (COEF) * (mj.y - m.y);                                \
-      acc.z += (COEF) * (mj.z - m.z);                                \
-    }                                                                \
-  }
-          MCQ_NB(x > 0, -1, a.ex[0])
-          MCQ_NB(x < d.nx - 1, +1, a.ex[0])
-          MCQ_NB(y > 0, -(long long)d.nx, a.ex[1])
-          MCQ_NB(y < d.ny - 1, +(long long)d.nx, a.ex[1])
-          MCQ_NB(z > 0, -(long long)d.nx * d.ny, a.ex[2])
-          MCQ_NB(z < d.nz - 1, +(long long)d.nx * d.ny, a.ex[2])
-#undef MCQ_NB
-          B.x += acc.x;
-          B.y += acc.y;
-          B.z += acc.z;
-        }
-        if (a.terms & MCQ_TERM_ANIS) {
-          if (a.ku != 0.f) {
-            const float mu = m.x * a.u[0] + m.y * a.u[1] + m.z * a.u[2];
-            B.x += a.ku * mu * a.u[0];
-            B.y += a.ku * mu * a.u[1];
-            B.z += a.ku * mu * a.u[2];
-          }
-          if (a.kc != 0.f) {
-            const float m1 = m.x * a.c1[0] + m.y * a.c1[1] + m.z * a.c1[2];
-            const float m2 = m.x * a.c2[0] + m.y * a.c2[1] + m.z * a.c2[2];
-            const float m3 = m.x * a.c3[0] + m.y * a.c3[1] + m.z * a.c3[2];
-            const float f1 = -a.kc * m1 * (m2 * m2 + m3 * m3);
-            const float f2 = -a.kc * m2 * (m1 * m1 + m3 * m3);
-            const float f3 = -a.kc * m3 * (m1 * m1 + m2 * m2);
-            B.x += f1 * a.c1[0] + f2 * a.c2[0] + f3 * a.c3[0];
-            B.y += f1 * a.c1[1] + f2 * a.c2[1] + f3 * a.c3[1];
-            B.z += f1 * a.c1[2] + f2 * a.c2[2] + f3 * a.c3[2];
-          }
-        }
-        if (gsum != 0.f) {
-          const float3 br = a.brms ? ld3(a.brms, N, idx) : make_float3(a.brms_u[0], a.brms_u[1], a.brms_u[2]);
-          B.x += br.x * gsum;
-          B.y += br.y * gsum;
-          B.z += br.z * gsum;
-        }
+  const long long rowbase = (long long)d.nx * (y + (long long)d.ny * z);
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const int n = t + TL * i;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int x = 2 * n + h;
+      float3 o = make_float3(0.f, 0.f, 0.f);
+      if (rowok && x < d.nx) {
+        const float3 Bd = h ? make_float3(v[0][i].y, v[1][i].y, v[2][i].y) : make_float3(v[0][i].x, v[1][i].x, v[2][i].x);
+        o = cell_update(a, rowbase + x, x, y, z, Bd, gsum, wacc, tmax);
       }
-      if (a.mode == MODE_FIELD) {
-        a.bout[idx] = B.x;
-        a.bout[N + idx] = B.y;
-        a.bout[2 * N + idx] = B.z;
-        continue;
-      }
-      const float3 mxB = cross3(m, B);
-      if (a.mode == MODE_MAXTORQUE) {
-        tmax = fmaxf(tmax, sqrtf(dot3(mxB, mxB)));
-        continue;
-      }
-      float3 k;
-      const float3 mmxB = cross3(m, mxB);
-      if (a.mode == MODE_LLG) {
-        k = make_float3(-a.gl * (mxB.x + a.alpha * mmxB.x), -a.gl * (mxB.y + a.alpha * mmxB.y),
-                        -a.gl * (mxB.z + a.alpha * mmxB.z));
-      } else {  // MODE_RELAX: -gamma m x (m x B)
-        k = make_float3(-a.gamma * mmxB.x, -a.gamma * mmxB.y, -a.gamma * mmxB.z);
-      }
-      const float3 mn = (stage == 1) ? m : ld3(a.mN, N, idx);
-      if (stage < 4) {
-        float3 acc;
-        if (stage == 1) {
-          acc = k;
-        } else {
-          const float3 ap = ld3(a.acc, N, idx);
-          acc = make_float3(ap.x + 2.f * k.x, ap.y + 2.f * k.y, ap.z + 2.f * k.z);
-        }
-        a.acc[idx] = acc.x;
-        a.acc[N + idx] = acc.y;
-        a.acc[2 * N + idx] = acc.z;
-        out = nrm3(make_float3(mn.x + a.h * k.x, mn.y + a.h * k.y, mn.z + a.h * k.z));
+      if (h) {
+        v[0][i].y = o.x;
+        v[1][i].y = o.y;
+        v[2][i].y = o.z;
       } else {
-        const float3 ap = ld3(a.acc, N, idx);
-        out = nrm3(make_float3(mn.x + a.dt6 * (ap.x + k.x), mn.y + a.dt6 * (ap.y + k.y),
-                               mn.z + a.dt6 * (ap.z + k.z)));
-        if (a.mode == MODE_LLG) {
-          const float3 br = a.brms ? ld3(a.brms, N, idx) : make_float3(a.brms_u[0], a.brms_u[1], a.brms_u[2]);
-          wacc += (double)(br.x * out.x) + (double)(br.y * out.y) + (double)(br.z * out.z);
-        }
+        v[0][i].x = o.x;
+        v[1][i].x = o.y;
+        v[2][i].x = o.z;
       }
-      a.mOut[idx] = out.x;
-      a.mOut[N + idx] = out.y;
-      a.mOut[2 * N + idx] = out.z;
     }
-    // stash m_{s+1} (or m for MODE_X0) as real rows for the x-R2C
-    const int n = x >> 1, lo = x & 1;
-    sf[2 * Lay::addr(n, 0 * RY + yl) + lo] = out.x;
-    sf[2 * Lay::addr(n, 1 * RY + yl) + lo] = out.y;
-    sf[2 * Lay::addr(n, 2 * RY + yl) + lo] = out.z;
   }
 
   // ---------------- reductions ----------------
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (NT + 31) / 32;
-  if (a.mode == MODE_LLG && stage == 4) {
+  if (a.mode == MODE_LLG && a.stage == 4) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) wacc += __shfl_down_sync(0xffffffffu, wacc, o);
     if (lane == 0) red[warp] = wacc;
     __syncthreads();
     if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int w = 0; w < nw; ++w) t += red[w];
-      a.partials[blockIdx.y * gridDim.x + blockIdx.x] = t;
+      double s = 0.0;
+      for (int w = 0; w < nw; ++w) s += red[w];
+      a.partials[blockIdx.y * gridDim.x + blockIdx.x] = s;
     }
   }
   if (a.mode == MODE_MAXTORQUE) {
@@ -230,47 +264,47 @@ __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const flo
     if (lane == 0) redf[warp] = tmax;
     __syncthreads();
     if (threadIdx.x == 0) {
-      float t = 0.f;
-      for (int w = 0; w < nw; ++w) t = fmaxf(t, redf[w]);
-      atomicMax(a.maxbits, __float_as_uint(t));
+      float s = 0.f;
+      for (int w = 0; w < nw; ++w) s = fmaxf(s, redf[w]);
+      atomicMax(a.maxbits, __float_as_uint(s));
     }
     return;
   }
   if (a.mode == MODE_FIELD) return;
 
-  // ---------------- C: x-R2C of the new rows ----------------
-  // zero the padding: real positions x in [nx, Lx) of each valid row
-  for (int e = threadIdx.x; e < NL * (LX - d.nx); e += NT) {
-    const int line = e / (LX - d.nx), x = d.nx + (e - line * (LX - d.nx));
-    sf[2 * Lay::addr(x >> 1, line) + (x & 1)] = 0.f;
-  }
-  if (nrow < RY) {  // ragged tail rows: keep them finite (never stored)
-    for (int e = threadIdx.x; e < NL * d.nx; e += NT) {
-      const int line = e / d.nx, x = e - line * d.nx;
-      if (line % RY >= nrow) sf[2 * Lay::addr(x >> 1, line) + (x & 1)] = 0.f;
-    }
-  }
+  // ---------------- C: packed x-R2C of the new rows ----------------
+  reg_fft<N2, E, 3, false, 2>(v, xs, A, tw, t);
+  // X_k = (Z_k + conj Z_{N-k})/2 - i/2 w^k (Z_k - conj Z_{N-k}); partner via shared memory
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int i = 0; i < E; ++i) xs[A(c, t + TL * i)] = v[c][i];
   __syncthreads();
-  block_fft<N2, NL, NT, false, Lay, 2>(s, tw);
-  for (int e = threadIdx.x; e < NL * (N2 + 1); e += NT) {
-    const int line = e / (N2 + 1), k = e - line * (N2 + 1);
-    const int comp = line / RY, yl = line - comp * RY;
-    if (yl >= nrow) continue;
-    const float2 zk = s[Lay::addr(k & (N2 - 1), line)];
-    const float2 zn = cconj(s[Lay::addr((N2 - k) & (N2 - 1), line)]);
-    const float2 ev = cadd(zk, zn);                         // 2 A_k
-    const float2 df = csub(zk, zn);                         // 2 i B_k
-    const float2 wd = cmul(tw[k], df);                      // w^k (Z_k - conj Z_{N-k})
-    // X_k = (Z_k + conj Z_{N-k})/2 - i/2 w^k (Z_k - conj Z_{N-k})
-    const float2 xk = make_float2(0.5f * (ev.x + wd.y), 0.5f * (ev.y - wd.x));
-    a.X[((size_t)(comp * d.nz + z) * d.ny + y0 + yl) * d.P + k] = xk;
+  if (rowok) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      float2* row = a.X + ((size_t)(c * d.nz + z) * d.ny + y) * d.P;
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int k = t + TL * i;
+        const float2 zk = v[c][i];
+        const float2 zn = cconj(xs[A(c, (N2 - k) & (N2 - 1))]);
+        const float2 ev = cadd(zk, zn);
+        const float2 wd = cmul(tw[k], csub(zk, zn));
+        row[k] = make_float2(0.5f * (ev.x + wd.y), 0.5f * (ev.y - wd.x));
+        if (k == 0) row[N2] = make_float2(zk.x - zk.y, 0.f);  // Nyquist: Re Z0 - Im Z0
+      }
+    }
   }
 }
 
 int update_grid_blocks(const Dims& d) {
   int ry = 1;
   switch (d.N2) {
-#define C_(n) case n: ry = UCfg<n>::RY; break;
+#define C_(n) \
+  case n:     \
+    ry = UCfg<n>::RY; \
+    break;
     C_(2) C_(4) C_(8) C_(16) C_(32) C_(64) C_(128) C_(256) C_(512)
 #undef C_
     default: break;
@@ -278,37 +312,32 @@ int update_grid_blocks(const Dims& d) {
   return ((d.ny + ry - 1) / ry) * d.nz;
 }
 
-#define MCQ_DISPATCH_N2(Nv, ...)                        \
-  switch (Nv) {                                          \
-    case 2: { constexpr int N2 = 2; __VA_ARGS__; } break;       \
-    case 4: { constexpr int N2 = 4; __VA_ARGS__; } break;       \
-    case 8: { constexpr int N2 = 8; __VA_ARGS__; } break;       \
-    case 16: { constexpr int N2 = 16; __VA_ARGS__; } break;     \
-    case 32: { constexpr int N2 = 32; __VA_ARGS__; } break;     \
-    case 64: { constexpr int N2 = 64; __VA_ARGS__; } break;     \
-    case 128: { constexpr int N2 = 128; __VA_ARGS__; } break;   \
-    case 256: { constexpr int N2 = 256; __VA_ARGS__; } break;   \
-    case 512: { constexpr int N2 = 512; __VA_ARGS__; } break;   \
-    default: break;                                      \
+#define MCQ_DISPATCH_N2(Nv, ...)                             \
+  switch (Nv) {                                              \
+    case 2: { constexpr int N2 = 2; __VA_ARGS__; } break;     \
+    case 4: { constexpr int N2 = 4; __VA_ARGS__; } break;     \
+    case 8: { constexpr int N2 = 8; __VA_ARGS__; } break;     \
+    case 16: { constexpr int N2 = 16; __VA_ARGS__; } break;   \
+    case 32: { constexpr int N2 = 32; __VA_ARGS__; } break;   \
+    case 64: { constexpr int N2 = 64; __VA_ARGS__; } break;   \
+    case 128: { constexpr int N2 = 128; __VA_ARGS__; } break; \
+    case 256: { constexpr int N2 = 256; __VA_ARGS__; } break; \
+    case 512: { constexpr int N2 = 512; __VA_ARGS__; } break; \
+    default: break;                                          \
   }
-
-template <int N2>
-static size_t update_smem() {
-  return (size_t)(2 * N2 + RowLayout<N2>::size(3 * UCfg<N2>::RY)) * sizeof(float2);
-}
 
 void launch_update(const UpdateArgs& a, const float2* tw, cudaStream_t st) {
   MCQ_DISPATCH_N2(a.d.N2, {
     using Cf = UCfg<N2>;
     dim3 grid((a.d.ny + Cf::RY - 1) / Cf::RY, a.d.nz);
-    k_update<N2><<<grid, Cf::NT, update_smem<N2>(), st>>>(a, tw);
+    k_update<N2><<<grid, Cf::NT, Cf::SMEM, st>>>(a, tw);
   })
 }
 
 void configure_update_kernels() {
   for (int n = 2; n <= 512; n *= 2) {
     MCQ_DISPATCH_N2(n, {
-      cudaFuncSetAttribute(k_update<N2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)update_smem<N2>());
+      cudaFuncSetAttribute(k_update<N2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UCfg<N2>::SMEM);
     })
   }
 }
@@ -383,7 +412,7 @@ __global__ void k_aos_to_soa(const float* __restrict__ in, float* __restrict__ o
       if (!(n2 > 0.f) || !isfinite(n2)) {
         atomicAdd(bad, 1);
         v = make_float3(0.f, 0.f, 0.f);
-      } else {
+      } else if (fabsf(n2 - 1.0f) > 1e-6f) {  // already-unit vectors (a saved state) kept bit-exact
         const float r = 1.0f / sqrtf(n2);
         v = make_float3(v.x * r, v.y * r, v.z * r);
       }
