@@ -14,6 +14,10 @@
 #include "common.cuh"
 #include "regfft.cuh"
 
+#ifndef MCQ_ZE
+#define MCQ_ZE 8   // complex values per thread per line in K-Z / K-Y2D (register budget)
+#endif
+
 namespace mcq {
 
 template <int L>
@@ -27,13 +31,14 @@ struct PassCfg {  // single-line passes (K-Y, K-YI)
 };
 
 template <int L>
-struct ZCfg {  // three-line passes with the Khat multiply (K-Z, K-Y2D)
-  static constexpr int E = L < 16 ? L : 16;
+struct ZCfg {  // three-component passes with the Khat multiply (K-Z, K-Y2D): one line per thread group
+  static constexpr int E = L >= 1024 ? 16 : (L < MCQ_ZE ? L : MCQ_ZE);
   static constexpr int TL = L / E;
-  static constexpr int C0 = 128 / TL;
+  static constexpr int C0 = 256 / TL;  // columns per CTA: NT = 3 * C * TL <= 768
   static constexpr int C = C0 < 4 ? 4 : (C0 > 64 ? 64 : C0);
-  static constexpr int NT = C * TL;
-  static constexpr size_t SMEM = (size_t)(L + (TL > 1 ? 3 * L * C : 0)) * sizeof(float2);
+  static_assert(3 * C * TL <= 1024, "block size");
+  static constexpr int NT = 3 * C * TL;
+  static constexpr size_t SMEM = (size_t)(L + 3 * L * C) * sizeof(float2);
 };
 
 template <int L>
@@ -127,84 +132,77 @@ __device__ __forceinline__ void khat_apply(const float* __restrict__ khat, const
   mz = bz;
 }
 
-// ---------------------------------------------------------------- K-Z: z fwd * Khat * z inv
-template <int L>
-__global__ void __launch_bounds__(ZCfg<L>::NT) k_zconv(float2* __restrict__ Y, const float* __restrict__ khat, Dims d,
-                                                       const float2* __restrict__ gtw) {
+// ---------------------------------------------------------------- K-Z / K-Y2D: fwd * Khat * inv
+// Thread group (component g, column c) owns one line; the forward transforms leave the three
+// components of a point in three different threads, so they meet once in shared memory for the
+// multiply: each thread forms its own component B_g = sum_h Khat_gh M_h at its positions.
+// AXIS2D = false: lines along z of Y[3][nz][Ly][P] at ky = blockIdx.y (K-Z);
+// AXIS2D = true : lines along y of X[3][1][ny][P] (K-Y2D, nz == 1, kz = 0).
+template <int L, bool AXIS2D>
+__global__ void __launch_bounds__(ZCfg<L>::NT) k_conv(float2* __restrict__ Y, const float* __restrict__ khat, Dims d,
+                                                      const float2* __restrict__ gtw) {
   using Cf = ZCfg<L>;
   constexpr int E = Cf::E, TL = Cf::TL, C = Cf::C, NT = Cf::NT;
   extern __shared__ float2 sm[];
   float2* tw = sm;
+  float2* xs = sm + L;
   load_tw<L>(tw, gtw, NT);
-  const int c = threadIdx.x % C, t = threadIdx.x / C;
-  const int kx = blockIdx.x * C + c, ky = blockIdx.y;
-  const bool ok = kx < d.NKX;
-  const size_t plane = (size_t)d.Ly * d.P;    // stride between z planes of one component
-  const size_t cstr = (size_t)d.nz * plane;
-  float2* base = Y + (size_t)ky * d.P + kx;
-  float2 v[3][E];
-#pragma unroll
-  for (int g = 0; g < 3; ++g)
-#pragma unroll
-    for (int i = 0; i < E; ++i) {
-      const int p = t + TL * i;
-      v[g][i] = (ok && p < d.nz) ? base[g * cstr + p * plane] : make_float2(0.f, 0.f);
-    }
-  const ColAddr<L, C> A{c};
-  reg_fft<L, E, 3, false>(v, sm + L, A, tw, t);
-  if (ok) {
-#pragma unroll
-    for (int i = 0; i < E; ++i) khat_apply(khat, d, kx, ky, t + TL * i, v[0][i], v[1][i], v[2][i]);
-  }
-  reg_fft<L, E, 3, true>(v, sm + L, A, tw, t);
-  if (ok) {
-#pragma unroll
-    for (int g = 0; g < 3; ++g)
-#pragma unroll
-      for (int i = 0; i < E; ++i) {
-        const int p = t + TL * i;
-        if (p < d.nz) base[g * cstr + p * plane] = v[g][i];
-      }
-  }
-}
-
-// ---------------------------------------------------------------- K-Y2D (nz == 1)
-template <int L>
-__global__ void __launch_bounds__(ZCfg<L>::NT) k_y2d(float2* __restrict__ X, const float* __restrict__ khat, Dims d,
-                                                     const float2* __restrict__ gtw) {
-  using Cf = ZCfg<L>;
-  constexpr int E = Cf::E, TL = Cf::TL, C = Cf::C, NT = Cf::NT;
-  extern __shared__ float2 sm[];
-  float2* tw = sm;
-  load_tw<L>(tw, gtw, NT);
-  const int c = threadIdx.x % C, t = threadIdx.x / C;
+  const int c = threadIdx.x % C, rest = threadIdx.x / C, g = rest % 3, t = rest / 3;
   const int kx = blockIdx.x * C + c;
+  const int ky = AXIS2D ? 0 : blockIdx.y;
   const bool ok = kx < d.NKX;
-  const size_t cstr = (size_t)d.ny * d.P;
-  float2* base = X + kx;
-  float2 v[3][E];
+  const int nin = AXIS2D ? d.ny : d.nz;
+  const size_t lstride = AXIS2D ? (size_t)d.P : (size_t)d.Ly * d.P;     // between line elements
+  const size_t cstr = AXIS2D ? (size_t)d.ny * d.P : (size_t)d.nz * d.Ly * d.P;
+  float2* base = Y + g * cstr + (size_t)ky * d.P + kx;
+  float2 v[1][E];
 #pragma unroll
-  for (int g = 0; g < 3; ++g)
+  for (int i = 0; i < E; ++i) {
+    const int p = t + TL * i;
+    v[0][i] = (ok && p < nin) ? base[p * lstride] : make_float2(0.f, 0.f);
+  }
+  // line l of this thread = component g; element (g, pos, c) at (g L + pos) C + c
+  struct A3 {
+    int g, c;
+    __device__ __forceinline__ int operator()(int, int pos) const { return (g * L + pos) * C + c; }
+  } A{g, c};
+  reg_fft<L, E, 1, false>(v, xs, A, tw, t);
+#pragma unroll
+  for (int i = 0; i < E; ++i) xs[A(0, t + TL * i)] = v[0][i];
+  __syncthreads();
+  if (ok) {
+    const int hy = d.Ly / 2, hz = d.Lz / 2;
+    const size_t cs = (size_t)(hz + 1) * (hy + 1) * d.P;
+    // components of row g of the symmetric tensor: (gg, g0, g1) with signs for the folds
+    // g = 0: (XX; XY*My, XZ*Mz)   g = 1: (YY; XY*Mx, YZ*Mz)   g = 2: (ZZ; XZ*Mx, YZ*My)
+    const int cd = g, co0 = g == 2 ? 4 : 3, co1 = g == 0 ? 4 : 5;
+    const int h0 = g == 0 ? 1 : 0, h1 = g == 2 ? 1 : 2;
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       const int p = t + TL * i;
-      v[g][i] = (ok && p < d.ny) ? base[g * cstr + (size_t)p * d.P] : make_float2(0.f, 0.f);
+      const int kyv = AXIS2D ? p : ky, kzv = AXIS2D ? 0 : p;
+      const int kyf = kyv <= hy ? kyv : d.Ly - kyv;
+      const int kzf = kzv <= hz ? kzv : d.Lz - kzv;
+      const float sy = kyv <= hy ? 1.f : -1.f, sz = kzv <= hz ? 1.f : -1.f;
+      const float sgn[6] = {1.f, 1.f, 1.f, sy, sz, sy * sz};
+      const size_t b = ((size_t)kzf * (hy + 1) + kyf) * d.P + kx;
+      const float kd = __ldg(khat + cd * cs + b);
+      const float k0 = sgn[co0] * __ldg(khat + co0 * cs + b);
+      const float k1 = sgn[co1] * __ldg(khat + co1 * cs + b);
+      const float2 md = v[0][i];
+      const float2 m0 = xs[(h0 * L + p) * C + c], m1 = xs[(h1 * L + p) * C + c];
+      v[0][i] = make_float2(kd * md.x + k0 * m0.x + k1 * m1.x, kd * md.y + k0 * m0.y + k1 * m1.y);
+      if ((i & 3) == 3) asm volatile("" ::: "memory");  // bound load hoisting (register budget)
     }
-  const ColAddr<L, C> A{c};
-  reg_fft<L, E, 3, false>(v, sm + L, A, tw, t);
-  if (ok) {
-#pragma unroll
-    for (int i = 0; i < E; ++i) khat_apply(khat, d, kx, t + TL * i, 0, v[0][i], v[1][i], v[2][i]);
   }
-  reg_fft<L, E, 3, true>(v, sm + L, A, tw, t);
+  __syncthreads();
+  reg_fft<L, E, 1, true>(v, xs, A, tw, t);
   if (ok) {
 #pragma unroll
-    for (int g = 0; g < 3; ++g)
-#pragma unroll
-      for (int i = 0; i < E; ++i) {
-        const int p = t + TL * i;
-        if (p < d.ny) base[g * cstr + (size_t)p * d.P] = v[g][i];
-      }
+    for (int i = 0; i < E; ++i) {
+      const int p = t + TL * i;
+      if (p < nin) base[p * lstride] = v[0][i];
+    }
   }
 }
 
@@ -244,7 +242,7 @@ void launch_zconv(const Dims& d, float2* Y, const float* khat, const float2* tw,
   MCQ_DISPATCH_L(d.Lz, {
     using Cf = ZCfg<L>;
     dim3 grid((d.NKX + Cf::C - 1) / Cf::C, d.Ly);
-    k_zconv<L><<<grid, Cf::NT, Cf::SMEM, st>>>(Y, khat, d, tw);
+    k_conv<L, false><<<grid, Cf::NT, Cf::SMEM, st>>>(Y, khat, d, tw);
   })
 }
 
@@ -252,7 +250,7 @@ void launch_y2d(const Dims& d, float2* X, const float* khat, const float2* tw, c
   MCQ_DISPATCH_L(d.Ly, {
     using Cf = ZCfg<L>;
     dim3 grid((d.NKX + Cf::C - 1) / Cf::C);
-    k_y2d<L><<<grid, Cf::NT, Cf::SMEM, st>>>(X, khat, d, tw);
+    k_conv<L, true><<<grid, Cf::NT, Cf::SMEM, st>>>(X, khat, d, tw);
   })
 }
 
@@ -262,8 +260,8 @@ void configure_pass_kernels() {
     MCQ_DISPATCH_L(Lv, {
       cudaFuncSetAttribute(k_yfwd<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PassCfg<L>::SMEM);
       cudaFuncSetAttribute(k_yinv<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PassCfg<L>::SMEM);
-      cudaFuncSetAttribute(k_zconv<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZCfg<L>::SMEM);
-      cudaFuncSetAttribute(k_y2d<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZCfg<L>::SMEM);
+      cudaFuncSetAttribute(k_conv<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZCfg<L>::SMEM);
+      cudaFuncSetAttribute(k_conv<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZCfg<L>::SMEM);
     })
   }
 }

@@ -16,11 +16,15 @@
 #include "regfft.cuh"
 #include "../../include/mcq.h"
 
+#ifndef MCQ_UE
+#define MCQ_UE 8   // packed row positions per thread in K-U (register budget)
+#endif
+
 namespace mcq {
 
 template <int N2>
 struct UCfg {
-  static constexpr int E = N2 < 16 ? N2 : 16;
+  static constexpr int E = N2 < MCQ_UE ? N2 : MCQ_UE;
   static constexpr int TL = N2 / E;                       // threads per row
   static constexpr int RY0 = 128 / TL;
   static constexpr int RY = RY0 < 1 ? 1 : (RY0 > 16 ? 16 : RY0);
@@ -55,11 +59,16 @@ struct RowAddr {  // shared-memory address of element pos of component-line l of
 
 // One cell: effective field, then (by mode) field output / max torque / RK4 stage update.
 // Returns the value that enters the x-R2C rows (m_{s+1}, or m for MODE_X0).
-__device__ __forceinline__ float3 cell_update(const UpdateArgs& a, long long idx, int x, int y, int z, float3 Bd,
-                                              float gsum, double& wacc, float& tmax) {
+// The state pointers come in as __restrict__ parameters so loads of the next cell can be hoisted
+// above the stores of this one (each cell touches only its own entries of acc / mOut).
+__device__ __forceinline__ float3 cell_update(const UpdateArgs& a, const float* __restrict__ mS,
+                                              const float* __restrict__ mN, float* __restrict__ mOut,
+                                              float* __restrict__ accp, const float* __restrict__ brms,
+                                              float* __restrict__ bout, long long idx, int x, int y, int z,
+                                              float3 Bd, float gsum, double& wacc, float& tmax) {
   const Dims& d = a.d;
   const long long N = d.N;
-  const float3 m = ld3(a.mS, N, idx);
+  const float3 m = ld3(mS, N,idx);
   if (a.mode == MODE_X0) return m;
   float3 B = make_float3(0.f, 0.f, 0.f);
   if (dot3(m, m) > 0.f) {
@@ -73,7 +82,7 @@ __device__ __forceinline__ float3 cell_update(const UpdateArgs& a, long long idx
       float3 acc = make_float3(0.f, 0.f, 0.f);
 #define MCQ_NB(COND, OFF, COEF)                  \
   if (COND) {                                    \
-    const float3 mj = ld3(a.mS, N, idx + (OFF)); \
+    const float3 mj = ld3(mS, N,idx + (OFF)); \
     if (dot3(mj, mj) > 0.f) {                    \
       acc.x += (COEF) * (mj.x - m.x);            \
       acc.y += (COEF) * (mj.y - m.y);            \
@@ -111,16 +120,16 @@ __device__ __forceinline__ float3 cell_update(const UpdateArgs& a, long long idx
       }
     }
     if (gsum != 0.f) {
-      const float3 br = a.brms ? ld3(a.brms, N, idx) : make_float3(a.brms_u[0], a.brms_u[1], a.brms_u[2]);
+      const float3 br = brms ? ld3(brms, N, idx) : make_float3(a.brms_u[0], a.brms_u[1], a.brms_u[2]);
       B.x += br.x * gsum;
       B.y += br.y * gsum;
       B.z += br.z * gsum;
     }
   }
   if (a.mode == MODE_FIELD) {
-    a.bout[idx] = B.x;
-    a.bout[N + idx] = B.y;
-    a.bout[2 * N + idx] = B.z;
+    bout[idx] = B.x;
+    bout[N + idx] = B.y;
+    bout[2 * N + idx] = B.z;
     return m;
   }
   const float3 mxB = cross3(m, B);
@@ -137,31 +146,31 @@ __device__ __forceinline__ float3 cell_update(const UpdateArgs& a, long long idx
     k = make_float3(-a.gamma * mmxB.x, -a.gamma * mmxB.y, -a.gamma * mmxB.z);
   }
   const int stage = a.stage;
-  const float3 mn = (stage == 1) ? m : ld3(a.mN, N, idx);
+  const float3 mn = (stage == 1) ? m : ld3(mN, N, idx);
   float3 out;
   if (stage < 4) {
     float3 acc;
     if (stage == 1) {
       acc = k;
     } else {
-      const float3 ap = ld3(a.acc, N, idx);
+      const float3 ap = ld3(accp, N, idx);
       acc = make_float3(ap.x + 2.f * k.x, ap.y + 2.f * k.y, ap.z + 2.f * k.z);
     }
-    a.acc[idx] = acc.x;
-    a.acc[N + idx] = acc.y;
-    a.acc[2 * N + idx] = acc.z;
+    accp[idx] = acc.x;
+    accp[N + idx] = acc.y;
+    accp[2 * N + idx] = acc.z;
     out = nrm3(make_float3(mn.x + a.h * k.x, mn.y + a.h * k.y, mn.z + a.h * k.z));
   } else {
-    const float3 ap = ld3(a.acc, N, idx);
+    const float3 ap = ld3(accp, N, idx);
     out = nrm3(make_float3(mn.x + a.dt6 * (ap.x + k.x), mn.y + a.dt6 * (ap.y + k.y), mn.z + a.dt6 * (ap.z + k.z)));
     if (a.mode == MODE_LLG) {
-      const float3 br = a.brms ? ld3(a.brms, N, idx) : make_float3(a.brms_u[0], a.brms_u[1], a.brms_u[2]);
+      const float3 br = brms ? ld3(brms, N, idx) : make_float3(a.brms_u[0], a.brms_u[1], a.brms_u[2]);
       wacc += (double)(br.x * out.x) + (double)(br.y * out.y) + (double)(br.z * out.z);
     }
   }
-  a.mOut[idx] = out.x;
-  a.mOut[N + idx] = out.y;
-  a.mOut[2 * N + idx] = out.z;
+  mOut[idx] = out.x;
+  mOut[N + idx] = out.y;
+  mOut[2 * N + idx] = out.z;
   return out;
 }
 
@@ -231,7 +240,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const flo
       float3 o = make_float3(0.f, 0.f, 0.f);
       if (rowok && x < d.nx) {
         const float3 Bd = h ? make_float3(v[0][i].y, v[1][i].y, v[2][i].y) : make_float3(v[0][i].x, v[1][i].x, v[2][i].x);
-        o = cell_update(a, rowbase + x, x, y, z, Bd, gsum, wacc, tmax);
+        o = cell_update(a, a.mS, a.mN, a.mOut, a.acc, a.brms, a.bout, rowbase + x, x, y, z, Bd, gsum, wacc, tmax);
       }
       if (h) {
         v[0][i].y = o.x;
