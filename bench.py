@@ -94,14 +94,16 @@ def alg_bytes(L, grid, has_map):
     Y = 3 * nz * Ly * nkx * 8
     K = 6 * (Lz // 2 + 1) * (Ly // 2 + 1) * nkx * 4
     state = (36 + 60 + 60 + 48) / 4 * N           # RK4 state traffic averaged over the 4 stages
-    out = {"yfwd": X + Y, "zconv": 2 * Y + K, "yinv": Y + X,
-           "y2d": 2 * X + 4 * ((Ly // 2 + 1) * nkx * 4),
+    out = {"yfwd": X + Y, "zconv": 2 * Y + K, "yinv": Y + X, "yz": 2 * X + K,
+           "y2d": 2 * X + 6 * ((Ly // 2 + 1) * nkx * 4),
            "update": 2 * X + state + (12 * N if has_map else 0), "cavity": 0}
     return out
 
 
 def step_alg_bytes(L, grid, has_map):
     b = alg_bytes(L, grid, has_map)
+    if grid[2] > 1 and L.get("yz_cluster", 0) > 0:
+        return 4 * (b["yz"] + b["update"])
     if grid[2] > 1:
         return 4 * (b["yfwd"] + b["zconv"] + b["yinv"] + b["update"])
     return 4 * (b["y2d"] + b["update"])
@@ -174,6 +176,8 @@ def main():
     ap.add_argument("--impl", default="mcq", choices=["mcq", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=5)
+    ap.add_argument("--demag-path", default="auto", choices=["auto", "3pass"],
+                    help="auto: cluster-fused y/z kernel when the kx plane fits; 3pass: force y/z/y")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -202,6 +206,8 @@ def main():
     stream = torch.cuda.Stream()          # a real stream: the library's kernels and our events share it
     torch.cuda.set_stream(stream)
     solver = mcq.Solver.from_config(cfg, stream=stream.cuda_stream)
+    if args.demag_path == "3pass":
+        mcq.mcq_debug_set_path(solver.ctx, 1)
     if cfg.relax_first:
         solver.relax(cfg.dt * 0.5, 1e-3, 2000)
         mcq.mcq_reset_memory(solver.ctx)

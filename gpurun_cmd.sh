@@ -1,4 +1,8 @@
 mkdir -p gpurun_out
-python bench.py --steps 10 --warmup 3 --no-cpu-baseline --profile-steps 1 > gpurun_out/plain6.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_conv|k_update" -s 20 -c 2 -o gpurun_out/prof6 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --profile-steps 1 > gpurun_out/ncu6.log 2>&1
-tail -2 gpurun_out/ncu6.log
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "field or 100_steps or khat or fused or launch" 2>&1 | tail -30 > gpurun_out/gpu_tests9.log
+timeout 600 python bench.py --steps 500 --warmup 10 --no-cpu-baseline > gpurun_out/bench9a.log 2>&1
+timeout 600 python bench.py --steps 500 --warmup 10 --no-cpu-baseline --demag-path 3pass > gpurun_out/bench9b.log 2>&1
+timeout 600 python bench.py --steps 200 --warmup 10 --no-cpu-baseline --config 3 > gpurun_out/bench9c.log 2>&1
+tail -5 gpurun_out/gpu_tests9.log
+for f in a b c; do python -c "
+import json;d=json.loads(open('gpurun_out/bench9$f.log').read().strip().splitlines()[-1]);print('$f',d['value'],d['ms_per_step'],{k:(round(v['ms'],4),v['per_step']) for k,v in d['kernels'].items()})"; done

@@ -12,7 +12,8 @@ import numpy as np
 
 from ._lib import (lib, MCQError, mcq_aniso, mcq_dist, mcq_cavity_state, EXPORTED,  # noqa: F401
                    TERM_ZEEMAN, TERM_EXCHANGE, TERM_ANIS, TERM_DEMAG, TERM_CAVITY, TERM_EXCITATION,
-                   TERM_ALL, NKCLASS, KCLASS_NAMES, K_YFWD, K_ZCONV, K_YINV, K_Y2D, K_UPDATE, K_CAVITY)
+                   TERM_ALL, NKCLASS, KCLASS_NAMES, K_YFWD, K_ZCONV, K_YINV, K_Y2D, K_UPDATE, K_CAVITY,
+                   K_YZ)
 
 __all__ = [n for n in EXPORTED] + ["Solver", "MCQError"]
 
@@ -171,7 +172,11 @@ def mcq_profile_run(ctx, dt, steps):
 def mcq_debug_layout(ctx):
     out = (C.c_longlong * 6)()
     _check(ctx, lib.mcq_debug_layout(ctx, out))
-    return dict(zip(("Lx", "Ly", "Lz", "NKX", "P", "n_partials"), list(out)))
+    return dict(zip(("Lx", "Ly", "Lz", "NKX", "yz_cluster", "n_partials"), list(out)))
+
+
+def mcq_debug_set_path(ctx, path):
+    _check(ctx, lib.mcq_debug_set_path(ctx, int(path)))
 
 
 def mcq_debug_tensor_octant(ctx):
@@ -184,10 +189,10 @@ def mcq_debug_tensor_octant(ctx):
 
 def mcq_debug_khat(ctx):
     L = mcq_debug_layout(ctx)
-    shape = (6, L["Lz"] // 2 + 1, L["Ly"] // 2 + 1, L["P"])
+    shape = (L["NKX"], 6, L["Lz"] // 2 + 1, L["Ly"] // 2 + 1)
     out = np.empty(shape, np.float32)
     _check(ctx, lib.mcq_debug_khat(ctx, out.ctypes.data))
-    return out[..., :L["NKX"]]
+    return out
 
 
 def mcq_last_error(ctx):

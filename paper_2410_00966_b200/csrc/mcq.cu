@@ -47,6 +47,9 @@ struct mcq_ctx {
   int* bad = nullptr;
   float* io = nullptr;
   bool m_set = false;
+  YZPlan yz{};        // cluster-fused y/z plan (ok == false: 3-pass fallback)
+  bool use_yz = false;   // demag schedule in use (fused y/z cluster kernel vs 3-pass)
+  bool auto_yz = false;  // the schedule picked by timing both at create
   // graphs: [0] = 1 LLG step, [1] = kGraphSteps LLG steps, [2] = 1 relax step, [3] = relax chunk
   cudaGraphExec_t g[4] = {nullptr, nullptr, nullptr, nullptr};
   double g_dt[4] = {0, 0, 0, 0};
@@ -170,7 +173,11 @@ struct Enq {
   }
   void demag() {
     const Dims& d = c->d;
-    if (d.nz > 1) {
+    if (d.nz > 1 && c->use_yz) {
+      pre(MCQ_K_YZ);
+      launch_yz(d, c->yz, c->X, c->khat, c->tw, s);
+      post(MCQ_K_YZ);
+    } else if (d.nz > 1) {
       pre(MCQ_K_YFWD);
       launch_yfwd(d, c->X, c->Y, c->tw, s);
       post(MCQ_K_YFWD);
@@ -267,8 +274,12 @@ int capture(mcq_ctx* c, int which, double dt, int steps) {
   return MCQ_OK;
 }
 
+int demag_kernels(const mcq_ctx* c) {
+  return (c->d.nz > 1 && !c->use_yz) ? 3 : 1;
+}
+
 long long kernels_per_step(const mcq_ctx* c, bool llg) {
-  return 4LL * ((c->d.nz > 1 ? 3 : 1) + 1) + (llg ? 1 : 0);
+  return 4LL * (demag_kernels(c) + 1) + (llg ? 1 : 0);
 }
 
 int set_cav_state(mcq_ctx* c, double re, double im, double t, long long step) {
@@ -361,6 +372,32 @@ void free_all(mcq_ctx* c) {
   if (c->cap) cudaStreamDestroy(c->cap);
 }
 
+// Pick the demag schedule by timing both on this GPU (the spectra are all zero at create, which
+// does not change the cost): the cluster-fused y/z kernel moves ~3x fewer bytes but is
+// occupancy-limited by shared memory; the 3-pass y / z / y schedule streams more.
+int autotune_demag(mcq_ctx* c) {
+  cudaEvent_t e0, e1;
+  CK(c, cudaEventCreate(&e0));
+  CK(c, cudaEventCreate(&e1));
+  float ms[2] = {0.f, 0.f};
+  for (int path = 0; path < 2; ++path) {
+    c->use_yz = path == 1;
+    Enq q{c, c->stream};
+    for (int i = 0; i < 2; ++i) q.demag();
+    cudaEventRecord(e0, c->stream);
+    for (int i = 0; i < 5; ++i) q.demag();
+    cudaEventRecord(e1, c->stream);
+    if (cudaEventSynchronize(e1) != cudaSuccess) break;
+    cudaEventElapsedTime(&ms[path], e0, e1);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  CK(c, cudaGetLastError());
+  c->auto_yz = ms[1] < ms[0];
+  c->use_yz = c->auto_yz;
+  return MCQ_OK;
+}
+
 std::once_flag g_cfg_once;
 
 }  // namespace
@@ -394,7 +431,7 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
   d.Lz = padded(d.nz);
   d.N2 = d.Lx / 2;
   d.NKX = d.N2 + 1;
-  d.P = (d.NKX + 7) / 8 * 8;
+  d.P = d.NKX;
   d.N = (long long)d.nx * d.ny * d.nz;
   auto bail = [&](int code) {
     free_all(c);
@@ -414,9 +451,10 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
     return bail(MCQ_ECUDA);
   c->stream = (dist && dist->cuda_stream) ? (cudaStream_t)dist->cuda_stream : c->own;
   const size_t N3 = 3ULL * d.N;
-  const size_t nX = 3ULL * d.nz * d.ny * d.P;
-  const size_t nY = d.nz > 1 ? 3ULL * d.nz * d.Ly * d.P : 0;
-  const size_t nK = 6ULL * (d.Lz / 2 + 1) * (d.Ly / 2 + 1) * d.P;
+  c->yz = plan_yz(d);
+  const size_t nX = 3ULL * d.NKX * d.nz * d.ny;
+  const size_t nY = d.nz > 1 ? 3ULL * d.NKX * d.nz * d.Ly : 0;  // 3-pass schedule (and its timing)
+  const size_t nK = 6ULL * d.NKX * (d.Lz / 2 + 1) * (d.Ly / 2 + 1);
   c->nparts = update_grid_blocks(d);
   bool ok = cudaMalloc(&c->mN, N3 * 4) == cudaSuccess && cudaMalloc(&c->mA, N3 * 4) == cudaSuccess &&
             cudaMalloc(&c->mB, N3 * 4) == cudaSuccess && cudaMalloc(&c->acc, N3 * 4) == cudaSuccess &&
@@ -448,6 +486,7 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
   }
   if (build_khat(c, nullptr) != MCQ_OK) return bail(MCQ_ECUDA);
   if (reset_memory(c) != MCQ_OK) return bail(MCQ_ECUDA);
+  if (c->yz.ok && autotune_demag(c) != MCQ_OK) return bail(MCQ_ECUDA);
   *out = c;
   return MCQ_OK;
 }
@@ -753,8 +792,17 @@ int mcq_debug_layout(const mcq_ctx* c, long long out[6]) {
   out[1] = c->d.Ly;
   out[2] = c->d.Lz;
   out[3] = c->d.NKX;
-  out[4] = c->d.P;
+  out[4] = (c->d.nz > 1 && c->use_yz) ? c->yz.CS : 0;
   out[5] = c->nparts;
+  return MCQ_OK;
+}
+
+int mcq_debug_set_path(mcq_ctx* c, int path) {
+  if (!c || path < 0 || path > 2) return MCQ_EINVAL;
+  if (path == 2 && !c->yz.ok) return fail(c, MCQ_EINVAL, "fused y/z kernel not available for this grid");
+  CK(c, cudaStreamSynchronize(c->stream));
+  c->use_yz = path == 0 ? c->auto_yz : (path == 2);
+  invalidate_graphs(c);
   return MCQ_OK;
 }
 
@@ -765,7 +813,7 @@ int mcq_debug_tensor_octant(mcq_ctx* c, double* out) {
 
 int mcq_debug_khat(mcq_ctx* c, float* out) {
   if (!c || !out) return MCQ_EINVAL;
-  const size_t nK = 6ULL * (c->d.Lz / 2 + 1) * (c->d.Ly / 2 + 1) * c->d.P;
+  const size_t nK = 6ULL * c->d.NKX * (c->d.Lz / 2 + 1) * (c->d.Ly / 2 + 1);
   CK(c, cudaMemcpyAsync(out, c->khat, nK * 4, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
   return MCQ_OK;

@@ -35,20 +35,25 @@ __device__ __forceinline__ void reg_stage(float2 (&v)[NLT][E], float2* __restric
     constexpr int NB = E / R;
     constexpr bool LAST = (Ns * R == L);
 #pragma unroll
-    for (int l = 0; l < NLT; ++l) {
+    for (int q = 0; q < NB; ++q) {
+      const int b = t + q * TL;
+      const int k = b & (Ns - 1);
+      // twiddles depend only on the butterfly, so all NLT lines of the thread share them
+      float2 w[R];
 #pragma unroll
-      for (int q = 0; q < NB; ++q) {
-        const int b = t + q * TL;
-        const int k = b & (Ns - 1);
+      for (int r = 1; r < R; ++r) {
+        if (Ns > 1) {
+          w[r] = tw[(r * k * (L / (Ns * R))) * TWS];
+          if (INV) w[r].y = -w[r].y;
+        }
+      }
+#pragma unroll
+      for (int l = 0; l < NLT; ++l) {
         float2 x[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           x[r] = v[l][q + r * NB];
-          if (Ns > 1 && r > 0) {
-            float2 w = tw[(r * k * (L / (Ns * R))) * TWS];
-            if (INV) w.y = -w.y;
-            x[r] = cmul(x[r], w);
-          }
+          if (Ns > 1 && r > 0) x[r] = cmul(x[r], w[r]);
         }
         dft<R, INV>(x);
         if (LAST) {

@@ -1,16 +1,17 @@
 // update.cu — the fused per-stage update kernel K-U, the cavity kernel K-CAV and layout helpers.
 //
 // K-U (one launch per RK4 stage), one CTA = RY full x-rows at one z,
-// TL = N2/E threads per row; thread t of a row owns the packed positions n = t + TL*i (i < E),
-// i.e. the cell pairs x = 2n, 2n+1:
-//   A. demag x-C2R: Z_n = E_n + i O_n from the y/z-processed spectrum row X'[0..N2] (packed
-//      half-length real transform), register-resident inverse FFT -> z_n = B(2n) + i B(2n+1);
+// TL = N2/E threads per row; in the transform/cell phases thread t of a row owns the packed
+// positions n = t + TL*i (i < E), i.e. the cell pairs x = 2n, 2n+1:
+//   A. demag x-C2R: Z_n = E_n + i O_n from the y/z-processed spectrum X'[n][c][z][y] (packed
+//      half-length real transform; read with rows fastest, since the spectrum is kx-major, and
+//      staged through shared memory), register-resident inverse FFT -> z_n = B(2n) + i B(2n+1);
 //   B. per cell: B' = demag + B_ext + exchange (6-neighbour, C9) + anisotropy (C10)
 //      + B_rms (Gamma(t_s) + a sinc(w t_s)) (eq:bcav P:239), LLG torque (eq:llg P:184),
 //      RK4 stage combine + renormalisation (C1, C2); at stage 4 the overlap partial
 //      sum B_rms . m_{n+1} in fp64;
-//   C. packed forward FFT of m_{s+1} rows (still in registers) and the real-to-half-complex
-//      post-processing -> X[3][z][y][0..N2] for the next stage's y/z passes.
+//   C. packed forward FFT of m_{s+1} rows (still in registers), real-to-half-complex
+//      post-processing through shared memory -> X[k][c][z][y] (rows fastest again).
 // Ms is folded into the kernel spectrum, so the transforms act on m directly.
 #include "common.cuh"
 #include "regfft.cuh"
@@ -29,7 +30,10 @@ struct UCfg {
   static constexpr int RY0 = 128 / TL;
   static constexpr int RY = RY0 < 1 ? 1 : (RY0 > 16 ? 16 : RY0);
   static constexpr int NT = RY * TL;
-  static constexpr int PITCH = N2 + (N2 >= 16 ? N2 / 16 : 1);
+  // row pitch (complex): a pad slot every 16 positions, and pitch = 2 (mod 16) so that the
+  // rows-fastest spectrum mapping (8 rows x 2 positions per half-warp) hits distinct banks
+  static constexpr int P0 = N2 + (N2 >= 16 ? N2 / 16 : 1);
+  static constexpr int PITCH = P0 + ((2 - P0 % 16) + 16) % 16;
   static constexpr size_t SMEM = (size_t)(2 * N2 + 3 * RY * PITCH) * sizeof(float2);
 };
 
@@ -68,7 +72,7 @@ __device__ __forceinline__ float3 cell_update(const UpdateArgs& a, const float* 
                                               float3 Bd, float gsum, double& wacc, float& tmax) {
   const Dims& d = a.d;
   const long long N = d.N;
-  const float3 m = ld3(mS, N,idx);
+  const float3 m = ld3(mS, N, idx);
   if (a.mode == MODE_X0) return m;
   float3 B = make_float3(0.f, 0.f, 0.f);
   if (dot3(m, m) > 0.f) {
@@ -80,14 +84,14 @@ __device__ __forceinline__ float3 cell_update(const UpdateArgs& a, const float* 
     }
     if (a.terms & MCQ_TERM_EXCHANGE) {
       float3 acc = make_float3(0.f, 0.f, 0.f);
-#define MCQ_NB(COND, OFF, COEF)                  \
-  if (COND) {                                    \
-    const float3 mj = ld3(mS, N,idx + (OFF)); \
-    if (dot3(mj, mj) > 0.f) {                    \
-      acc.x += (COEF) * (mj.x - m.x);            \
-      acc.y += (COEF) * (mj.y - m.y);            \
-      acc.z += (COEF) * (mj.z - m.z);            \
-    }                                            \
+#define MCQ_NB(COND, OFF, COEF)                \
+  if (COND) {                                  \
+    const float3 mj = ld3(mS, N, idx + (OFF)); \
+    if (dot3(mj, mj) > 0.f) {                  \
+      acc.x += (COEF) * (mj.x - m.x);          \
+      acc.y += (COEF) * (mj.y - m.y);          \
+      acc.z += (COEF) * (mj.z - m.z);          \
+    }                                          \
   }
       MCQ_NB(x > 0, -1, a.ex[0])
       MCQ_NB(x < d.nx - 1, +1, a.ex[0])
@@ -185,12 +189,18 @@ __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const flo
   __shared__ float redf[32];
 
   const Dims& d = a.d;
-  const int yl = threadIdx.x / TL, t = threadIdx.x - yl * TL;
-  const int y0 = blockIdx.x * RY, z = blockIdx.y, y = y0 + yl;
+  const size_t kst = (size_t)3 * d.nz * d.ny;  // X stride between kx planes
+  const int y0 = blockIdx.x * RY, z = blockIdx.y;
+  // spectrum access mapping: rows fastest (a warp reads RY consecutive y of one kx column)
+  const int ylg = threadIdx.x % RY, tg = threadIdx.x / RY;
+  const bool rowg = y0 + ylg < d.ny;
+  // transform / cell mapping: positions fastest (a warp owns consecutive cell pairs of a row)
+  const int yl = threadIdx.x / TL, t = threadIdx.x % TL, y = y0 + yl;
   const bool rowok = y < d.ny;
   for (int m = threadIdx.x; m < LX; m += NT) tw[m] = gtw[m * (kTwMax / LX)];
   __syncthreads();
   const RowAddr<N2> A{yl};
+  const RowAddr<N2> Ag{ylg};
   float2 v[3][E];
 
   // ---------------- A: demag rows (packed x-C2R) ----------------
@@ -198,20 +208,26 @@ __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const flo
   if (use_demag) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const float2* row = a.X + ((size_t)(c * d.nz + z) * d.ny + (rowok ? y : 0)) * d.P;
+      const float2* col = a.X + ((size_t)c * d.nz + z) * d.ny + (rowg ? y0 + ylg : 0);  // X[.][c][z][y]
 #pragma unroll
       for (int i = 0; i < E; ++i) {
-        const int n = t + TL * i;
+        const int n = tg + TL * i;
         float2 zn = make_float2(0.f, 0.f);
-        if (rowok) {
-          const float2 xk = row[n], xn = cconj(row[N2 - n]);
+        if (rowg) {
+          const float2 xk = col[n * kst], xn = cconj(col[(N2 - n) * kst]);
           const float2 ev = cadd(xk, xn);
           const float2 od = cmul(csub(xk, xn), cconj(tw[n]));  // * w^{-n}
           zn = make_float2(ev.x - od.y, ev.y + od.x);           // E + i O
         }
-        v[c][i] = zn;
+        xs[Ag(c, n)] = zn;
       }
     }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int i = 0; i < E; ++i) v[c][i] = xs[A(c, t + TL * i)];
+    __syncthreads();
     reg_fft<N2, E, 3, true, 2>(v, xs, A, tw, t);
   } else {
 #pragma unroll
@@ -283,25 +299,25 @@ __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const flo
 
   // ---------------- C: packed x-R2C of the new rows ----------------
   reg_fft<N2, E, 3, false, 2>(v, xs, A, tw, t);
-  // X_k = (Z_k + conj Z_{N-k})/2 - i/2 w^k (Z_k - conj Z_{N-k}); partner via shared memory
+  // X_k = (Z_k + conj Z_{N-k})/2 - i/2 w^k (Z_k - conj Z_{N-k}); partners via shared memory
 #pragma unroll
   for (int c = 0; c < 3; ++c)
 #pragma unroll
     for (int i = 0; i < E; ++i) xs[A(c, t + TL * i)] = v[c][i];
   __syncthreads();
-  if (rowok) {
+  if (rowg) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      float2* row = a.X + ((size_t)(c * d.nz + z) * d.ny + y) * d.P;
+      float2* col = a.X + ((size_t)c * d.nz + z) * d.ny + y0 + ylg;
 #pragma unroll
       for (int i = 0; i < E; ++i) {
-        const int k = t + TL * i;
-        const float2 zk = v[c][i];
-        const float2 zn = cconj(xs[A(c, (N2 - k) & (N2 - 1))]);
+        const int k = tg + TL * i;
+        const float2 zk = xs[Ag(c, k)];
+        const float2 zn = cconj(xs[Ag(c, (N2 - k) & (N2 - 1))]);
         const float2 ev = cadd(zk, zn);
         const float2 wd = cmul(tw[k], csub(zk, zn));
-        row[k] = make_float2(0.5f * (ev.x + wd.y), 0.5f * (ev.y - wd.x));
-        if (k == 0) row[N2] = make_float2(zk.x - zk.y, 0.f);  // Nyquist: Re Z0 - Im Z0
+        col[k * kst] = make_float2(0.5f * (ev.x + wd.y), 0.5f * (ev.y - wd.x));
+        if (k == 0) col[N2 * kst] = make_float2(zk.x - zk.y, 0.f);  // Nyquist: Re Z0 - Im Z0
       }
     }
   }
