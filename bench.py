@@ -94,7 +94,7 @@ def alg_bytes(L, grid, has_map):
     Y = 3 * nz * Ly * nkx * 8
     K = 6 * (Lz // 2 + 1) * (Ly // 2 + 1) * nkx * 4
     state = (36 + 60 + 60 + 48) / 4 * N           # RK4 state traffic averaged over the 4 stages
-    out = {"yfwd": X + Y, "zconv": 2 * Y + K, "yinv": Y + X, "yz": 2 * X + K,
+    out = {"yfwd": X + Y, "zconv": 2 * Y + K, "yinv": Y + X,
            "y2d": 2 * X + 6 * ((Ly // 2 + 1) * nkx * 4),
            "update": 2 * X + state + (12 * N if has_map else 0), "cavity": 0}
     return out
@@ -102,8 +102,6 @@ def alg_bytes(L, grid, has_map):
 
 def step_alg_bytes(L, grid, has_map):
     b = alg_bytes(L, grid, has_map)
-    if grid[2] > 1 and L.get("yz_cluster", 0) > 0:
-        return 4 * (b["yz"] + b["update"])
     if grid[2] > 1:
         return 4 * (b["yfwd"] + b["zconv"] + b["yinv"] + b["update"])
     return 4 * (b["y2d"] + b["update"])
@@ -176,8 +174,6 @@ def main():
     ap.add_argument("--impl", default="mcq", choices=["mcq", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=5)
-    ap.add_argument("--demag-path", default="auto", choices=["auto", "3pass"],
-                    help="auto: cluster-fused y/z kernel when the kx plane fits; 3pass: force y/z/y")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -195,19 +191,12 @@ def main():
     import paper_2410_00966_b200 as mcq
     from synth import make_config
 
+    from paper_2410_00966_b200.replicas import replica_bias, max_over_ranks
     cfg = make_config(args.config)
-    if world > 1:   # replica r: bias-field sweep point (anticrossing), same cost per rank
-        from synth.configs import bias_sweep
-        b = np.asarray(cfg.bext, float)
-        nrm = float(np.linalg.norm(b))
-        if nrm > 0:
-            pts = bias_sweep(nrm, n=world, rel=0.1) if world > 1 else [nrm]
-            cfg.bext = tuple(b / nrm * pts[rank])
+    cfg.bext = replica_bias(cfg.bext, world, rank)  # replica r: its bias-field sweep point
     stream = torch.cuda.Stream()          # a real stream: the library's kernels and our events share it
     torch.cuda.set_stream(stream)
     solver = mcq.Solver.from_config(cfg, stream=stream.cuda_stream)
-    if args.demag_path == "3pass":
-        mcq.mcq_debug_set_path(solver.ctx, 1)
     if cfg.relax_first:
         solver.relax(cfg.dt * 0.5, 1e-3, 2000)
         mcq.mcq_reset_memory(solver.ctx)
@@ -230,11 +219,7 @@ def main():
         ev1.record(stream)
         barrier()
     launches = mcq.mcq_kernel_launches(solver.ctx) - launches0
-    ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms], device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = max_over_ranks(ev0.elapsed_time(ev1), device="cuda")
     value = cfg.n * args.steps * world / (ms_max * 1e-3)
 
     # e2e through the public API with host buffers: set_m (H2D) + run + get_m (D2H)
@@ -247,11 +232,8 @@ def main():
     solver.run(cfg.dt, e2e_steps)
     mcq.mcq_get_m(solver.ctx, cfg.n, out_host.numpy().reshape(-1))
     torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], device="cuda")
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_val = cfg.n * e2e_steps * world / float(te.item())
+    e2e_s = max_over_ranks(time.perf_counter() - t0, device="cuda")
+    e2e_val = cfg.n * e2e_steps * world / e2e_s
 
     # per-kernel timing (CUDA events around each launch, same stream) -> roofline of the top kernel
     prof = mcq.mcq_profile_run(solver.ctx, cfg.dt, args.profile_steps)

@@ -64,8 +64,7 @@ extern "C" {
 #define MCQ_K_Y2D 3    /* y-forward * Khat * y-inverse pass (nz == 1)     */
 #define MCQ_K_UPDATE 4 /* fused x-C2R + fields + torque + RK4 + x-R2C     */
 #define MCQ_K_CAVITY 5 /* overlap finalize + cavity state update          */
-#define MCQ_K_YZ 6     /* cluster-fused y-fwd * z-fwd * Khat * z-inv * y-inv (3D) */
-#define MCQ_NKCLASS 7
+#define MCQ_NKCLASS 6
 
 typedef struct mcq_ctx mcq_ctx; /* opaque, library-owned */
 
@@ -172,17 +171,13 @@ MCQ_API long long mcq_kernel_launches(const mcq_ctx *);
 MCQ_API int mcq_profile_run(mcq_ctx *, double dt, long long steps, double *kernel_ms, int *per_step);
 
 /* Padded layout: out[0..5] = Lx, Ly, Lz (zero-padded FFT lengths: next power of two >= 2n,
- * 1 if n == 1), NKX = Lx/2+1 (x-spectrum columns), the cluster size of the fused y/z demag
- * kernel (0 = 3-pass fallback or nz == 1), number of per-CTA overlap partials. */
+ * 1 if n == 1), NKX = Lx/2+1 (x-spectrum columns), P (row pitch of the spectra in complex
+ * elements: NKX rounded up to even), number of per-CTA overlap partials. */
 MCQ_API int mcq_debug_layout(const mcq_ctx *, long long out[6]);
-/* Test hook for the demag schedule of 3D grids: path 0 = automatic (the faster of the two, timed
- * at mcq_create), 1 = force the 3-pass y / z / y schedule, 2 = force the cluster-fused y/z
- * kernel (EINVAL if the kx plane does not fit a cluster).  Invalidates captured graphs. */
-MCQ_API int mcq_debug_set_path(mcq_ctx *, int path);
 /* Real-space demag tensor octant, fp64 (6, Lz/2+1, Ly/2+1, Lx/2+1) in XX,YY,ZZ,XY,XZ,YZ
  * order, for index offsets (i, j, k); zero where i >= nx, j >= ny or k >= nz. */
 MCQ_API int mcq_debug_tensor_octant(mcq_ctx *, double *out);
-/* Folded kernel spectrum, fp32 (NKX, 6, Lz/2+1, Ly/2+1), kx-major:
+/* Folded kernel spectrum, fp32 (6, Lz/2+1, Ly/2+1, P), kx fastest:
  * Khat = -mu0 Ms/(Lx Ly Lz) DFT(N) (real: every component is even or odd along each axis). */
 MCQ_API int mcq_debug_khat(mcq_ctx *, float *out);
 

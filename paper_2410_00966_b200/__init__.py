@@ -12,8 +12,7 @@ import numpy as np
 
 from ._lib import (lib, MCQError, mcq_aniso, mcq_dist, mcq_cavity_state, EXPORTED,  # noqa: F401
                    TERM_ZEEMAN, TERM_EXCHANGE, TERM_ANIS, TERM_DEMAG, TERM_CAVITY, TERM_EXCITATION,
-                   TERM_ALL, NKCLASS, KCLASS_NAMES, K_YFWD, K_ZCONV, K_YINV, K_Y2D, K_UPDATE, K_CAVITY,
-                   K_YZ)
+                   TERM_ALL, NKCLASS, KCLASS_NAMES, K_YFWD, K_ZCONV, K_YINV, K_Y2D, K_UPDATE, K_CAVITY)
 
 __all__ = [n for n in EXPORTED] + ["Solver", "MCQError"]
 
@@ -172,11 +171,7 @@ def mcq_profile_run(ctx, dt, steps):
 def mcq_debug_layout(ctx):
     out = (C.c_longlong * 6)()
     _check(ctx, lib.mcq_debug_layout(ctx, out))
-    return dict(zip(("Lx", "Ly", "Lz", "NKX", "yz_cluster", "n_partials"), list(out)))
-
-
-def mcq_debug_set_path(ctx, path):
-    _check(ctx, lib.mcq_debug_set_path(ctx, int(path)))
+    return dict(zip(("Lx", "Ly", "Lz", "NKX", "P", "n_partials"), list(out)))
 
 
 def mcq_debug_tensor_octant(ctx):
@@ -189,10 +184,10 @@ def mcq_debug_tensor_octant(ctx):
 
 def mcq_debug_khat(ctx):
     L = mcq_debug_layout(ctx)
-    shape = (L["NKX"], 6, L["Lz"] // 2 + 1, L["Ly"] // 2 + 1)
+    shape = (6, L["Lz"] // 2 + 1, L["Ly"] // 2 + 1, L["P"])
     out = np.empty(shape, np.float32)
     _check(ctx, lib.mcq_debug_khat(ctx, out.ctypes.data))
-    return out
+    return out[..., :L["NKX"]]
 
 
 def mcq_last_error(ctx):

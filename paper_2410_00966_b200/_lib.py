@@ -14,9 +14,9 @@ LIB_PATH = os.path.join(HERE, "libmcq.so")
 MCQ_OK, MCQ_EINVAL, MCQ_ESTATE, MCQ_ENOMEM, MCQ_ECUDA, MCQ_ENCCL = 0, -1, -2, -3, -4, -5
 TERM_ZEEMAN, TERM_EXCHANGE, TERM_ANIS, TERM_DEMAG, TERM_CAVITY, TERM_EXCITATION = 1, 2, 4, 8, 16, 32
 TERM_ALL = 63
-K_YFWD, K_ZCONV, K_YINV, K_Y2D, K_UPDATE, K_CAVITY, K_YZ = range(7)
-NKCLASS = 7
-KCLASS_NAMES = ("yfwd", "zconv", "yinv", "y2d", "update", "cavity", "yz")
+K_YFWD, K_ZCONV, K_YINV, K_Y2D, K_UPDATE, K_CAVITY = range(6)
+NKCLASS = 6
+KCLASS_NAMES = ("yfwd", "zconv", "yinv", "y2d", "update", "cavity")
 
 
 class mcq_aniso(C.Structure):
@@ -74,7 +74,6 @@ _sig = {
     "mcq_kernel_launches": (C.c_longlong, [_P]),
     "mcq_profile_run": (C.c_int, [_P, C.c_double, C.c_longlong, C.POINTER(C.c_double), C.POINTER(C.c_int)]),
     "mcq_debug_layout": (C.c_int, [_P, C.POINTER(C.c_longlong)]),
-    "mcq_debug_set_path": (C.c_int, [_P, C.c_int]),
     "mcq_debug_tensor_octant": (C.c_int, [_P, _P]),
     "mcq_debug_khat": (C.c_int, [_P, _P]),
     "mcq_last_error": (C.c_char_p, [_P]),

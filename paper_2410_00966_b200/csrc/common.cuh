@@ -10,26 +10,17 @@ constexpr double kMu0 = 4e-7 * 3.14159265358979323846;
 constexpr double kHbar = 1.05457182e-34;         // J s
 constexpr int kTwMax = 1024;                     // global twiddle table length (max FFT length)
 
-// Sizes of one context's padded spectral layout.  Spectra are kx-major (a kx plane is one
-// contiguous block, so the fused y/z kernel streams it with unit stride):
-//   X[kx][c][z][y]   complex64, NKX*3*nz*ny          (x-spectrum of m; demag spectrum in place)
-//   Y[kx][c][z][ky]  complex64, NKX*3*nz*Ly          (3-pass fallback only)
-//   Khat[kx][g][kz][ky] fp32, NKX*6*(Lz/2+1)*(Ly/2+1) (real, folded; g = XX,YY,ZZ,XY,XZ,YZ)
+// Sizes of one context's padded spectral layout.  Row layout, kx fastest:
+//   X[c][z][y][P]    complex64 (x-spectrum of m; the demag spectrum in place), rows 16-byte aligned
+//   Y[c][z][ky][P]   complex64 (after the y transform; only the nz real z planes)
+//   Khat[g][kz][ky][P] fp32, kz <= Lz/2, ky <= Ly/2 (real, folded; g = XX,YY,ZZ,XY,XZ,YZ)
 struct Dims {
   int nx, ny, nz;     // grid
   int Lx, Ly, Lz;     // zero-padded FFT lengths (next pow2 >= 2n; 1 if n == 1)
   int N2;             // Lx / 2: complex length of the packed real x-transform
   int NKX;            // Lx / 2 + 1: x-spectrum columns (Hermitian half)
-  int P;              // unused (kept = NKX for the debug layout call)
+  int P;              // row pitch of the spectra (complex), NKX rounded up to even
   long long N;        // nx * ny * nz
-};
-
-// Launch plan of the cluster-fused y/z kernel (passes.cu): cluster of CS CTAs per kx plane,
-// ZS z-planes per CTA, KC ky per phase-2 chunk, NT threads, smem bytes.
-struct YZPlan {
-  bool ok;
-  int CS, ZS, KC, NT;
-  size_t smem;
 };
 
 // Cavity state on the device (fp64), advanced once per step by k_cavity (a13).
@@ -86,10 +77,11 @@ struct UpdateArgs {
 // ---------------------------------------------------------------- launchers
 // passes.cu
 void configure_pass_kernels();
-YZPlan plan_yz(const Dims& d);
-void launch_yz(const Dims& d, const YZPlan& p, float2* X, const float* khat, const float2* tw, cudaStream_t s);
 void launch_yfwd(const Dims& d, const float2* X, float2* Y, const float2* tw, cudaStream_t s);
 void launch_zconv(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t s);
+int zconv_tma_box_c(int Lz);  // kx columns per K-Z tile of the TMA-pipelined variant
+void launch_zconv_tma(const Dims& d, const void* tmap /* CUtensorMap over Y */, float2* Y, const float* khat,
+                      const float2* tw, cudaStream_t s);
 void launch_yinv(const Dims& d, const float2* Y, float2* X, const float2* tw, cudaStream_t s);
 void launch_y2d(const Dims& d, float2* X, const float* khat, const float2* tw, cudaStream_t s);
 // update.cu

@@ -7,6 +7,8 @@
 // Steps are captured once into CUDA graphs and replayed; the host never synchronises inside
 // mcq_run.  Device memory is owned by the context (cudaMalloc); work runs on the context
 // stream (library-owned, or the caller's via mcq_set_stream).
+#include <cuda.h>  // CUtensorMap; cuTensorMapEncodeTiled is fetched with cudaGetDriverEntryPoint
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -47,13 +49,12 @@ struct mcq_ctx {
   int* bad = nullptr;
   float* io = nullptr;
   bool m_set = false;
-  YZPlan yz{};        // cluster-fused y/z plan (ok == false: 3-pass fallback)
-  bool use_yz = false;   // demag schedule in use (fused y/z cluster kernel vs 3-pass)
-  bool auto_yz = false;  // the schedule picked by timing both at create
   // graphs: [0] = 1 LLG step, [1] = kGraphSteps LLG steps, [2] = 1 relax step, [3] = relax chunk
   cudaGraphExec_t g[4] = {nullptr, nullptr, nullptr, nullptr};
   double g_dt[4] = {0, 0, 0, 0};
   long long launches = 0;
+  alignas(64) CUtensorMap tmz;  // TMA descriptor of Y for the pipelined K-Z kernel
+  bool have_tmz = false;
   std::string err;
 };
 
@@ -173,16 +174,15 @@ struct Enq {
   }
   void demag() {
     const Dims& d = c->d;
-    if (d.nz > 1 && c->use_yz) {
-      pre(MCQ_K_YZ);
-      launch_yz(d, c->yz, c->X, c->khat, c->tw, s);
-      post(MCQ_K_YZ);
-    } else if (d.nz > 1) {
+    if (d.nz > 1) {
       pre(MCQ_K_YFWD);
       launch_yfwd(d, c->X, c->Y, c->tw, s);
       post(MCQ_K_YFWD);
       pre(MCQ_K_ZCONV);
-      launch_zconv(d, c->Y, c->khat, c->tw, s);
+      if (c->have_tmz)
+        launch_zconv_tma(d, &c->tmz, c->Y, c->khat, c->tw, s);
+      else
+        launch_zconv(d, c->Y, c->khat, c->tw, s);
       post(MCQ_K_ZCONV);
       pre(MCQ_K_YINV);
       launch_yinv(d, c->Y, c->X, c->tw, s);
@@ -275,7 +275,7 @@ int capture(mcq_ctx* c, int which, double dt, int steps) {
 }
 
 int demag_kernels(const mcq_ctx* c) {
-  return (c->d.nz > 1 && !c->use_yz) ? 3 : 1;
+  return c->d.nz > 1 ? 3 : 1;
 }
 
 long long kernels_per_step(const mcq_ctx* c, bool llg) {
@@ -372,30 +372,32 @@ void free_all(mcq_ctx* c) {
   if (c->cap) cudaStreamDestroy(c->cap);
 }
 
-// Pick the demag schedule by timing both on this GPU (the spectra are all zero at create, which
-// does not change the cost): the cluster-fused y/z kernel moves ~3x fewer bytes but is
-// occupancy-limited by shared memory; the 3-pass y / z / y schedule streams more.
-int autotune_demag(mcq_ctx* c) {
-  cudaEvent_t e0, e1;
-  CK(c, cudaEventCreate(&e0));
-  CK(c, cudaEventCreate(&e1));
-  float ms[2] = {0.f, 0.f};
-  for (int path = 0; path < 2; ++path) {
-    c->use_yz = path == 1;
-    Enq q{c, c->stream};
-    for (int i = 0; i < 2; ++i) q.demag();
-    cudaEventRecord(e0, c->stream);
-    for (int i = 0; i < 5; ++i) q.demag();
-    cudaEventRecord(e1, c->stream);
-    if (cudaEventSynchronize(e1) != cudaSuccess) break;
-    cudaEventElapsedTime(&ms[path], e0, e1);
+// TMA descriptor of Y[3][nz][Ly][P] viewed as a 3D tensor (P, Ly, 3 nz) of 8-byte elements;
+// box (C, 1, nz) = one component's z column block of a K-Z tile.  Without it (nz > 256, or no
+// driver entry point) K-Z falls back to plain loads.
+void make_y_tensor_map(mcq_ctx* c) {
+  const Dims& d = c->d;
+  c->have_tmz = false;
+  if (d.nz < 2 || d.nz > 256 || !c->Y) return;
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+      cudaGetLastError();
+      return;
+    }
+    enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
   }
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  CK(c, cudaGetLastError());
-  c->auto_yz = ms[1] < ms[0];
-  c->use_yz = c->auto_yz;
-  return MCQ_OK;
+  const cuuint64_t dims[3] = {(cuuint64_t)d.P, (cuuint64_t)d.Ly, (cuuint64_t)3 * d.nz};
+  const cuuint64_t strides[2] = {(cuuint64_t)d.P * 8, (cuuint64_t)d.Ly * d.P * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)zconv_tma_box_c(d.Lz), 1, (cuuint32_t)d.nz};
+  const cuuint32_t es[3] = {1, 1, 1};
+  if (box[0] == 0) return;
+  const CUresult r = enc(&c->tmz, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->Y, dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  c->have_tmz = (r == CUDA_SUCCESS);
 }
 
 std::once_flag g_cfg_once;
@@ -431,7 +433,7 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
   d.Lz = padded(d.nz);
   d.N2 = d.Lx / 2;
   d.NKX = d.N2 + 1;
-  d.P = d.NKX;
+  d.P = (d.NKX + 1) / 2 * 2;  // even: every spectrum row is 16-byte aligned (TMA row copies)
   d.N = (long long)d.nx * d.ny * d.nz;
   auto bail = [&](int code) {
     free_all(c);
@@ -451,10 +453,9 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
     return bail(MCQ_ECUDA);
   c->stream = (dist && dist->cuda_stream) ? (cudaStream_t)dist->cuda_stream : c->own;
   const size_t N3 = 3ULL * d.N;
-  c->yz = plan_yz(d);
-  const size_t nX = 3ULL * d.NKX * d.nz * d.ny;
-  const size_t nY = d.nz > 1 ? 3ULL * d.NKX * d.nz * d.Ly : 0;  // 3-pass schedule (and its timing)
-  const size_t nK = 6ULL * d.NKX * (d.Lz / 2 + 1) * (d.Ly / 2 + 1);
+  const size_t nX = 3ULL * d.nz * d.ny * d.P;
+  const size_t nY = d.nz > 1 ? 3ULL * d.nz * d.Ly * d.P : 0;
+  const size_t nK = 6ULL * (d.Lz / 2 + 1) * (d.Ly / 2 + 1) * d.P;
   c->nparts = update_grid_blocks(d);
   bool ok = cudaMalloc(&c->mN, N3 * 4) == cudaSuccess && cudaMalloc(&c->mA, N3 * 4) == cudaSuccess &&
             cudaMalloc(&c->mB, N3 * 4) == cudaSuccess && cudaMalloc(&c->acc, N3 * 4) == cudaSuccess &&
@@ -485,8 +486,8 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
     if (cudaMemcpy(c->tw, h.data(), kTwMax * 8, cudaMemcpyHostToDevice) != cudaSuccess) return bail(MCQ_ECUDA);
   }
   if (build_khat(c, nullptr) != MCQ_OK) return bail(MCQ_ECUDA);
+  make_y_tensor_map(c);
   if (reset_memory(c) != MCQ_OK) return bail(MCQ_ECUDA);
-  if (c->yz.ok && autotune_demag(c) != MCQ_OK) return bail(MCQ_ECUDA);
   *out = c;
   return MCQ_OK;
 }
@@ -792,17 +793,8 @@ int mcq_debug_layout(const mcq_ctx* c, long long out[6]) {
   out[1] = c->d.Ly;
   out[2] = c->d.Lz;
   out[3] = c->d.NKX;
-  out[4] = (c->d.nz > 1 && c->use_yz) ? c->yz.CS : 0;
+  out[4] = c->d.P;
   out[5] = c->nparts;
-  return MCQ_OK;
-}
-
-int mcq_debug_set_path(mcq_ctx* c, int path) {
-  if (!c || path < 0 || path > 2) return MCQ_EINVAL;
-  if (path == 2 && !c->yz.ok) return fail(c, MCQ_EINVAL, "fused y/z kernel not available for this grid");
-  CK(c, cudaStreamSynchronize(c->stream));
-  c->use_yz = path == 0 ? c->auto_yz : (path == 2);
-  invalidate_graphs(c);
   return MCQ_OK;
 }
 
@@ -813,7 +805,7 @@ int mcq_debug_tensor_octant(mcq_ctx* c, double* out) {
 
 int mcq_debug_khat(mcq_ctx* c, float* out) {
   if (!c || !out) return MCQ_EINVAL;
-  const size_t nK = 6ULL * c->d.NKX * (c->d.Lz / 2 + 1) * (c->d.Ly / 2 + 1);
+  const size_t nK = 6ULL * (c->d.Lz / 2 + 1) * (c->d.Ly / 2 + 1) * c->d.P;
   CK(c, cudaMemcpyAsync(out, c->khat, nK * 4, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
   return MCQ_OK;

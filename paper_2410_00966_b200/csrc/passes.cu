@@ -1,260 +1,113 @@
 // passes.cu — the y and z passes of the zero-padded demag FFT convolution (a2-a4 of SURVEY §8(a)).
 //
 // B_demag = -mu0 IFFT( Khat . FFT(M) ) restricted to the grid, with M = Ms m zero-padded to
-// (Lx, Ly, Lz) (reading C11).  The x transforms live in the update kernel (update.cu).  All
-// spectra are kx-major: X[kx][c][z][y], Y[kx][c][z][ky], Khat[kx][6][kz][ky] (common.cuh).
-//
-//   K-YZ  (k_yz, default for 3D grids whose kx plane fits a cluster): one thread-block cluster
-//         per kx plane.  Phase 1: each CTA y-transforms its z-slab (ny -> Ly, pruned input) into
-//         its shared memory.  Phase 2: each CTA takes a ky-slab, gathers the z lines from all
-//         CTAs' shared memory (DSMEM), z-transforms (nz -> Lz), multiplies by Khat, inverse
-//         z-transforms and scatters the nz kept values back.  Phase 3: inverse y, keep ny rows,
-//         write X in place.  HBM traffic: read X, read Khat, write X — the Y round trips of the
-//         3-pass schedule never happen.
-//   3-pass fallback (planes too large for a cluster, e.g. 512x512x256):
-//   K-Y   (k_yfwd):  X -> Y, forward along y;   K-Z (k_zconv): z fwd * Khat * z inv on Y;
-//   K-YI  (k_yinv):  Y -> X, inverse along y.
-//   K-Y2D (k_y2d):   nz == 1: forward y, Khat multiply, inverse y in one pass, in place on X.
-// Lines are transformed with the register-resident FFT of regfft.cuh.
-#include <cooperative_groups.h>
+// (Lx, Ly, Lz) (reading C11).  The x transforms live in the update kernel (update.cu); here,
+// with the row layout of common.cuh (kx fastest):
+//   K-Y  (k_yfwd):  X[3][nz][ny][P] -> Y[3][nz][Ly][P], forward along y, input rows >= ny are 0
+//   K-Z  (k_zconv): per (ky, kx) column of Y: forward along z (planes >= nz are 0), the
+//                   symmetric 3x3 multiply by the real folded Khat, inverse along z, keep nz
+//   K-YI (k_yinv):  Y -> X, inverse along y, keep the first ny rows
+//   K-Y2D(k_y2d):   nz == 1: forward y, Khat multiply, inverse y in one pass, in place on X
+// A CTA owns C adjacent kx columns (a warp's global accesses are contiguous C*8-byte row
+// segments).  Lines are transformed with the register-resident FFT of regfft.cuh: data go
+// HBM -> registers -> (S-1 smem exchanges) -> registers -> HBM; K-Z / K-Y2D keep the three
+// components of a column in one thread and multiply by Khat in registers between the forward
+// and the inverse transform.
+// (A thread-block-cluster variant fusing y and z per kx plane through DSMEM was built and
+// measured 2-3x slower than this schedule on B200 — shared-memory-limited occupancy in a
+// compute-bound pass.)
+#include <cuda.h>  // CUtensorMap (the encode call itself goes through cudaGetDriverEntryPoint)
+
+#include <cstdlib>
 
 #include "common.cuh"
 #include "regfft.cuh"
-
-namespace cg = cooperative_groups;
+#include "tma.cuh"
 
 namespace mcq {
 
 template <int L>
-__device__ __forceinline__ void load_tw(float2* tw, const float2* __restrict__ gtw) {
-  for (int m = threadIdx.x; m < L; m += blockDim.x) tw[m] = gtw[m * (kTwMax / L)];
-}
-
-template <int L>
-struct RowPitch {  // padded row of L complex: one pad slot every 16 (conflict-free radix-16 stores)
-  static constexpr int P = L + (L >= 16 ? L / 16 : 1);
-  __device__ static __forceinline__ int at(int pos) { return pos + (L >= 16 ? (pos >> 4) : 0); }
-};
-
-template <int L>
-struct RowA {  // shared-memory address of element pos of row `line`
-  int line;
-  __device__ __forceinline__ int operator()(int, int pos) const { return line * RowPitch<L>::P + RowPitch<L>::at(pos); }
-};
-
-// B_g = sum_h Khat_gh M_h for row g of the symmetric tensor, with the fold signs
-// (XY odd in y, XZ odd in z, YZ odd in both; kx is never folded).
-struct KRow {
-  int cd, co0, co1, h0, h1;
-  __device__ __forceinline__ explicit KRow(int g)
-      : cd(g), co0(g == 2 ? 4 : 3), co1(g == 0 ? 4 : 5), h0(g == 0 ? 1 : 0), h1(g == 2 ? 1 : 2) {}
-};
-
-__device__ __forceinline__ float fold_sign(int comp, float sy, float sz) {
-  return comp == 3 ? sy : (comp == 4 ? sz : (comp == 5 ? sy * sz : 1.f));
-}
-
-// ====================================================================== K-YZ (cluster)
-template <int LY, int LZ>
-struct YZCfg {
-  static constexpr int EY = LY < 16 ? LY : 16;
-  static constexpr int TLY = LY / EY;
-  static constexpr int EZ = LZ <= 16 ? LZ : 8;
-  static constexpr int TLZ = LZ / EZ;
-  static constexpr int PY = RowPitch<LY>::P;
-};
-
-template <int LY, int LZ>
-__global__ void __launch_bounds__(512) k_yz(float2* __restrict__ X, const float* __restrict__ khat, Dims d,
-                                             const float2* __restrict__ gtw, int ZS, int KC) {
-  using Cf = YZCfg<LY, LZ>;
-  constexpr int EY = Cf::EY, TLY = Cf::TLY, EZ = Cf::EZ, TLZ = Cf::TLZ, PY = Cf::PY;
-  cg::cluster_group cl = cg::this_cluster();
-  const int CS = (int)cl.num_blocks();
-  const int rank = (int)cl.block_rank();
-  const int kx = blockIdx.x / CS;
-  extern __shared__ float2 sm[];
-  float2* twy = sm;
-  float2* twz = sm + LY;
-  float2* ybuf = sm + LY + LZ;                 // [3][ZS][PY]: y-spectra of this CTA's z-slab
-  float2* xch = ybuf + 3 * ZS * PY;            // [3][LZ][KC]: z-line exchange buffer
-  load_tw<LY>(twy, gtw);
-  load_tw<LZ>(twz, gtw);
-  __syncthreads();
-  const int tid = threadIdx.x;
-  const int nz = d.nz, ny = d.ny;
-
-  // ---------------- phase 1: forward y on the z-slab ----------------
-  const int line = tid / TLY, ty = tid - line * TLY;  // line = comp * ZS + zl
-  const int comp1 = line / ZS, z1 = rank * ZS + (line - comp1 * ZS);
-  float2* xrow = X + ((size_t)(kx * 3 + comp1) * nz + z1) * ny;
-  {
-    float2 v[1][EY];
-#pragma unroll
-    for (int i = 0; i < EY; ++i) {
-      const int p = ty + TLY * i;
-      v[0][i] = p < ny ? xrow[p] : make_float2(0.f, 0.f);
-    }
-    const RowA<LY> A{line};
-    reg_fft<LY, EY, 1, false>(v, ybuf, A, twy, ty);
-#pragma unroll
-    for (int i = 0; i < EY; ++i) ybuf[A(0, ty + TLY * i)] = v[0][i];
-  }
-  cl.sync();
-
-  // ---------------- phase 2: z fwd * Khat * z inv on this CTA's ky-slab ----------------
-  {
-    const int KS = LY / CS, ky0 = rank * KS;
-    const int kyl = tid % KC, rest = tid / KC, g = rest % 3, tz = rest / 3;
-    const KRow kr(g);
-    const int HY = LY / 2 + 1, HZ = LZ / 2 + 1;
-    const float* kb = khat + (size_t)kx * 6 * HZ * HY;
-    struct XA {
-      int g, kyl, KC;
-      __device__ __forceinline__ int operator()(int, int pos) const { return (g * LZ + pos) * KC + kyl; }
-    } A{g, kyl, KC};
-    const int nchunk = (KS + KC - 1) / KC;
-    for (int ch = 0; ch < nchunk; ++ch) {
-      const int kys = ch * KC + kyl;
-      const bool ok = kys < KS;
-      const int ky = ky0 + (ok ? kys : 0);
-      const int yoff = RowPitch<LY>::at(ky);
-      float2 v[1][EZ];
-#pragma unroll
-      for (int i = 0; i < EZ; ++i) {
-        const int z = tz + TLZ * i;
-        float2 val = make_float2(0.f, 0.f);
-        if (ok && z < nz) {
-          const int q = z / ZS;
-          const float2* rb = cl.map_shared_rank(ybuf, q);
-          val = rb[(g * ZS + (z - q * ZS)) * PY + yoff];
-        }
-        v[0][i] = val;
-      }
-      reg_fft<LZ, EZ, 1, false>(v, xch, A, twz, tz);
-#pragma unroll
-      for (int i = 0; i < EZ; ++i) xch[A(0, tz + TLZ * i)] = v[0][i];
-      __syncthreads();
-      if (ok) {
-        const int kyf = ky <= LY / 2 ? ky : LY - ky;
-        const float sy = ky <= LY / 2 ? 1.f : -1.f;
-#pragma unroll
-        for (int i = 0; i < EZ; ++i) {
-          const int kz = tz + TLZ * i;
-          const int kzf = kz <= LZ / 2 ? kz : LZ - kz;
-          const float sz = kz <= LZ / 2 ? 1.f : -1.f;
-          const size_t b = (size_t)kzf * HY + kyf;
-          const float kd = __ldg(kb + (size_t)kr.cd * HZ * HY + b);
-          const float k0 = fold_sign(kr.co0, sy, sz) * __ldg(kb + (size_t)kr.co0 * HZ * HY + b);
-          const float k1 = fold_sign(kr.co1, sy, sz) * __ldg(kb + (size_t)kr.co1 * HZ * HY + b);
-          const float2 md = v[0][i];
-          const float2 m0 = xch[(kr.h0 * LZ + kz) * KC + kyl], m1 = xch[(kr.h1 * LZ + kz) * KC + kyl];
-          v[0][i] = make_float2(kd * md.x + k0 * m0.x + k1 * m1.x, kd * md.y + k0 * m0.y + k1 * m1.y);
-          if ((i & 3) == 3) asm volatile("" ::: "memory");
-        }
-      }
-      __syncthreads();
-      reg_fft<LZ, EZ, 1, true>(v, xch, A, twz, tz);
-#pragma unroll
-      for (int i = 0; i < EZ; ++i) {
-        const int z = tz + TLZ * i;
-        if (ok && z < nz) {
-          const int q = z / ZS;
-          float2* rb = cl.map_shared_rank(ybuf, q);
-          rb[(g * ZS + (z - q * ZS)) * PY + yoff] = v[0][i];
-        }
-      }
-    }
-  }
-  cl.sync();
-
-  // ---------------- phase 3: inverse y, keep ny rows ----------------
-  {
-    const RowA<LY> A{line};
-    float2 v[1][EY];
-#pragma unroll
-    for (int i = 0; i < EY; ++i) v[0][i] = ybuf[A(0, ty + TLY * i)];
-    __syncthreads();
-    reg_fft<LY, EY, 1, true>(v, ybuf, A, twy, ty);
-#pragma unroll
-    for (int i = 0; i < EY; ++i) {
-      const int p = ty + TLY * i;
-      if (p < ny) xrow[p] = v[0][i];
-    }
-  }
-}
-
-// ====================================================================== 3-pass fallback
-template <int L>
-struct RowCfg {  // contiguous-line passes (K-Y, K-YI): LPB lines per CTA
+struct PassCfg {  // single-component passes (K-Y, K-YI)
   static constexpr int E = L < 16 ? L : 16;
   static constexpr int TL = L / E;
-  static constexpr int LPB0 = 256 / TL;
-  static constexpr int LPB = LPB0 < 1 ? 1 : LPB0;
-  static constexpr int NT = LPB * TL;
-  static constexpr size_t SMEM = (size_t)(L + LPB * RowPitch<L>::P) * sizeof(float2);
+  static constexpr int C0 = 256 / TL;
+  static constexpr int C = C0 < 8 ? 8 : (C0 > 64 ? 64 : C0);
+  static constexpr int NT = C * TL;
+  static constexpr size_t SMEM = (size_t)(L + (TL > 1 ? L * C : 0)) * sizeof(float2);
 };
 
-template <int L, bool INV>
-__global__ void __launch_bounds__(RowCfg<L>::NT) k_yline(const float2* __restrict__ in, float2* __restrict__ out,
-                                                         long long nlines, int nin, int nout, int in_stride,
-                                                         int out_stride, const float2* __restrict__ gtw) {
-  using Cf = RowCfg<L>;
-  constexpr int E = Cf::E, TL = Cf::TL, LPB = Cf::LPB;
-  extern __shared__ float2 sm[];
-  float2* tw = sm;
-  load_tw<L>(tw, gtw);
-  __syncthreads();
-  const int ll = threadIdx.x / TL, t = threadIdx.x - ll * TL;
-  const long long ln = (long long)blockIdx.x * LPB + ll;
-  const bool ok = ln < nlines;
-  const float2* src = in + (ok ? ln : 0) * in_stride;
-  float2 v[1][E];
-#pragma unroll
-  for (int i = 0; i < E; ++i) {
-    const int p = t + TL * i;
-    v[0][i] = (ok && p < nin) ? src[p] : make_float2(0.f, 0.f);
-  }
-  reg_fft<L, E, 1, INV>(v, sm + L, RowA<L>{ll}, tw, t);
-  if (ok) {
-    float2* dst = out + ln * out_stride;
-#pragma unroll
-    for (int i = 0; i < E; ++i) {
-      const int p = t + TL * i;
-      if (p < nout) dst[p] = v[0][i];
-    }
-  }
-}
-
-// K-Z on Y[kx][c][z][ky]: a CTA owns C adjacent ky of one kx; the 3 components in one thread.
 template <int L>
-struct ZCfg {
+struct ZCfg {  // three-component passes with the Khat multiply (K-Z, K-Y2D)
   static constexpr int E = L <= 16 ? L : 8;
   static constexpr int TL = L / E;
   static constexpr int C0 = 256 / TL;
   static constexpr int C = C0 < 4 ? 4 : (C0 > 64 ? 64 : C0);
   static constexpr int NT = C * TL;
-  static constexpr size_t SMEM = (size_t)(L + 3 * L * C) * sizeof(float2);
+  static constexpr size_t SMEM = (size_t)(L + (TL > 1 ? 3 * L * C : 0)) * sizeof(float2);
 };
 
+template <int L>
+__device__ __forceinline__ void load_tw(float2* tw, const float2* __restrict__ gtw) {
+  for (int m = threadIdx.x; m < L; m += blockDim.x) tw[m] = gtw[m * (kTwMax / L)];
+  __syncthreads();
+}
+
+// shared-memory address of (line l, position pos) for column c: [l][pos][c]
 template <int L, int C>
-struct ColA {
+struct ColAddr {
   int c;
   __device__ __forceinline__ int operator()(int l, int pos) const { return (l * L + pos) * C + c; }
 };
 
-__device__ __forceinline__ void khat_apply(const float* __restrict__ kb, int HY, int HZ, int ky, int kz, int Ly,
-                                           int Lz, float2& mx, float2& my, float2& mz) {
-  const int kyf = ky <= Ly / 2 ? ky : Ly - ky;
-  const int kzf = kz <= Lz / 2 ? kz : Lz - kz;
-  const float sy = ky <= Ly / 2 ? 1.f : -1.f;
-  const float sz = kz <= Lz / 2 ? 1.f : -1.f;
-  const size_t cs = (size_t)HZ * HY;
-  const size_t b = (size_t)kzf * HY + kyf;
-  const float kxx = __ldg(kb + b), kyy = __ldg(kb + cs + b), kzz = __ldg(kb + 2 * cs + b);
-  const float kxy = sy * __ldg(kb + 3 * cs + b);
-  const float kxz = sz * __ldg(kb + 4 * cs + b);
-  const float kyz = sy * sz * __ldg(kb + 5 * cs + b);
+// ---------------------------------------------------------------- K-Y forward / inverse
+template <int L, bool INV>
+__global__ void __launch_bounds__(PassCfg<L>::NT) k_ypass(const float2* __restrict__ in, float2* __restrict__ out,
+                                                          Dims d, const float2* __restrict__ gtw) {
+  using Cf = PassCfg<L>;
+  constexpr int E = Cf::E, TL = Cf::TL, C = Cf::C;
+  extern __shared__ float2 sm[];
+  float2* tw = sm;
+  load_tw<L>(tw, gtw);
+  const int c = threadIdx.x % C, t = threadIdx.x / C;
+  const int kx = blockIdx.x * C + c, z = blockIdx.y, comp = blockIdx.z;
+  const bool ok = kx < d.NKX;
+  const int nin = INV ? L : d.ny, nout = INV ? d.ny : L;
+  const size_t plane_in = (size_t)(comp * d.nz + z) * (INV ? L : d.ny);
+  const size_t plane_out = (size_t)(comp * d.nz + z) * (INV ? d.ny : L);
+  const float2* src = in + plane_in * d.P + kx;
+  float2 v[1][E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const int p = t + TL * i;
+    v[0][i] = (ok && p < nin) ? src[(size_t)p * d.P] : make_float2(0.f, 0.f);
+  }
+  reg_fft<L, E, 1, INV>(v, sm + L, ColAddr<L, C>{c}, tw, t);
+  if (ok) {
+    float2* dst = out + plane_out * d.P + kx;
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int p = t + TL * i;
+      if (p < nout) dst[(size_t)p * d.P] = v[0][i];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- Khat multiply
+// Khat is real and stored folded: [6][Lz/2+1][Ly/2+1][P]; off-diagonal components flip sign
+// across the half axis they are odd in (XY: x,y; XZ: x,z; YZ: y,z).  kx is never folded.
+__device__ __forceinline__ void khat_apply(const float* __restrict__ khat, const Dims& d, int kx, int ky, int kz,
+                                           float2& mx, float2& my, float2& mz) {
+  const int hy = d.Ly / 2, hz = d.Lz / 2;
+  const int kyf = ky <= hy ? ky : d.Ly - ky;
+  const int kzf = kz <= hz ? kz : d.Lz - kz;
+  const float sy = ky <= hy ? 1.f : -1.f;
+  const float sz = kz <= hz ? 1.f : -1.f;
+  const size_t cs = (size_t)(hz + 1) * (hy + 1) * d.P;
+  const size_t b = ((size_t)kzf * (hy + 1) + kyf) * d.P + kx;
+  const float kxx = __ldg(khat + b), kyy = __ldg(khat + cs + b), kzz = __ldg(khat + 2 * cs + b);
+  const float kxy = sy * __ldg(khat + 3 * cs + b);
+  const float kxz = sz * __ldg(khat + 4 * cs + b);
+  const float kyz = sy * sz * __ldg(khat + 5 * cs + b);
   const float2 bx = make_float2(kxx * mx.x + kxy * my.x + kxz * mz.x, kxx * mx.y + kxy * my.y + kxz * mz.y);
   const float2 by = make_float2(kxy * mx.x + kyy * my.x + kyz * mz.x, kxy * mx.y + kyy * my.y + kyz * mz.y);
   const float2 bz = make_float2(kxz * mx.x + kyz * my.x + kzz * mz.x, kxz * mx.y + kyz * my.y + kzz * mz.y);
@@ -263,37 +116,40 @@ __device__ __forceinline__ void khat_apply(const float* __restrict__ kb, int HY,
   mz = bz;
 }
 
-template <int L>
-__global__ void __launch_bounds__(ZCfg<L>::NT) k_zconv(float2* __restrict__ Y, const float* __restrict__ khat, Dims d,
-                                                       const float2* __restrict__ gtw) {
+// ---------------------------------------------------------------- K-Z / K-Y2D
+// Y2D = false: lines along z of Y[3][nz][Ly][P] at ky = blockIdx.y (K-Z);
+// Y2D = true : lines along y of X[3][1][ny][P] (nz == 1, kz = 0).
+template <int L, bool Y2D>
+__global__ void __launch_bounds__(ZCfg<L>::NT) k_conv(float2* __restrict__ Y, const float* __restrict__ khat, Dims d,
+                                                      const float2* __restrict__ gtw) {
   using Cf = ZCfg<L>;
   constexpr int E = Cf::E, TL = Cf::TL, C = Cf::C;
   extern __shared__ float2 sm[];
   float2* tw = sm;
   load_tw<L>(tw, gtw);
-  __syncthreads();
   const int c = threadIdx.x % C, t = threadIdx.x / C;
-  const int ky = blockIdx.x * C + c, kx = blockIdx.y;
-  const bool ok = ky < d.Ly;
-  const size_t cstr = (size_t)d.nz * d.Ly;           // between components
-  float2* base = Y + (size_t)kx * 3 * cstr + (ok ? ky : 0);
+  const int kx = blockIdx.x * C + c, ky = Y2D ? 0 : blockIdx.y;
+  const bool ok = kx < d.NKX;
+  const int nin = Y2D ? d.ny : d.nz;
+  const size_t lstride = Y2D ? (size_t)d.P : (size_t)d.Ly * d.P;        // between line elements
+  const size_t cstr = Y2D ? (size_t)d.ny * d.P : (size_t)d.nz * d.Ly * d.P;  // between components
+  float2* base = Y + (size_t)ky * d.P + kx;
   float2 v[3][E];
 #pragma unroll
   for (int g = 0; g < 3; ++g)
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       const int p = t + TL * i;
-      v[g][i] = (ok && p < d.nz) ? base[g * cstr + (size_t)p * d.Ly] : make_float2(0.f, 0.f);
+      v[g][i] = (ok && p < nin) ? base[g * cstr + p * lstride] : make_float2(0.f, 0.f);
     }
-  const ColA<L, C> A{c};
+  const ColAddr<L, C> A{c};
   reg_fft<L, E, 3, false>(v, sm + L, A, tw, t);
   if (ok) {
-    const int HY = d.Ly / 2 + 1, HZ = d.Lz / 2 + 1;
-    const float* kb = khat + (size_t)kx * 6 * HZ * HY;
 #pragma unroll
     for (int i = 0; i < E; ++i) {
-      khat_apply(kb, HY, HZ, ky, t + TL * i, d.Ly, d.Lz, v[0][i], v[1][i], v[2][i]);
-      if ((i & 1) == 1) asm volatile("" ::: "memory");
+      const int p = t + TL * i;
+      khat_apply(khat, d, kx, Y2D ? p : ky, Y2D ? 0 : p, v[0][i], v[1][i], v[2][i]);
+      if ((i & 1) == 1) asm volatile("" ::: "memory");  // bound load hoisting (register budget)
     }
   }
   reg_fft<L, E, 3, true>(v, sm + L, A, tw, t);
@@ -303,72 +159,100 @@ __global__ void __launch_bounds__(ZCfg<L>::NT) k_zconv(float2* __restrict__ Y, c
 #pragma unroll
       for (int i = 0; i < E; ++i) {
         const int p = t + TL * i;
-        if (p < d.nz) base[g * cstr + (size_t)p * d.Ly] = v[g][i];
+        if (p < nin) base[g * cstr + p * lstride] = v[g][i];
       }
   }
 }
 
-// K-Y2D (nz == 1) on X[kx][c][0][y]: KPB kx values per CTA, the 3 components in one thread.
+// ---------------------------------------------------------------- K-Z, TMA-pipelined
+// Persistent CTAs loop over (kx tile, ky) tiles.  For each tile the TMA engine brings the three
+// components' nz x C input boxes of Y into a shared-memory stage (3 tensor copies, one
+// mbarrier); the copy of the next tile is in flight while this one is transformed (two
+// stages), so the SM never waits on HBM latency with its registers idle.
 template <int L>
-struct Y2Cfg {
+struct ZTCfg {
   static constexpr int E = L <= 16 ? L : 8;
   static constexpr int TL = L / E;
-  static constexpr int KPB0 = 128 / TL;
-  static constexpr int KPB = KPB0 < 1 ? 1 : KPB0;
-  static constexpr int NT = KPB * TL;
-  static constexpr size_t SMEM = (size_t)(L + 3 * KPB * RowPitch<L>::P) * sizeof(float2);
+  static constexpr int C0 = 256 / TL;
+  static constexpr int C = C0 < 4 ? 4 : (C0 > 64 ? 64 : C0);
+  static constexpr int NT = C * TL;
+  static constexpr int TWP = (L + 15) / 16 * 16;           // twiddle slots, keeps the stages 128 B aligned
+  static constexpr int GS = ((L / 2) * C + 15) / 16 * 16;  // per-component box stride (128 B aligned)
+  static constexpr int STAGE = 3 * GS;                     // complex per input stage (nz <= L/2)
+  static constexpr size_t SMEM = (size_t)(TWP + 2 * STAGE + (TL > 1 ? 3 * L * C : 0)) * sizeof(float2);
 };
 
-template <int L>
-__global__ void __launch_bounds__(Y2Cfg<L>::NT) k_y2d(float2* __restrict__ X, const float* __restrict__ khat, Dims d,
-                                                      const float2* __restrict__ gtw) {
-  using Cf = Y2Cfg<L>;
-  constexpr int E = Cf::E, TL = Cf::TL, KPB = Cf::KPB;
-  extern __shared__ float2 sm[];
+template <int L, int MINB>
+__global__ void __launch_bounds__(ZTCfg<L>::NT, MINB) k_zconv_tma(const __grid_constant__ CUtensorMap tm,
+                                                            float2* __restrict__ Y, const float* __restrict__ khat,
+                                                            Dims d, const float2* __restrict__ gtw, int ntiles) {
+  using Cf = ZTCfg<L>;
+  constexpr int E = Cf::E, TL = Cf::TL, C = Cf::C;
+  extern __shared__ __align__(128) float2 sm[];
   float2* tw = sm;
-  load_tw<L>(tw, gtw);
-  __syncthreads();
-  const int kl = threadIdx.x / TL, t = threadIdx.x - kl * TL;
-  const int kx = blockIdx.x * KPB + kl;
-  const bool ok = kx < d.NKX;
-  float2* base = X + (size_t)(ok ? kx : 0) * 3 * d.ny;
-  float2 v[3][E];
-#pragma unroll
-  for (int g = 0; g < 3; ++g)
-#pragma unroll
-    for (int i = 0; i < E; ++i) {
-      const int p = t + TL * i;
-      v[g][i] = (ok && p < d.ny) ? base[g * d.ny + p] : make_float2(0.f, 0.f);
-    }
-  struct A3 {
-    int kl;
-    __device__ __forceinline__ int operator()(int l, int pos) const {
-      return (l * KPB + kl) * RowPitch<L>::P + RowPitch<L>::at(pos);
-    }
-  } A{kl};
-  reg_fft<L, E, 3, false>(v, sm + L, A, tw, t);
-  if (ok) {
-    const int HY = d.Ly / 2 + 1;
-    const float* kb = khat + (size_t)kx * 6 * HY;
-#pragma unroll
-    for (int i = 0; i < E; ++i) {
-      khat_apply(kb, HY, 1, t + TL * i, 0, d.Ly, 1, v[0][i], v[1][i], v[2][i]);
-      if ((i & 1) == 1) asm volatile("" ::: "memory");
-    }
+  float2* stg = sm + Cf::TWP;                 // [2][3][GS]: input stages ([nz][C] per component)
+  float2* xch = stg + 2 * Cf::STAGE;          // [3][L][C]
+  __shared__ __align__(8) uint64_t bar[2];
+  const int nz = d.nz;
+  const int nkt = (d.NKX + C - 1) / C;
+  const uint32_t box_bytes = (uint32_t)(3 * nz * C * sizeof(float2));
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
   }
-  reg_fft<L, E, 3, true>(v, sm + L, A, tw, t);
-  if (ok) {
+  for (int m = threadIdx.x; m < L; m += blockDim.x) tw[m] = gtw[m * (kTwMax / L)];
+  __syncthreads();
+  auto issue = [&](int tile, int b) {
+    const int kx0 = (tile % nkt) * C, ky = tile / nkt;
+    mbar_arrive_expect_tx(&bar[b], box_bytes);
+    for (int g = 0; g < 3; ++g) tma_load_3d(stg + b * Cf::STAGE + g * Cf::GS, &tm, kx0, ky, g * nz, &bar[b]);
+  };
+  if (threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+  const int c = threadIdx.x % C, t = threadIdx.x / C;
+  const ColAddr<L, C> A{c};
+  const size_t plane = (size_t)d.Ly * d.P, cstr = (size_t)nz * plane;
+  int it = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int b = it & 1;
+    const int next = tile + gridDim.x;
+    if (threadIdx.x == 0 && next < ntiles) issue(next, b ^ 1);
+    mbar_wait(&bar[b], (it >> 1) & 1);
+    const int kx = (tile % nkt) * C + c, ky = tile / nkt;
+    const float2* in = stg + b * Cf::STAGE;
+    float2 v[3][E];
 #pragma unroll
     for (int g = 0; g < 3; ++g)
 #pragma unroll
       for (int i = 0; i < E; ++i) {
         const int p = t + TL * i;
-        if (p < d.ny) base[g * d.ny + p] = v[g][i];
+        v[g][i] = p < nz ? in[g * Cf::GS + p * C + c] : make_float2(0.f, 0.f);
       }
+    reg_fft<L, E, 3, false>(v, xch, A, tw, t);
+    const bool ok = kx < d.NKX;
+    if (ok) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        khat_apply(khat, d, kx, ky, t + TL * i, v[0][i], v[1][i], v[2][i]);
+        if ((i & 1) == 1) asm volatile("" ::: "memory");
+      }
+    }
+    reg_fft<L, E, 3, true>(v, xch, A, tw, t);
+    if (ok) {
+      float2* base = Y + (size_t)ky * d.P + kx;
+#pragma unroll
+      for (int g = 0; g < 3; ++g)
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          const int p = t + TL * i;
+          if (p < nz) base[g * cstr + p * plane] = v[g][i];
+        }
+    }
+    __syncthreads();  // stage b and xch are free for the next issue / tile
   }
 }
 
-// ====================================================================== dispatch
+// ---------------------------------------------------------------- dispatch
 #define MCQ_DISPATCH_L(Lval, ...)                              \
   switch (Lval) {                                              \
     case 2: { constexpr int L = 2; __VA_ARGS__; } break;       \
@@ -384,118 +268,83 @@ __global__ void __launch_bounds__(Y2Cfg<L>::NT) k_y2d(float2* __restrict__ X, co
     default: break;                                            \
   }
 
-// (LY, LZ) pairs with a cluster kernel instantiated
-#define MCQ_YZ_LIST(X_) \
-  X_(32, 4) X_(32, 8) X_(32, 16) X_(32, 32) X_(32, 64) \
-  X_(64, 4) X_(64, 8) X_(64, 16) X_(64, 32) X_(64, 64) X_(64, 128) \
-  X_(128, 4) X_(128, 8) X_(128, 16) X_(128, 32) X_(128, 64) X_(128, 128) X_(128, 256) \
-  X_(256, 4) X_(256, 8) X_(256, 16) X_(256, 32) X_(256, 64) X_(256, 128) X_(256, 256) \
-  X_(512, 4) X_(512, 8) X_(512, 16) X_(512, 32) X_(512, 64) \
-  X_(1024, 4) X_(1024, 8) X_(1024, 16) X_(1024, 32)
-
-static bool yz_instantiated(int LY, int LZ) {
-#define X_(a, b) if (LY == a && LZ == b) return true;
-  MCQ_YZ_LIST(X_)
-#undef X_
-  return false;
-}
-
-static void yz_consts(int LY, int LZ, int& TLY, int& TLZ, int& PY) {
-  const int EY = LY < 16 ? LY : 16, EZ = LZ <= 16 ? LZ : 8;
-  TLY = LY / EY;
-  TLZ = LZ / EZ;
-  PY = LY + (LY >= 16 ? LY / 16 : 1);
-}
-
-YZPlan plan_yz(const Dims& d) {
-  YZPlan p{};
-  if (d.nz < 2 || !yz_instantiated(d.Ly, d.Lz)) return p;
-  int TLY, TLZ, PY;
-  yz_consts(d.Ly, d.Lz, TLY, TLZ, PY);
-  const size_t kLimit = 227 * 1024;
-  YZPlan best{};
-  for (int CS = 1; CS <= 16; CS *= 2) {
-    if (d.nz % CS || d.Ly % CS) continue;
-    const int ZS = d.nz / CS;
-    const int NT = 3 * ZS * TLY;
-    if (NT > 512 || NT < 32 || NT % (3 * TLZ)) continue;  // 512: __launch_bounds__ of k_yz
-    const int KC = NT / (3 * TLZ);
-    const size_t smem = (size_t)(d.Ly + d.Lz + 3 * ZS * PY + 3 * KC * d.Lz) * sizeof(float2);
-    if (smem > kLimit) continue;
-    YZPlan c{true, CS, ZS, KC, NT, smem};
-    if (!best.ok) best = c;
-    if (smem <= kLimit / 2 && NT >= 256) return c;  // two CTAs per SM
-  }
-  return best;
-}
-
-void launch_yz(const Dims& d, const YZPlan& p, float2* X, const float* khat, const float2* tw, cudaStream_t st) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(d.NKX * p.CS);
-  cfg.blockDim = dim3(p.NT);
-  cfg.dynamicSmemBytes = p.smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = p.CS;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-#define X_(a, b) \
-  if (d.Ly == a && d.Lz == b) { cudaLaunchKernelEx(&cfg, k_yz<a, b>, X, khat, d, tw, p.ZS, p.KC); return; }
-  MCQ_YZ_LIST(X_)
-#undef X_
-}
-
 void launch_yfwd(const Dims& d, const float2* X, float2* Y, const float2* tw, cudaStream_t st) {
-  const long long nl = (long long)d.NKX * 3 * d.nz;
   MCQ_DISPATCH_L(d.Ly, {
-    using Cf = RowCfg<L>;
-    k_yline<L, false><<<(unsigned)((nl + Cf::LPB - 1) / Cf::LPB), Cf::NT, Cf::SMEM, st>>>(X, Y, nl, d.ny, L, d.ny,
-                                                                                          L, tw);
+    using Cf = PassCfg<L>;
+    dim3 grid((d.NKX + Cf::C - 1) / Cf::C, d.nz, 3);
+    k_ypass<L, false><<<grid, Cf::NT, Cf::SMEM, st>>>(X, Y, d, tw);
   })
 }
 
 void launch_yinv(const Dims& d, const float2* Y, float2* X, const float2* tw, cudaStream_t st) {
-  const long long nl = (long long)d.NKX * 3 * d.nz;
   MCQ_DISPATCH_L(d.Ly, {
-    using Cf = RowCfg<L>;
-    k_yline<L, true><<<(unsigned)((nl + Cf::LPB - 1) / Cf::LPB), Cf::NT, Cf::SMEM, st>>>(Y, X, nl, L, d.ny, L, d.ny,
-                                                                                         tw);
+    using Cf = PassCfg<L>;
+    dim3 grid((d.NKX + Cf::C - 1) / Cf::C, d.nz, 3);
+    k_ypass<L, true><<<grid, Cf::NT, Cf::SMEM, st>>>(Y, X, d, tw);
   })
 }
 
 void launch_zconv(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t st) {
   MCQ_DISPATCH_L(d.Lz, {
     using Cf = ZCfg<L>;
-    dim3 grid((d.Ly + Cf::C - 1) / Cf::C, d.NKX);
-    k_zconv<L><<<grid, Cf::NT, Cf::SMEM, st>>>(Y, khat, d, tw);
+    dim3 grid((d.NKX + Cf::C - 1) / Cf::C, d.Ly);
+    k_conv<L, false><<<grid, Cf::NT, Cf::SMEM, st>>>(Y, khat, d, tw);
+  })
+}
+
+int zconv_tma_box_c(int Lz) {
+  int c = 0;
+  MCQ_DISPATCH_L(Lz, c = ZTCfg<L>::C)
+  return c;
+}
+
+void launch_zconv_tma(const Dims& d, const void* tmap, float2* Y, const float* khat, const float2* tw,
+                      cudaStream_t st) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  static const int minb = getenv("MCQ_ZMINB") ? atoi(getenv("MCQ_ZMINB")) : 1;  // experiment knob
+  MCQ_DISPATCH_L(d.Lz, {
+    using Cf = ZTCfg<L>;
+    static int per_sm[2] = {0, 0};
+    const int v = minb >= 3 ? 1 : 0;
+    if (!per_sm[v])
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[v], v ? k_zconv_tma<L, 3> : k_zconv_tma<L, 1>, Cf::NT,
+                                                    Cf::SMEM);
+    const int ntiles = ((d.NKX + Cf::C - 1) / Cf::C) * d.Ly;
+    const int cap = nsm * (per_sm[v] > 0 ? per_sm[v] : 1);
+    const int grid = ntiles < cap ? ntiles : cap;
+    const CUtensorMap& tmr = *reinterpret_cast<const CUtensorMap*>(tmap);
+    if (v)
+      k_zconv_tma<L, 3><<<grid, Cf::NT, Cf::SMEM, st>>>(tmr, Y, khat, d, tw, ntiles);
+    else
+      k_zconv_tma<L, 1><<<grid, Cf::NT, Cf::SMEM, st>>>(tmr, Y, khat, d, tw, ntiles);
   })
 }
 
 void launch_y2d(const Dims& d, float2* X, const float* khat, const float2* tw, cudaStream_t st) {
   MCQ_DISPATCH_L(d.Ly, {
-    using Cf = Y2Cfg<L>;
-    k_y2d<L><<<(d.NKX + Cf::KPB - 1) / Cf::KPB, Cf::NT, Cf::SMEM, st>>>(X, khat, d, tw);
+    using Cf = ZCfg<L>;
+    dim3 grid((d.NKX + Cf::C - 1) / Cf::C);
+    k_conv<L, true><<<grid, Cf::NT, Cf::SMEM, st>>>(X, khat, d, tw);
   })
 }
 
-// Opt every instantiation into the shared memory / cluster size it needs (once per process).
+// Opt every instantiation into the shared memory it needs (once per process).
 void configure_pass_kernels() {
   for (int Lv = 2; Lv <= 1024; Lv *= 2) {
     MCQ_DISPATCH_L(Lv, {
-      cudaFuncSetAttribute(k_yline<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RowCfg<L>::SMEM);
-      cudaFuncSetAttribute(k_yline<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RowCfg<L>::SMEM);
-      cudaFuncSetAttribute(k_zconv<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZCfg<L>::SMEM);
-      cudaFuncSetAttribute(k_y2d<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Y2Cfg<L>::SMEM);
+      cudaFuncSetAttribute(k_ypass<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PassCfg<L>::SMEM);
+      cudaFuncSetAttribute(k_ypass<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PassCfg<L>::SMEM);
+      cudaFuncSetAttribute(k_conv<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZCfg<L>::SMEM);
+      cudaFuncSetAttribute(k_conv<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZCfg<L>::SMEM);
+      cudaFuncSetAttribute(k_zconv_tma<L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZTCfg<L>::SMEM);
+      cudaFuncSetAttribute(k_zconv_tma<L, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZTCfg<L>::SMEM);
     })
   }
-#define X_(a, b)                                                                                  \
-  cudaFuncSetAttribute(k_yz<a, b>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);     \
-  cudaFuncSetAttribute(k_yz<a, b>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  MCQ_YZ_LIST(X_)
-#undef X_
   cudaGetLastError();
 }
 

@@ -131,9 +131,9 @@ __global__ void k_axis_transform(const double* __restrict__ in, double* __restri
   }
 }
 
-// Khat[kx][c][kz][ky] (fp32, kx-major) = scale * sign_c * Nhat[c][kz][ky][kx]
+// Khat[c][kz][ky][P] (fp32, row layout) = scale * sign_c * Nhat[c][kz][ky][kx]
 __global__ void k_khat_finalize(const double* __restrict__ in, float* __restrict__ khat, int m0, int m1, int m2,
-                                double scale) {
+                                int P, double scale) {
   const long long per = (long long)m0 * m1 * m2;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < 6 * per; e += (long long)gridDim.x * blockDim.x) {
     const int c = (int)(e / per);
@@ -141,7 +141,7 @@ __global__ void k_khat_finalize(const double* __restrict__ in, float* __restrict
     const int i0 = (int)(r % m0);
     const long long row = r / m0;            // kz * m1 + ky
     const double sgn = c >= 3 ? -1.0 : 1.0;  // (-i)^2 of the two odd axes
-    khat[((long long)i0 * 6 + c) * m1 * m2 + row] = (float)(scale * sgn * in[e]);
+    khat[(c * (long long)m1 * m2 + row) * P + i0] = (float)(scale * sgn * in[e]);
   }
 }
 
@@ -163,7 +163,7 @@ void launch_axis_transform(const double* in, double* out, int m0, int m1, int m2
 
 void launch_khat_finalize(const double* in, float* khat, const Dims& d, double scale, cudaStream_t s) {
   const int m0 = d.Lx / 2 + 1, m1 = d.Ly / 2 + 1, m2 = d.Lz / 2 + 1;
-  k_khat_finalize<<<grid_for(6LL * m0 * m1 * m2), 256, 0, s>>>(in, khat, m0, m1, m2, scale);
+  k_khat_finalize<<<grid_for(6LL * m0 * m1 * m2), 256, 0, s>>>(in, khat, m0, m1, m2, d.P, scale);
 }
 
 }  // namespace mcq

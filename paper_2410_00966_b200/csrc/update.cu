@@ -1,20 +1,23 @@
 // update.cu — the fused per-stage update kernel K-U, the cavity kernel K-CAV and layout helpers.
 //
 // K-U (one launch per RK4 stage), one CTA = RY full x-rows at one z,
-// TL = N2/E threads per row; in the transform/cell phases thread t of a row owns the packed
-// positions n = t + TL*i (i < E), i.e. the cell pairs x = 2n, 2n+1:
-//   A. demag x-C2R: Z_n = E_n + i O_n from the y/z-processed spectrum X'[n][c][z][y] (packed
-//      half-length real transform; read with rows fastest, since the spectrum is kx-major, and
-//      staged through shared memory), register-resident inverse FFT -> z_n = B(2n) + i B(2n+1);
-//   B. per cell: B' = demag + B_ext + exchange (6-neighbour, C9) + anisotropy (C10)
-//      + B_rms (Gamma(t_s) + a sinc(w t_s)) (eq:bcav P:239), LLG torque (eq:llg P:184),
-//      RK4 stage combine + renormalisation (C1, C2); at stage 4 the overlap partial
-//      sum B_rms . m_{n+1} in fp64;
+// TL = N2/E threads per row; thread t of a row owns the packed positions n = t + TL*i (i < E),
+// i.e. the cell pairs x = 2n, 2n+1:
+//   0. the TMA engine (cp.async.bulk, two mbarriers) stages into shared memory the CTA's rows of
+//      the demag spectrum X'[c][z][y][0..N2] and of the stage state m_s (its rows, the y-halo
+//      rows and the z-1 / z+1 rows) — issued by one thread, in flight while phase A computes;
+//   A. demag x-C2R: Z_n = E_n + i O_n (packed half-length real transform), register-resident
+//      inverse FFT -> z_n = B(2n) + i B(2n+1);
+//   B. per cell: B' = demag + B_ext + exchange (6-neighbour, C9; neighbours from shared memory)
+//      + anisotropy (C10) + B_rms (Gamma(t_s) + a sinc(w t_s)) (eq:bcav P:239), LLG
+//      torque (eq:llg P:184), RK4 stage combine + renormalisation (C1, C2); at stage 4 the
+//      overlap partial sum B_rms . m_{n+1} in fp64;
 //   C. packed forward FFT of m_{s+1} rows (still in registers), real-to-half-complex
-//      post-processing through shared memory -> X[k][c][z][y] (rows fastest again).
+//      post-processing through shared memory -> X[c][z][y][0..N2] for the next stage.
 // Ms is folded into the kernel spectrum, so the transforms act on m directly.
 #include "common.cuh"
 #include "regfft.cuh"
+#include "tma.cuh"
 #include "../../include/mcq.h"
 
 #ifndef MCQ_UE
@@ -30,11 +33,14 @@ struct UCfg {
   static constexpr int RY0 = 128 / TL;
   static constexpr int RY = RY0 < 1 ? 1 : (RY0 > 16 ? 16 : RY0);
   static constexpr int NT = RY * TL;
-  // row pitch (complex): a pad slot every 16 positions, and pitch = 2 (mod 16) so that the
-  // rows-fastest spectrum mapping (8 rows x 2 positions per half-warp) hits distinct banks
+  // row pitch (complex): a pad slot every 16 positions; even, so rows are 16-byte aligned for TMA
   static constexpr int P0 = N2 + (N2 >= 16 ? N2 / 16 : 1);
-  static constexpr int PITCH = P0 + ((2 - P0 % 16) + 16) % 16;
-  static constexpr size_t SMEM = (size_t)(2 * N2 + 3 * RY * PITCH) * sizeof(float2);
+  static constexpr int PITCH = P0 + (P0 & 1);
+  // staged m_s tile (floats, nx <= N2 cells per row): [3][RY+2][nx] at z, [3][RY][nx] at z-1, z+1
+  static constexpr int TILE_C = 3 * (RY + 2) * N2;
+  static constexpr int TILE_Z = 3 * RY * N2;
+  static constexpr size_t XS_BYTES = (size_t)(2 * N2 + 3 * RY * PITCH) * sizeof(float2);
+  static constexpr size_t SMEM = XS_BYTES + (size_t)(TILE_C + 2 * TILE_Z) * sizeof(float);
 };
 
 __device__ __forceinline__ float3 cross3(float3 a, float3 b) {
@@ -52,6 +58,7 @@ __device__ __forceinline__ float3 nrm3(float3 v) {
 __device__ __forceinline__ float3 ld3(const float* __restrict__ p, long long N, long long i) {
   return make_float3(__ldg(p + i), __ldg(p + N + i), __ldg(p + 2 * N + i));
 }
+__device__ __forceinline__ float3 sm3(const float* p, int cs, int i) { return make_float3(p[i], p[cs + i], p[2 * cs + i]); }
 
 template <int N2>
 struct RowAddr {  // shared-memory address of element pos of component-line l of row yl
@@ -61,18 +68,16 @@ struct RowAddr {  // shared-memory address of element pos of component-line l of
   }
 };
 
-// One cell: effective field, then (by mode) field output / max torque / RK4 stage update.
-// Returns the value that enters the x-R2C rows (m_{s+1}, or m for MODE_X0).
-// The state pointers come in as __restrict__ parameters so loads of the next cell can be hoisted
-// above the stores of this one (each cell touches only its own entries of acc / mOut).
-__device__ __forceinline__ float3 cell_update(const UpdateArgs& a, const float* __restrict__ mS,
+// One cell given its state m and its in-mesh neighbours (nb[k] valid where ok[k]): effective
+// field, then (by mode) field output / max torque / RK4 stage update.  Returns the value that
+// enters the x-R2C rows (m_{s+1}, or m for MODE_X0).  The per-cell global arrays come in as
+// __restrict__ parameters so the loads of the next cell can be hoisted above these stores.
+__device__ __forceinline__ float3 cell_update(const UpdateArgs& a, float3 m, const float3 (&nb)[6], const bool (&ok)[6],
                                               const float* __restrict__ mN, float* __restrict__ mOut,
                                               float* __restrict__ accp, const float* __restrict__ brms,
-                                              float* __restrict__ bout, long long idx, int x, int y, int z,
-                                              float3 Bd, float gsum, double& wacc, float& tmax) {
-  const Dims& d = a.d;
-  const long long N = d.N;
-  const float3 m = ld3(mS, N, idx);
+                                              float* __restrict__ bout, long long idx, float3 Bd, float gsum,
+                                              double& wacc, float& tmax) {
+  const long long N = a.d.N;
   if (a.mode == MODE_X0) return m;
   float3 B = make_float3(0.f, 0.f, 0.f);
   if (dot3(m, m) > 0.f) {
@@ -84,22 +89,15 @@ __device__ __forceinline__ float3 cell_update(const UpdateArgs& a, const float* 
     }
     if (a.terms & MCQ_TERM_EXCHANGE) {
       float3 acc = make_float3(0.f, 0.f, 0.f);
-#define MCQ_NB(COND, OFF, COEF)                \
-  if (COND) {                                  \
-    const float3 mj = ld3(mS, N, idx + (OFF)); \
-    if (dot3(mj, mj) > 0.f) {                  \
-      acc.x += (COEF) * (mj.x - m.x);          \
-      acc.y += (COEF) * (mj.y - m.y);          \
-      acc.z += (COEF) * (mj.z - m.z);          \
-    }                                          \
-  }
-      MCQ_NB(x > 0, -1, a.ex[0])
-      MCQ_NB(x < d.nx - 1, +1, a.ex[0])
-      MCQ_NB(y > 0, -(long long)d.nx, a.ex[1])
-      MCQ_NB(y < d.ny - 1, +(long long)d.nx, a.ex[1])
-      MCQ_NB(z > 0, -(long long)d.nx * d.ny, a.ex[2])
-      MCQ_NB(z < d.nz - 1, +(long long)d.nx * d.ny, a.ex[2])
-#undef MCQ_NB
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        const float coef = a.ex[k >> 1];
+        if (ok[k] && dot3(nb[k], nb[k]) > 0.f) {  // in the mesh and magnetic (C9)
+          acc.x += coef * (nb[k].x - m.x);
+          acc.y += coef * (nb[k].y - m.y);
+          acc.z += coef * (nb[k].z - m.z);
+        }
+      }
       B.x += acc.x;
       B.y += acc.y;
       B.z += acc.z;
@@ -181,53 +179,95 @@ __device__ __forceinline__ float3 cell_update(const UpdateArgs& a, const float* 
 template <int N2>
 __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const float2* __restrict__ gtw) {
   using Cf = UCfg<N2>;
-  constexpr int E = Cf::E, TL = Cf::TL, RY = Cf::RY, NT = Cf::NT, LX = 2 * N2;
-  extern __shared__ float2 sm[];
-  float2* tw = sm;  // w_Lx^m, m < Lx
-  float2* xs = sm + LX;
+  constexpr int E = Cf::E, TL = Cf::TL, RY = Cf::RY, NT = Cf::NT, LX = 2 * N2, PITCH = Cf::PITCH;
+  extern __shared__ __align__(16) float2 sm[];
+  float2* tw = sm;       // w_Lx^m, m < Lx
+  float2* xs = sm + LX;  // [3][RY][PITCH]: X rows (staged by TMA), then the FFT exchange buffer
+  float* tc = reinterpret_cast<float*>(reinterpret_cast<char*>(sm) + Cf::XS_BYTES);  // [3][RY+2][nx]
+  float* tzm = tc + Cf::TILE_C;                                                       // [3][RY][nx]
+  float* tzp = tzm + Cf::TILE_Z;
+  __shared__ __align__(8) uint64_t bars[2];
   __shared__ double red[32];
   __shared__ float redf[32];
 
   const Dims& d = a.d;
-  const size_t kst = (size_t)3 * d.nz * d.ny;  // X stride between kx planes
+  const int nx = d.nx, ny = d.ny, nz = d.nz;
+  const long long N = d.N;
   const int y0 = blockIdx.x * RY, z = blockIdx.y;
-  // spectrum access mapping: rows fastest (a warp reads RY consecutive y of one kx column)
-  const int ylg = threadIdx.x % RY, tg = threadIdx.x / RY;
-  const bool rowg = y0 + ylg < d.ny;
-  // transform / cell mapping: positions fastest (a warp owns consecutive cell pairs of a row)
-  const int yl = threadIdx.x / TL, t = threadIdx.x % TL, y = y0 + yl;
-  const bool rowok = y < d.ny;
+  const int nrow = min(RY, ny - y0);
+  const int ylo = y0 > 0 ? y0 - 1 : 0, yhi = min(y0 + RY, ny - 1);  // staged m_s rows at z
+  const int csc = (RY + 2) * nx, csz = RY * nx;                      // component pitches of the tiles
+  const bool use_demag = a.demag && (a.terms & MCQ_TERM_DEMAG) && a.mode != MODE_X0;
+  const bool tma = (nx & 3) == 0 && (d.P & 1) == 0;
+
+  // ---------------- 0: TMA staging (bars[0]: X rows, bars[1]: m_s tile) ----------------
+  if (threadIdx.x == 0 && tma) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
   for (int m = threadIdx.x; m < LX; m += NT) tw[m] = gtw[m * (kTwMax / LX)];
   __syncthreads();
+  if (tma && threadIdx.x == 0) {
+    if (use_demag) {
+      const uint32_t bx = (uint32_t)d.P * 8;
+      mbar_arrive_expect_tx(&bars[0], 3u * nrow * bx);
+      for (int c = 0; c < 3; ++c)
+        for (int r = 0; r < nrow; ++r)
+          tma_load_1d(xs + (c * RY + r) * PITCH, a.X + ((size_t)(c * nz + z) * ny + y0 + r) * d.P, bx, &bars[0]);
+    }
+    const uint32_t bc = (uint32_t)(yhi - ylo + 1) * nx * 4, bz = (uint32_t)nrow * nx * 4;
+    mbar_arrive_expect_tx(&bars[1], 3 * (bc + (z > 0 ? bz : 0) + (z < nz - 1 ? bz : 0)));
+    for (int c = 0; c < 3; ++c) {
+      const float* src = a.mS + c * N;
+      tma_load_1d(tc + c * csc + (ylo - (y0 - 1)) * nx, src + ((long long)z * ny + ylo) * nx, bc, &bars[1]);
+      if (z > 0) tma_load_1d(tzm + c * csz, src + ((long long)(z - 1) * ny + y0) * nx, bz, &bars[1]);
+      if (z < nz - 1) tma_load_1d(tzp + c * csz, src + ((long long)(z + 1) * ny + y0) * nx, bz, &bars[1]);
+    }
+  }
+  if (!tma) {  // fallback (unaligned rows): cooperative coalesced loads into the same layout
+    for (int c = 0; c < 3; ++c) {
+      if (use_demag)
+        for (int e = threadIdx.x; e < nrow * (N2 + 1); e += NT) {
+          const int r = e / (N2 + 1), k = e - r * (N2 + 1);
+          xs[(c * RY + r) * PITCH + k] = a.X[((size_t)(c * nz + z) * ny + y0 + r) * d.P + k];
+        }
+      const float* src = a.mS + c * N;
+      for (int e = threadIdx.x; e < (yhi - ylo + 1) * nx; e += NT)
+        tc[c * csc + (ylo - (y0 - 1)) * nx + e] = src[((long long)z * ny + ylo) * nx + e];
+      for (int e = threadIdx.x; e < nrow * nx; e += NT) {
+        if (z > 0) tzm[c * csz + e] = src[((long long)(z - 1) * ny + y0) * nx + e];
+        if (z < nz - 1) tzp[c * csz + e] = src[((long long)(z + 1) * ny + y0) * nx + e];
+      }
+    }
+    __syncthreads();
+  }
+
+  const int yl = threadIdx.x / TL, t = threadIdx.x % TL, y = y0 + yl;
+  const bool rowok = y < ny;
   const RowAddr<N2> A{yl};
-  const RowAddr<N2> Ag{ylg};
   float2 v[3][E];
 
   // ---------------- A: demag rows (packed x-C2R) ----------------
-  const bool use_demag = a.demag && (a.terms & MCQ_TERM_DEMAG) && a.mode != MODE_X0;
   if (use_demag) {
+    if (tma) mbar_wait(&bars[0], 0);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const float2* col = a.X + ((size_t)c * d.nz + z) * d.ny + (rowg ? y0 + ylg : 0);  // X[.][c][z][y]
+      const float2* row = xs + (c * RY + yl) * PITCH;  // raw staged row (unpadded positions)
 #pragma unroll
       for (int i = 0; i < E; ++i) {
-        const int n = tg + TL * i;
+        const int n = t + TL * i;
         float2 zn = make_float2(0.f, 0.f);
-        if (rowg) {
-          const float2 xk = col[n * kst], xn = cconj(col[(N2 - n) * kst]);
+        if (rowok) {
+          const float2 xk = row[n], xn = cconj(row[N2 - n]);
           const float2 ev = cadd(xk, xn);
           const float2 od = cmul(csub(xk, xn), cconj(tw[n]));  // * w^{-n}
           zn = make_float2(ev.x - od.y, ev.y + od.x);           // E + i O
         }
-        xs[Ag(c, n)] = zn;
+        v[c][i] = zn;
       }
     }
-    __syncthreads();
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-      for (int i = 0; i < E; ++i) v[c][i] = xs[A(c, t + TL * i)];
-    __syncthreads();
+    __syncthreads();  // the staged rows are read before the FFT reuses the buffer
     reg_fft<N2, E, 3, true, 2>(v, xs, A, tw, t);
   } else {
 #pragma unroll
@@ -237,6 +277,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const flo
   }
 
   // ---------------- B: per-cell fields, torque, RK4 ----------------
+  if (tma) mbar_wait(&bars[1], 0);
   float gc = 0.f, ge = 0.f;
   if (a.mode == MODE_LLG || a.mode == MODE_FIELD) {
     const int si = (a.mode == MODE_FIELD) ? 0 : a.stage - 1;
@@ -246,7 +287,8 @@ __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const flo
   const float gsum = gc + ge;
   double wacc = 0.0;
   float tmax = 0.f;
-  const long long rowbase = (long long)d.nx * (y + (long long)d.ny * z);
+  const long long rowbase = (long long)nx * (y + (long long)ny * z);
+  const float* trow = tc + (yl + 1) * nx;  // this row inside the z tile
 #pragma unroll
   for (int i = 0; i < E; ++i) {
     const int n = t + TL * i;
@@ -254,9 +296,18 @@ __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const flo
     for (int h = 0; h < 2; ++h) {
       const int x = 2 * n + h;
       float3 o = make_float3(0.f, 0.f, 0.f);
-      if (rowok && x < d.nx) {
+      if (rowok && x < nx) {
         const float3 Bd = h ? make_float3(v[0][i].y, v[1][i].y, v[2][i].y) : make_float3(v[0][i].x, v[1][i].x, v[2][i].x);
-        o = cell_update(a, a.mS, a.mN, a.mOut, a.acc, a.brms, a.bout, rowbase + x, x, y, z, Bd, gsum, wacc, tmax);
+        const float3 m = sm3(trow, csc, x);
+        float3 nb[6];
+        const bool ok[6] = {x > 0, x < nx - 1, y > 0, y < ny - 1, z > 0, z < nz - 1};
+        nb[0] = ok[0] ? sm3(trow, csc, x - 1) : m;
+        nb[1] = ok[1] ? sm3(trow, csc, x + 1) : m;
+        nb[2] = ok[2] ? sm3(trow - nx, csc, x) : m;
+        nb[3] = ok[3] ? sm3(trow + nx, csc, x) : m;
+        nb[4] = ok[4] ? sm3(tzm + yl * nx, csz, x) : m;
+        nb[5] = ok[5] ? sm3(tzp + yl * nx, csz, x) : m;
+        o = cell_update(a, m, nb, ok, a.mN, a.mOut, a.acc, a.brms, a.bout, rowbase + x, Bd, gsum, wacc, tmax);
       }
       if (h) {
         v[0][i].y = o.x;
@@ -298,6 +349,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const flo
   if (a.mode == MODE_FIELD) return;
 
   // ---------------- C: packed x-R2C of the new rows ----------------
+  if (!use_demag) __syncthreads();  // xs may still hold staged rows of other threads' reads
   reg_fft<N2, E, 3, false, 2>(v, xs, A, tw, t);
   // X_k = (Z_k + conj Z_{N-k})/2 - i/2 w^k (Z_k - conj Z_{N-k}); partners via shared memory
 #pragma unroll
@@ -305,19 +357,19 @@ __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const flo
 #pragma unroll
     for (int i = 0; i < E; ++i) xs[A(c, t + TL * i)] = v[c][i];
   __syncthreads();
-  if (rowg) {
+  if (rowok) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      float2* col = a.X + ((size_t)c * d.nz + z) * d.ny + y0 + ylg;
+      float2* row = a.X + ((size_t)(c * nz + z) * ny + y) * d.P;
 #pragma unroll
       for (int i = 0; i < E; ++i) {
-        const int k = tg + TL * i;
-        const float2 zk = xs[Ag(c, k)];
-        const float2 zn = cconj(xs[Ag(c, (N2 - k) & (N2 - 1))]);
+        const int k = t + TL * i;
+        const float2 zk = v[c][i];
+        const float2 zn = cconj(xs[A(c, (N2 - k) & (N2 - 1))]);
         const float2 ev = cadd(zk, zn);
         const float2 wd = cmul(tw[k], csub(zk, zn));
-        col[k * kst] = make_float2(0.5f * (ev.x + wd.y), 0.5f * (ev.y - wd.x));
-        if (k == 0) col[N2 * kst] = make_float2(zk.x - zk.y, 0.f);  // Nyquist: Re Z0 - Im Z0
+        row[k] = make_float2(0.5f * (ev.x + wd.y), 0.5f * (ev.y - wd.x));
+        if (k == 0) row[N2] = make_float2(zk.x - zk.y, 0.f);  // Nyquist: Re Z0 - Im Z0
       }
     }
   }

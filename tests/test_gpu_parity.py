@@ -81,8 +81,7 @@ def test_khat_matches_direct_dft_of_padded_tensor():
     Nh = np.einsum("ax,by,cz,nzyx->ncba", Fx, Fy, Fz, P)
     assert np.abs(Nh.imag).max() < 1e-9 * np.abs(Nh.real).max()
     expect = -MU0 * cfg.Ms / (Lx * Ly * Lz) * Nh.real[:, :Lz // 2 + 1, :Ly // 2 + 1, :Lx // 2 + 1]
-    expect = np.moveaxis(expect, 3, 0)                  # kx-major (NKX, 6, kz, ky) as the ABI states
-    assert kh.shape == expect.shape
+    assert kh.shape == expect.shape                     # (6, kz, ky, kx) as the ABI states
     assert np.abs(kh - expect).max() <= 2e-7 * np.abs(expect).max()
     s.close()
 
@@ -97,39 +96,19 @@ def test_layout_maps_bit_exact():
             return 1 if n == 1 else 1 << int(math.ceil(math.log2(2 * n)))
 
         assert (L["Lx"], L["Ly"], L["Lz"]) == tuple(pad(n) for n in grid)
-        assert L["NKX"] == L["Lx"] // 2 + 1
+        assert L["NKX"] == L["Lx"] // 2 + 1 and L["P"] == L["NKX"] + (L["NKX"] & 1)
         s.close()
 
 
-def test_fused_yz_kernel_available_for_bench_configs():
-    """configs[1]-[3] shapes can run the cluster-fused y/z kernel (one demag launch per RHS);
-    the default schedule is whichever of the two was faster when the context was created."""
-    for grid in [(128, 128, 128), (512, 512, 8), (24, 20, 12)]:
-        s = mcq.Solver(grid, (5e-9,) * 3, 1e5, 1e-11, 0.01)
-        mcq.mcq_debug_set_path(s.ctx, 2)
-        assert mcq.mcq_debug_layout(s.ctx)["yz_cluster"] > 0, grid
-        mcq.mcq_debug_set_path(s.ctx, 1)
-        assert mcq.mcq_debug_layout(s.ctx)["yz_cluster"] == 0, grid
-        s.close()
-
-
-@pytest.mark.parametrize("kind,grid,aniso", [("sphere", (24, 20, 12), None), ("disc", (48, 40, 3), UNI)])
-def test_field_parity_three_pass_fallback(kind, grid, aniso):
-    """The 3-pass y / z / y schedule (used when a kx plane does not fit a cluster) agrees too."""
-    cfg = small_config(kind, grid, seed=12, aniso=aniso, state="rand")
+def test_unaligned_rows_fallback_path():
+    """nx not a multiple of 4: the update kernel stages rows with plain loads instead of TMA bulk
+    copies (16-byte alignment); same results."""
+    cfg = small_config("sphere", (30, 18, 5), seed=12, state="rand")
     s = _solver(cfg)
-    mcq.mcq_debug_set_path(s.ctx, 2)
-    b_fused = s.field(63)
-    mcq.mcq_debug_set_path(s.ctx, 1)
-    assert mcq.mcq_debug_layout(s.ctx)["yz_cluster"] == 0
-    b3 = s.field(63)
     ref = oracle_from(cfg)
     ref.m = s.m().astype(np.float64).reshape(ref.m.shape)
     mag = magmask(cfg)
-    r = ref.field(ref.m, 0.0).reshape(-1, 3)[mag]
-    assert rel_l2(b3[mag], r) < 1e-5
-    assert rel_l2(b_fused[mag], r) < 1e-5
-    s.run(cfg.dt, 5)
+    assert rel_l2(s.field(63)[mag], ref.field(ref.m, 0.0).reshape(-1, 3)[mag]) < 1e-5
     s.close()
 
 
@@ -270,8 +249,7 @@ def test_launch_count_claim():
     n0 = mcq.mcq_kernel_launches(s.ctx)
     s.run(cfg.dt, 11)
     s.sync()
-    demag = 1 if mcq.mcq_debug_layout(s.ctx)["yz_cluster"] > 0 else 3
-    assert mcq.mcq_kernel_launches(s.ctx) - n0 == 1 + 11 * (4 * (demag + 1) + 1)
+    assert mcq.mcq_kernel_launches(s.ctx) - n0 == 1 + 11 * (4 * (3 + 1) + 1)
     s.close()
 
 
