@@ -172,7 +172,7 @@ MCQ_API int mcq_profile_run(mcq_ctx *, double dt, long long steps, double *kerne
 
 /* Padded layout: out[0..5] = Lx, Ly, Lz (zero-padded FFT lengths: next power of two >= 2n,
  * 1 if n == 1), NKX = Lx/2+1 (x-spectrum columns), P (row pitch of the spectra in complex
- * elements: NKX rounded up to even), number of per-CTA overlap partials. */
+ * elements: NKX rounded up to a multiple of 16), number of per-CTA overlap partials. */
 MCQ_API int mcq_debug_layout(const mcq_ctx *, long long out[6]);
 /* Real-space demag tensor octant, fp64 (6, Lz/2+1, Ly/2+1, Lx/2+1) in XX,YY,ZZ,XY,XZ,YZ
  * order, for index offsets (i, j, k); zero where i >= nx, j >= ny or k >= nz. */

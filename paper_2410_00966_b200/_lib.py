@@ -9,7 +9,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmcq.so")
+LIB_PATH = os.environ.get("MCQ_LIB_PATH") or os.path.join(HERE, "libmcq.so")  # override: tuning variants
 
 MCQ_OK, MCQ_EINVAL, MCQ_ESTATE, MCQ_ENOMEM, MCQ_ECUDA, MCQ_ENCCL = 0, -1, -2, -3, -4, -5
 TERM_ZEEMAN, TERM_EXCHANGE, TERM_ANIS, TERM_DEMAG, TERM_CAVITY, TERM_EXCITATION = 1, 2, 4, 8, 16, 32

@@ -19,7 +19,7 @@ struct Dims {
   int Lx, Ly, Lz;     // zero-padded FFT lengths (next pow2 >= 2n; 1 if n == 1)
   int N2;             // Lx / 2: complex length of the packed real x-transform
   int NKX;            // Lx / 2 + 1: x-spectrum columns (Hermitian half)
-  int P;              // row pitch of the spectra (complex), NKX rounded up to even
+  int P;              // row pitch of the spectra (complex), NKX rounded up to 16 (128-byte rows)
   long long N;        // nx * ny * nz
 };
 

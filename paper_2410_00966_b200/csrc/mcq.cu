@@ -433,7 +433,7 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
   d.Lz = padded(d.nz);
   d.N2 = d.Lx / 2;
   d.NKX = d.N2 + 1;
-  d.P = (d.NKX + 1) / 2 * 2;  // even: every spectrum row is 16-byte aligned (TMA row copies)
+  d.P = (d.NKX + 15) / 16 * 16;  // 128-byte aligned spectrum rows: whole-sector column tiles, TMA rows
   d.N = (long long)d.nx * d.ny * d.nz;
   auto bail = [&](int code) {
     free_all(c);

@@ -170,8 +170,11 @@ __global__ void __launch_bounds__(ZCfg<L>::NT) k_conv(float2* __restrict__ Y, co
 // mbarrier); the copy of the next tile is in flight while this one is transformed (two
 // stages), so the SM never waits on HBM latency with its registers idle.
 template <int L>
+#ifndef MCQ_ZTE
+#define MCQ_ZTE 8  // points per thread per line in the pipelined K-Z
+#endif
 struct ZTCfg {
-  static constexpr int E = L <= 16 ? L : 8;
+  static constexpr int E = L <= 16 ? L : MCQ_ZTE;
   static constexpr int TL = L / E;
   static constexpr int C0 = 256 / TL;
   static constexpr int C = C0 < 4 ? 4 : (C0 > 64 ? 64 : C0);

@@ -96,7 +96,7 @@ def test_layout_maps_bit_exact():
             return 1 if n == 1 else 1 << int(math.ceil(math.log2(2 * n)))
 
         assert (L["Lx"], L["Ly"], L["Lz"]) == tuple(pad(n) for n in grid)
-        assert L["NKX"] == L["Lx"] // 2 + 1 and L["P"] == L["NKX"] + (L["NKX"] & 1)
+        assert L["NKX"] == L["Lx"] // 2 + 1 and L["P"] == (L["NKX"] + 15) // 16 * 16
         s.close()
 
 
