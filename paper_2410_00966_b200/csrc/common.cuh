@@ -79,6 +79,7 @@ struct UpdateArgs {
 void configure_pass_kernels();
 void launch_yfwd(const Dims& d, const float2* X, float2* Y, const float2* tw, cudaStream_t s);
 void launch_zconv(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t s);
+void launch_zconv_seq(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t s);
 int zconv_tma_box_c(int Lz);  // kx columns per K-Z tile of the TMA-pipelined variant
 void launch_zconv_tma(const Dims& d, const void* tmap /* CUtensorMap over Y */, float2* Y, const float* khat,
                       const float2* tw, cudaStream_t s);

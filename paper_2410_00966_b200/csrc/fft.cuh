@@ -1,16 +1,7 @@
-// fft.cuh — block-level power-of-two complex FFTs in shared memory for sm_100a.
-//
-// The demag convolution (B_demag = -mu0 N * M, P:188 via Mumax3; reading C11) is evaluated as a
-// zero-padded 3D FFT convolution.  Every pass of that convolution moves whole lines of length
-// L <= 1024 through shared memory: one CTA owns NLINES lines, each thread keeps E = L*NLINES/NT
-// complex values in registers, and the transform runs as a Stockham autosort sequence of
-// radix-R stages (R in {2,4,8,16}, register codelets), one smem exchange per stage.
-//
-//   stage (Ns = product of previous radices), butterfly j in [0, L/R), k = j mod Ns:
-//     v[r] = x[j + r L/R] * w_{Ns R}^{r k}, v = DFT_R(v), y[(j-k) R + k + r Ns] = v[r]
-//
-// Forward transforms use w = exp(-2 pi i / L); inverse transforms are unnormalised
-// (the 1/(Lx Ly Lz) factor is folded into the kernel spectrum Khat).
+// fft.cuh — complex helpers and the radix-2/4/8/16 register DFT codelets used by the
+// register-resident Stockham FFT of regfft.cuh (the demag convolution, P:188 / reading C11).
+// Forward transforms use w = exp(-2 pi i / L); inverse transforms are unnormalised (the
+// 1/(Lx Ly Lz) factor is folded into the kernel spectrum Khat).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -91,8 +82,16 @@ __device__ __forceinline__ void dft16(float2* v) {
 #pragma unroll
     for (int k1 = 1; k1 < 4; ++k1) {
       const int e = n2 * k1;
-      float2 w = make_float2(cs[e], INV ? sn[e] : -sn[e]);
-      a[n2][k1] = cmul(a[n2][k1], w);
+      float2& x = a[n2][k1];
+      if (e == 4) {  // w^4 = -i (fwd) / +i (inv): a swap
+        x = mul_mi<INV>(x);
+      } else if (e == 2) {  // (c, -+c)
+        x = INV ? make_float2(C2 * (x.x - x.y), C2 * (x.x + x.y)) : make_float2(C2 * (x.x + x.y), C2 * (x.y - x.x));
+      } else if (e == 6) {  // (-c, -+c)
+        x = INV ? make_float2(-C2 * (x.x + x.y), C2 * (x.x - x.y)) : make_float2(C2 * (x.y - x.x), -C2 * (x.x + x.y));
+      } else {
+        x = cmul(x, make_float2(cs[e], INV ? sn[e] : -sn[e]));
+      }
     }
   }
 #pragma unroll
@@ -121,108 +120,7 @@ __device__ __forceinline__ void dft(float2* v) {
   }
 }
 
-// ---------------------------------------------------------------- smem layouts
-// Column layout: NLINES = G * C lines; line c' = g*C + c; element i of line c' at g*L*C + i*C + c.
-// Used by the y/z passes, whose lines are strided columns of a row-major global array (threads
-// in a warp walk c, so both global and shared accesses are contiguous).
-template <int L, int C>
-struct ColLayout {
-  static constexpr int size(int nlines) { return nlines * L; }
-  __device__ static __forceinline__ int addr(int i, int line) {
-    return (line / C) * (L * C) + i * C + (line % C);
-  }
-  // butterfly b of a stage with Q = L/R butterflies per line -> (line, j)
-  template <int Q>
-  __device__ static __forceinline__ void map(int b, int& line, int& j) {
-    const int g = b / (Q * C);
-    const int rem = b - g * (Q * C);
-    j = rem / C;
-    line = g * C + (rem - j * C);
-  }
-};
-
-// Row layout: each line contiguous, one pad slot every 16 elements (conflict-free stride-16).
-template <int L>
-struct RowLayout {
-  static constexpr int PITCH = L + (L >= 16 ? L / 16 : 1);
-  static constexpr int size(int nlines) { return nlines * PITCH; }
-  __device__ static __forceinline__ int addr(int i, int line) { return line * PITCH + i + (i >> 4); }
-  template <int Q>
-  __device__ static __forceinline__ void map(int b, int& line, int& j) {
-    line = b / Q;
-    j = b - line * Q;
-  }
-};
-
-// ---------------------------------------------------------------- Stockham stages
 __host__ __device__ constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x / 2); }
 __host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
-
-// Radix of the stage that starts at Ns: the remainder radix goes first, then max radix.
-template <int L, int E>
-__host__ __device__ constexpr int stage_radix(int Ns) {
-  constexpr int RMAX = cmin(16, cmin(E, L));
-  constexpr int lm = ilog2c(RMAX);
-  constexpr int lr = ilog2c(L);
-  constexpr int first = (lr % lm) ? (1 << (lr % lm)) : RMAX;
-  return Ns == 1 ? first : RMAX;
-}
-
-// tw[m * TWS] = exp(-2 pi i m / L), m in [0, L)
-template <int L, int R, int Ns, int NLINES, int NT, bool INV, class Lay, int TWS>
-__device__ __forceinline__ void stockham_stage(float2* __restrict__ s, const float2* __restrict__ tw) {
-  constexpr int E = L * NLINES / NT;
-  constexpr int NB = E / R;
-  constexpr int Q = L / R;
-  static_assert(NB * R == E, "elements per thread must be a multiple of the radix");
-  float2 v[E];
-#pragma unroll
-  for (int q = 0; q < NB; ++q) {
-    int line, j;
-    Lay::template map<Q>(threadIdx.x + q * NT, line, j);
-    const int k = j & (Ns - 1);
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      float2 x = s[Lay::addr(j + r * Q, line)];
-      if (Ns > 1 && r > 0) {
-        float2 w = tw[(r * k * (L / (Ns * R))) * TWS];
-        if (INV) w.y = -w.y;
-        x = cmul(x, w);
-      }
-      v[q * R + r] = x;
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < NB; ++q) {
-    dft<R, INV>(&v[q * R]);
-    int line, j;
-    Lay::template map<Q>(threadIdx.x + q * NT, line, j);
-    const int k = j & (Ns - 1);
-    const int base = (j - k) * R + k;
-#pragma unroll
-    for (int r = 0; r < R; ++r) s[Lay::addr(base + r * Ns, line)] = v[q * R + r];
-  }
-  __syncthreads();
-}
-
-template <int L, int Ns, int NLINES, int NT, bool INV, class Lay, int TWS>
-__device__ __forceinline__ void stockham_from(float2* __restrict__ s, const float2* __restrict__ tw) {
-  if constexpr (Ns < L) {
-    constexpr int E = L * NLINES / NT;
-    constexpr int R = stage_radix<L, E>(Ns);
-    stockham_stage<L, R, Ns, NLINES, NT, INV, Lay, TWS>(s, tw);
-    stockham_from<L, Ns * R, NLINES, NT, INV, Lay, TWS>(s, tw);
-  }
-}
-
-// In-place FFT of NLINES lines of length L held in shared memory.  Callers must
-// __syncthreads() before (data written) — the routine ends with a barrier.
-template <int L, int NLINES, int NT, bool INV, class Lay, int TWS = 1>
-__device__ __forceinline__ void block_fft(float2* __restrict__ s, const float2* __restrict__ tw) {
-  static_assert((L & (L - 1)) == 0, "power-of-two length");
-  static_assert((L * NLINES) % NT == 0, "threads must divide the elements");
-  if constexpr (L > 1) stockham_from<L, 1, NLINES, NT, INV, Lay, TWS>(s, tw);
-}
 
 }  // namespace mcq

@@ -13,6 +13,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -179,10 +180,15 @@ struct Enq {
       launch_yfwd(d, c->X, c->Y, c->tw, s);
       post(MCQ_K_YFWD);
       pre(MCQ_K_ZCONV);
-      if (c->have_tmz)
+      // K-Z variant (measured on configs[1], 1x B200: seq 170 us, tma 180 us, plain 206 us per
+      // launch); MCQ_ZVARIANT=tma|plain selects the others (experiments / profiling)
+      static const char* zv = getenv("MCQ_ZVARIANT");
+      if (zv && !strcmp(zv, "tma") && c->have_tmz)
         launch_zconv_tma(d, &c->tmz, c->Y, c->khat, c->tw, s);
-      else
+      else if (zv && !strcmp(zv, "plain"))
         launch_zconv(d, c->Y, c->khat, c->tw, s);
+      else
+        launch_zconv_seq(d, c->Y, c->khat, c->tw, s);
       post(MCQ_K_ZCONV);
       pre(MCQ_K_YINV);
       launch_yinv(d, c->Y, c->X, c->tw, s);

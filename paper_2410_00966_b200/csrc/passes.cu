@@ -164,6 +164,86 @@ __global__ void __launch_bounds__(ZCfg<L>::NT) k_conv(float2* __restrict__ Y, co
   }
 }
 
+// ---------------------------------------------------------------- K-Z, component-sequential
+// Low-register variant: the three component lines of a column pass through the register FFT
+// one after another (a thread holds E points of ONE line at a time); forward results are parked
+// in the shared exchange buffer at the thread's own positions, the K-hat multiply reads and
+// writes them there, and the inverse transforms reload them.  ~60 registers instead of ~128, so
+// twice the warps per SM for the same shared memory.
+#ifndef MCQ_ZSE
+#define MCQ_ZSE 16  // points per thread per line in the component-sequential K-Z
+#endif
+template <int L>
+struct ZSCfg {
+  static constexpr int E = L <= MCQ_ZSE ? L : MCQ_ZSE;
+  static constexpr int TL = L / E;
+  static constexpr int C0 = 256 / TL;
+  static constexpr int C = C0 < 4 ? 4 : (C0 > 64 ? 64 : C0);
+  static constexpr int NT = C * TL;
+  static constexpr size_t SMEM = (size_t)(L + 3 * L * C) * sizeof(float2);
+};
+
+template <int L>
+__global__ void __launch_bounds__(ZSCfg<L>::NT) k_zconv_seq(float2* __restrict__ Y, const float* __restrict__ khat,
+                                                            Dims d, const float2* __restrict__ gtw) {
+  using Cf = ZSCfg<L>;
+  constexpr int E = Cf::E, TL = Cf::TL, C = Cf::C;
+  extern __shared__ float2 sm[];
+  float2* tw = sm;
+  float2* xch = sm + L;  // [3][L][C]
+  load_tw<L>(tw, gtw);
+  const int c = threadIdx.x % C, t = threadIdx.x / C;
+  const int kx = blockIdx.x * C + c, ky = blockIdx.y;
+  const bool ok = kx < d.NKX;
+  const int nz = d.nz;
+  const size_t plane = (size_t)d.Ly * d.P, cstr = (size_t)nz * plane;
+  float2* base = Y + (size_t)ky * d.P + kx;
+  struct GA {
+    int g, c;
+    __device__ __forceinline__ int operator()(int, int pos) const { return (g * L + pos) * C + c; }
+  };
+#pragma unroll 1
+  for (int g = 0; g < 3; ++g) {
+    float2 v[1][E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int p = t + TL * i;
+      v[0][i] = (ok && p < nz) ? base[g * cstr + p * plane] : make_float2(0.f, 0.f);
+    }
+    const GA A{g, c};
+    reg_fft<L, E, 1, false>(v, xch, A, tw, t);
+#pragma unroll
+    for (int i = 0; i < E; ++i) xch[A(0, t + TL * i)] = v[0][i];
+  }
+  if (ok) {  // own positions only: no barrier needed
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int p = t + TL * i;
+      float2 mx = xch[(0 * L + p) * C + c], my = xch[(1 * L + p) * C + c], mz = xch[(2 * L + p) * C + c];
+      khat_apply(khat, d, kx, ky, p, mx, my, mz);
+      xch[(0 * L + p) * C + c] = mx;
+      xch[(1 * L + p) * C + c] = my;
+      xch[(2 * L + p) * C + c] = mz;
+    }
+  }
+#pragma unroll 1
+  for (int g = 0; g < 3; ++g) {
+    const GA A{g, c};
+    float2 v[1][E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[0][i] = xch[A(0, t + TL * i)];
+    __syncthreads();  // region g is read before its exchanges overwrite it
+    reg_fft<L, E, 1, true>(v, xch, A, tw, t);
+    if (ok) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int p = t + TL * i;
+        if (p < nz) base[g * cstr + p * plane] = v[0][i];
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- K-Z, TMA-pipelined
 // Persistent CTAs loop over (kx tile, ky) tiles.  For each tile the TMA engine brings the three
 // components' nz x C input boxes of Y into a shared-memory stage (3 tensor copies, one
@@ -295,6 +375,14 @@ void launch_zconv(const Dims& d, float2* Y, const float* khat, const float2* tw,
   })
 }
 
+void launch_zconv_seq(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t st) {
+  MCQ_DISPATCH_L(d.Lz, {
+    using Cf = ZSCfg<L>;
+    dim3 grid((d.NKX + Cf::C - 1) / Cf::C, d.Ly);
+    k_zconv_seq<L><<<grid, Cf::NT, Cf::SMEM, st>>>(Y, khat, d, tw);
+  })
+}
+
 int zconv_tma_box_c(int Lz) {
   int c = 0;
   MCQ_DISPATCH_L(Lz, c = ZTCfg<L>::C)
@@ -345,6 +433,7 @@ void configure_pass_kernels() {
       cudaFuncSetAttribute(k_conv<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZCfg<L>::SMEM);
       cudaFuncSetAttribute(k_conv<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZCfg<L>::SMEM);
       cudaFuncSetAttribute(k_zconv_tma<L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZTCfg<L>::SMEM);
+      cudaFuncSetAttribute(k_zconv_seq<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZSCfg<L>::SMEM);
       cudaFuncSetAttribute(k_zconv_tma<L, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZTCfg<L>::SMEM);
     })
   }

@@ -68,16 +68,13 @@ struct RowAddr {  // shared-memory address of element pos of component-line l of
   }
 };
 
-// One cell given its state m and its in-mesh neighbours (nb[k] valid where ok[k]): effective
-// field, then (by mode) field output / max torque / RK4 stage update.  Returns the value that
-// enters the x-R2C rows (m_{s+1}, or m for MODE_X0).  The per-cell global arrays come in as
-// __restrict__ parameters so the loads of the next cell can be hoisted above these stores.
-__device__ __forceinline__ float3 cell_update(const UpdateArgs& a, float3 m, const float3 (&nb)[6], const bool (&ok)[6],
-                                              const float* __restrict__ mN, float* __restrict__ mOut,
-                                              float* __restrict__ accp, const float* __restrict__ brms,
-                                              float* __restrict__ bout, long long idx, float3 Bd, float gsum,
-                                              double& wacc, float& tmax) {
-  const long long N = a.d.N;
+// One cell from register inputs: state m, in-mesh neighbours nb[k] (valid where ok[k]), m_n,
+// the RK4 accumulator so far, B_rms and the demag field.  Computes B' and, by mode, the field
+// (Bout), the max torque, or the RK4 stage update (returns m_{s+1}, writes the new accumulator
+// to acc_out).  All memory traffic stays in the caller (paired 8-byte accesses).
+__device__ __forceinline__ float3 cell_core(const UpdateArgs& a, float3 m, const float3 (&nb)[6], const bool (&ok)[6],
+                                            float3 mn, float3 ap, float3 br, float3 Bd, float gsum, double& wacc,
+                                            float& tmax, float3& acc_out, float3& Bout) {
   if (a.mode == MODE_X0) return m;
   float3 B = make_float3(0.f, 0.f, 0.f);
   if (dot3(m, m) > 0.f) {
@@ -122,16 +119,13 @@ __device__ __forceinline__ float3 cell_update(const UpdateArgs& a, float3 m, con
       }
     }
     if (gsum != 0.f) {
-      const float3 br = brms ? ld3(brms, N, idx) : make_float3(a.brms_u[0], a.brms_u[1], a.brms_u[2]);
       B.x += br.x * gsum;
       B.y += br.y * gsum;
       B.z += br.z * gsum;
     }
   }
   if (a.mode == MODE_FIELD) {
-    bout[idx] = B.x;
-    bout[N + idx] = B.y;
-    bout[2 * N + idx] = B.z;
+    Bout = B;
     return m;
   }
   const float3 mxB = cross3(m, B);
@@ -148,33 +142,33 @@ __device__ __forceinline__ float3 cell_update(const UpdateArgs& a, float3 m, con
     k = make_float3(-a.gamma * mmxB.x, -a.gamma * mmxB.y, -a.gamma * mmxB.z);
   }
   const int stage = a.stage;
-  const float3 mn = (stage == 1) ? m : ld3(mN, N, idx);
+  if (stage == 1) mn = m;
   float3 out;
   if (stage < 4) {
-    float3 acc;
-    if (stage == 1) {
-      acc = k;
-    } else {
-      const float3 ap = ld3(accp, N, idx);
-      acc = make_float3(ap.x + 2.f * k.x, ap.y + 2.f * k.y, ap.z + 2.f * k.z);
-    }
-    accp[idx] = acc.x;
-    accp[N + idx] = acc.y;
-    accp[2 * N + idx] = acc.z;
+    acc_out = (stage == 1) ? k : make_float3(ap.x + 2.f * k.x, ap.y + 2.f * k.y, ap.z + 2.f * k.z);
     out = nrm3(make_float3(mn.x + a.h * k.x, mn.y + a.h * k.y, mn.z + a.h * k.z));
   } else {
-    const float3 ap = ld3(accp, N, idx);
     out = nrm3(make_float3(mn.x + a.dt6 * (ap.x + k.x), mn.y + a.dt6 * (ap.y + k.y), mn.z + a.dt6 * (ap.z + k.z)));
-    if (a.mode == MODE_LLG) {
-      const float3 br = brms ? ld3(brms, N, idx) : make_float3(a.brms_u[0], a.brms_u[1], a.brms_u[2]);
-      wacc += (double)(br.x * out.x) + (double)(br.y * out.y) + (double)(br.z * out.z);
-    }
+    if (a.mode == MODE_LLG) wacc += (double)(br.x * out.x) + (double)(br.y * out.y) + (double)(br.z * out.z);
   }
-  mOut[idx] = out.x;
-  mOut[N + idx] = out.y;
-  mOut[2 * N + idx] = out.z;
   return out;
 }
+
+// paired access to cells (x, x+1) of an SoA component: one 8-byte access when the index is even
+// (nx even), else two 4-byte ones; `two` = the second cell exists.
+__device__ __forceinline__ float2 ld_pair(const float* __restrict__ p, long long i, bool vec, bool two) {
+  if (vec) return __ldg(reinterpret_cast<const float2*>(p + i));
+  return make_float2(__ldg(p + i), two ? __ldg(p + i + 1) : 0.f);
+}
+__device__ __forceinline__ void st_pair(float* __restrict__ p, long long i, float2 v, bool vec, bool two) {
+  if (vec) {
+    *reinterpret_cast<float2*>(p + i) = v;
+  } else {
+    p[i] = v.x;
+    if (two) p[i + 1] = v.y;
+  }
+}
+__device__ __forceinline__ float2 sm_pair(const float* p) { return *reinterpret_cast<const float2*>(p); }
 
 template <int N2>
 __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const float2* __restrict__ gtw) {
@@ -196,7 +190,8 @@ __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const flo
   const int y0 = blockIdx.x * RY, z = blockIdx.y;
   const int nrow = min(RY, ny - y0);
   const int ylo = y0 > 0 ? y0 - 1 : 0, yhi = min(y0 + RY, ny - 1);  // staged m_s rows at z
-  const int csc = (RY + 2) * nx, csz = RY * nx;                      // component pitches of the tiles
+  const int nxp = nx + (nx & 1);                                     // tile row pitch (8-byte pairs)
+  const int csc = (RY + 2) * nxp, csz = RY * nxp;                    // component pitches of the tiles
   const bool use_demag = a.demag && (a.terms & MCQ_TERM_DEMAG) && a.mode != MODE_X0;
   const bool tma = (nx & 3) == 0 && (d.P & 1) == 0;
 
@@ -233,11 +228,14 @@ __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const flo
           xs[(c * RY + r) * PITCH + k] = a.X[((size_t)(c * nz + z) * ny + y0 + r) * d.P + k];
         }
       const float* src = a.mS + c * N;
-      for (int e = threadIdx.x; e < (yhi - ylo + 1) * nx; e += NT)
-        tc[c * csc + (ylo - (y0 - 1)) * nx + e] = src[((long long)z * ny + ylo) * nx + e];
+      for (int e = threadIdx.x; e < (yhi - ylo + 1) * nx; e += NT) {
+        const int r = e / nx, x = e - r * nx;
+        tc[c * csc + (ylo - (y0 - 1) + r) * nxp + x] = src[((long long)z * ny + ylo) * nx + e];
+      }
       for (int e = threadIdx.x; e < nrow * nx; e += NT) {
-        if (z > 0) tzm[c * csz + e] = src[((long long)(z - 1) * ny + y0) * nx + e];
-        if (z < nz - 1) tzp[c * csz + e] = src[((long long)(z + 1) * ny + y0) * nx + e];
+        const int r = e / nx, x = e - r * nx;
+        if (z > 0) tzm[c * csz + r * nxp + x] = src[((long long)(z - 1) * ny + y0) * nx + e];
+        if (z < nz - 1) tzp[c * csz + r * nxp + x] = src[((long long)(z + 1) * ny + y0) * nx + e];
       }
     }
     __syncthreads();
@@ -288,37 +286,87 @@ __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const flo
   double wacc = 0.0;
   float tmax = 0.f;
   const long long rowbase = (long long)nx * (y + (long long)ny * z);
-  const float* trow = tc + (yl + 1) * nx;  // this row inside the z tile
+  const float* trow = tc + (yl + 1) * nxp;  // this row inside the z tile
+  const bool vec = (nx & 1) == 0;           // global pairs are 8-byte aligned
+  const bool st = a.mode == MODE_LLG || a.mode == MODE_RELAX;
+  const bool need_mn = st && a.stage > 1, need_acc = st && a.stage > 1;
+  const bool need_br = a.brms && (gsum != 0.f || (a.mode == MODE_LLG && a.stage == 4));
 #pragma unroll
   for (int i = 0; i < E; ++i) {
-    const int n = t + TL * i;
+    const int x0 = 2 * (t + TL * i);
+    float2 o[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    if (rowok && x0 < nx) {
+      const bool two = x0 + 1 < nx;
+      const long long idx = rowbase + x0;
+      // the pair (x0, x0+1) and its neighbours from the staged tile; m_n, acc, B_rms from HBM
+      float2 mc[3], ym[3], yp[3], zm[3], zp[3], mn2[3], ap2[3], br2[3];
+      float xl[3], xr[3];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int x = 2 * n + h;
-      float3 o = make_float3(0.f, 0.f, 0.f);
-      if (rowok && x < nx) {
-        const float3 Bd = h ? make_float3(v[0][i].y, v[1][i].y, v[2][i].y) : make_float3(v[0][i].x, v[1][i].x, v[2][i].x);
-        const float3 m = sm3(trow, csc, x);
-        float3 nb[6];
-        const bool ok[6] = {x > 0, x < nx - 1, y > 0, y < ny - 1, z > 0, z < nz - 1};
-        nb[0] = ok[0] ? sm3(trow, csc, x - 1) : m;
-        nb[1] = ok[1] ? sm3(trow, csc, x + 1) : m;
-        nb[2] = ok[2] ? sm3(trow - nx, csc, x) : m;
-        nb[3] = ok[3] ? sm3(trow + nx, csc, x) : m;
-        nb[4] = ok[4] ? sm3(tzm + yl * nx, csz, x) : m;
-        nb[5] = ok[5] ? sm3(tzp + yl * nx, csz, x) : m;
-        o = cell_update(a, m, nb, ok, a.mN, a.mOut, a.acc, a.brms, a.bout, rowbase + x, Bd, gsum, wacc, tmax);
+      for (int c = 0; c < 3; ++c) {
+        const float* r = trow + c * csc;
+        mc[c] = sm_pair(r + x0);
+        ym[c] = y > 0 ? sm_pair(r - nxp + x0) : mc[c];
+        yp[c] = y < ny - 1 ? sm_pair(r + nxp + x0) : mc[c];
+        zm[c] = z > 0 ? sm_pair(tzm + c * csz + yl * nxp + x0) : mc[c];
+        zp[c] = z < nz - 1 ? sm_pair(tzp + c * csz + yl * nxp + x0) : mc[c];
+        xl[c] = x0 > 0 ? r[x0 - 1] : 0.f;
+        xr[c] = x0 + 2 < nx ? r[x0 + 2] : 0.f;
+        mn2[c] = need_mn ? ld_pair(a.mN + c * N, idx, vec, two) : make_float2(0.f, 0.f);
+        ap2[c] = need_acc ? ld_pair(a.acc + c * N, idx, vec, two) : make_float2(0.f, 0.f);
+        br2[c] = need_br ? ld_pair(a.brms + c * N, idx, vec, two)
+                         : make_float2(a.brms_u[c], a.brms_u[c]);
       }
-      if (h) {
-        v[0][i].y = o.x;
-        v[1][i].y = o.y;
-        v[2][i].y = o.z;
-      } else {
-        v[0][i].x = o.x;
-        v[1][i].x = o.y;
-        v[2][i].x = o.z;
+      float2 acc2[3], bf2[3];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (h == 1 && !two) break;
+        const int x = x0 + h;
+#define MCQ_PICK(p) (h ? (p).y : (p).x)
+        const float3 m = make_float3(MCQ_PICK(mc[0]), MCQ_PICK(mc[1]), MCQ_PICK(mc[2]));
+        const bool ok[6] = {x > 0, x < nx - 1, y > 0, y < ny - 1, z > 0, z < nz - 1};
+        float3 nb[6];
+        nb[0] = h ? make_float3(mc[0].x, mc[1].x, mc[2].x) : make_float3(xl[0], xl[1], xl[2]);
+        nb[1] = h ? make_float3(xr[0], xr[1], xr[2]) : make_float3(mc[0].y, mc[1].y, mc[2].y);
+        nb[2] = make_float3(MCQ_PICK(ym[0]), MCQ_PICK(ym[1]), MCQ_PICK(ym[2]));
+        nb[3] = make_float3(MCQ_PICK(yp[0]), MCQ_PICK(yp[1]), MCQ_PICK(yp[2]));
+        nb[4] = make_float3(MCQ_PICK(zm[0]), MCQ_PICK(zm[1]), MCQ_PICK(zm[2]));
+        nb[5] = make_float3(MCQ_PICK(zp[0]), MCQ_PICK(zp[1]), MCQ_PICK(zp[2]));
+        const float3 mn = make_float3(MCQ_PICK(mn2[0]), MCQ_PICK(mn2[1]), MCQ_PICK(mn2[2]));
+        const float3 ap = make_float3(MCQ_PICK(ap2[0]), MCQ_PICK(ap2[1]), MCQ_PICK(ap2[2]));
+        const float3 br = make_float3(MCQ_PICK(br2[0]), MCQ_PICK(br2[1]), MCQ_PICK(br2[2]));
+        const float3 Bd = make_float3(MCQ_PICK(v[0][i]), MCQ_PICK(v[1][i]), MCQ_PICK(v[2][i]));
+#undef MCQ_PICK
+        float3 accn = make_float3(0.f, 0.f, 0.f), Bf = make_float3(0.f, 0.f, 0.f);
+        const float3 out = cell_core(a, m, nb, ok, mn, ap, br, Bd, gsum, wacc, tmax, accn, Bf);
+        if (h) {
+          o[0].y = out.x; o[1].y = out.y; o[2].y = out.z;
+          acc2[0].y = accn.x; acc2[1].y = accn.y; acc2[2].y = accn.z;
+          bf2[0].y = Bf.x; bf2[1].y = Bf.y; bf2[2].y = Bf.z;
+        } else {
+          o[0].x = out.x; o[1].x = out.y; o[2].x = out.z;
+          acc2[0].x = accn.x; acc2[1].x = accn.y; acc2[2].x = accn.z;
+          bf2[0].x = Bf.x; bf2[1].x = Bf.y; bf2[2].x = Bf.z;
+        }
+      }
+      if (!two) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          o[c].y = 0.f;
+          acc2[c].y = 0.f;
+          bf2[c].y = 0.f;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        if (a.mode == MODE_FIELD) st_pair(a.bout + c * N, idx, bf2[c], vec, two);
+        if (st) {
+          st_pair(a.mOut + c * N, idx, o[c], vec, two);
+          if (a.stage < 4) st_pair(a.acc + c * N, idx, acc2[c], vec, two);
+        }
       }
     }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) v[c][i] = o[c];
   }
 
   // ---------------- reductions ----------------
