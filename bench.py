@@ -3,8 +3,10 @@
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config k] [--impl mcq|reference]
 
-One process per GPU (torchrun for N > 1).  N > 1 runs independent replicas (one bias-field sweep
-point per rank, "scaling": "weak"; the z-slab decomposition is not in this build).  Timing: W
+One process per GPU (torchrun for N > 1).  N > 1 (default --decomp slab): the SAME grid z-slab
+decomposed over the ranks (libmcq's NCCL halos, demag all-to-all transpose and W all-gather;
+"scaling": "strong"); --decomp replicas: independent replicas, one bias-field
+sweep point per rank ("scaling": "weak").  Timing: W
 untimed warm-up steps, then exactly K steps between barrier + synchronize, CUDA events on the
 library's stream, max over ranks.  Rank 0 prints one JSON line.
 """
@@ -85,14 +87,16 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- algorithmic bytes
-def alg_bytes(L, grid, has_map):
-    """Algorithmic HBM bytes per launch of each kernel class (fp32 state, complex64 spectra)."""
+def alg_bytes(L, grid, has_map, slabs=1):
+    """Algorithmic HBM bytes per launch of each kernel class (fp32 state, complex64 spectra);
+    with z slabs, one launch covers 1/slabs of the grid (and of the Khat columns in K-Z)."""
     nx, ny, nz = grid
+    nz //= slabs
     N = nx * ny * nz
     nkx, Ly, Lz = L["NKX"], L["Ly"], L["Lz"]
     X = 3 * nz * ny * nkx * 8
     Y = 3 * nz * Ly * nkx * 8
-    K = 6 * (Lz // 2 + 1) * (Ly // 2 + 1) * nkx * 4
+    K = 6 * (Lz // 2 + 1) * (Ly // 2 + 1) * nkx * 4 // slabs
     state = (36 + 60 + 60 + 48) / 4 * N           # RK4 state traffic averaged over the 4 stages
     out = {"yfwd": X + Y, "zconv": 2 * Y + K, "yinv": Y + X,
            "y2d": 2 * X + 6 * ((Ly // 2 + 1) * nkx * 4),
@@ -100,8 +104,8 @@ def alg_bytes(L, grid, has_map):
     return out
 
 
-def step_alg_bytes(L, grid, has_map):
-    b = alg_bytes(L, grid, has_map)
+def step_alg_bytes(L, grid, has_map, slabs=1):
+    b = alg_bytes(L, grid, has_map, slabs)
     if grid[2] > 1:
         return 4 * (b["yfwd"] + b["zconv"] + b["yinv"] + b["update"])
     return 4 * (b["y2d"] + b["update"])
@@ -174,6 +178,10 @@ def main():
     ap.add_argument("--impl", default="mcq", choices=["mcq", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=5)
+    ap.add_argument("--decomp", default="slab", choices=["slab", "replicas"],
+                    help="N > 1: z-slab decomposition of one grid (strong) or independent replicas (weak)")
+    ap.add_argument("--loopback", type=int, default=0,
+                    help="N == 1: run the decomposed schedule with this many z slabs on the one GPU")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -192,11 +200,18 @@ def main():
     from synth import make_config
 
     from paper_2410_00966_b200.replicas import replica_bias, max_over_ranks
+    from paper_2410_00966_b200.slabs import slab_dist
     cfg = make_config(args.config)
-    cfg.bext = replica_bias(cfg.bext, world, rank)  # replica r: its bias-field sweep point
+    slab = world > 1 and args.decomp == "slab"
+    if world > 1 and not slab:
+        cfg.bext = replica_bias(cfg.bext, world, rank)  # replica r: its bias-field sweep point
     stream = torch.cuda.Stream()          # a real stream: the library's kernels and our events share it
     torch.cuda.set_stream(stream)
-    solver = mcq.Solver.from_config(cfg, stream=stream.cuda_stream)
+    dd = slab_dist(rank, world, local) if slab else None
+    if world == 1 and args.loopback > 1:
+        dd = {"rank": -1, "world": args.loopback}
+    solver = mcq.Solver.from_config(cfg, stream=stream.cuda_stream, dist=dd)
+    jobs = 1 if slab else world           # grids the job advances per step
     if cfg.relax_first:
         solver.relax(cfg.dt * 0.5, 1e-3, 2000)
         mcq.mcq_reset_memory(solver.ctx)
@@ -220,7 +235,7 @@ def main():
         barrier()
     launches = mcq.mcq_kernel_launches(solver.ctx) - launches0
     ms_max = max_over_ranks(ev0.elapsed_time(ev1), device="cuda")
-    value = cfg.n * args.steps * world / (ms_max * 1e-3)
+    value = cfg.n * args.steps * jobs / (ms_max * 1e-3)
 
     # e2e through the public API with host buffers: set_m (H2D) + run + get_m (D2H)
     m_host = torch.from_numpy(np.ascontiguousarray(cfg.m0, np.float32)).pin_memory()
@@ -233,26 +248,29 @@ def main():
     mcq.mcq_get_m(solver.ctx, cfg.n, out_host.numpy().reshape(-1))
     torch.cuda.synchronize()
     e2e_s = max_over_ranks(time.perf_counter() - t0, device="cuda")
-    e2e_val = cfg.n * e2e_steps * world / e2e_s
+    e2e_val = cfg.n * e2e_steps * jobs / e2e_s
 
     # per-kernel timing (CUDA events around each launch, same stream) -> roofline of the top kernel
     prof = mcq.mcq_profile_run(solver.ctx, cfg.dt, args.profile_steps)
-    ab = alg_bytes(L, cfg.grid, cfg.brms_map is not None)
+    ns = world if slab else 1
+    ab = alg_bytes(L, cfg.grid, cfg.brms_map is not None, ns)
     share = {k: v[0] * v[1] for k, v in prof.items() if v[1] > 0}
     top = max(share, key=share.get)
     pk = peaks()
     achieved = ab[top] / (prof[top][0] * 1e-3) / 1e9
-    step_bytes = step_alg_bytes(L, cfg.grid, cfg.brms_map is not None)
+    step_bytes = step_alg_bytes(L, cfg.grid, cfg.brms_map is not None, ns)
     ms_step = ms_max / args.steps
 
     if rank == 0:
         res = {
             "metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if slab else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg.name, "grid": list(cfg.grid), "cells": cfg.n,
                        "magnetic_cells": cfg.n_magnetic(), "dt_s": cfg.dt, "integrator": "RK4 (4 RHS/step)",
-                       "parallelism": "replicas" if world > 1 else "single GPU",
+                       "parallelism": (f"z-slab x{world} (NCCL)" if slab else f"replicas x{world}")
+                       if world > 1 else (f"single GPU, loopback z-slab x{args.loopback}"
+                                          if args.loopback > 1 else "single GPU"),
                        "l2": "working set > 126 MB L2 every step (no flush needed)",
                        "padded_fft": [L["Lx"], L["Ly"], L["Lz"]]},
             "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": pk["hbm_gbs"],
@@ -267,8 +285,8 @@ def main():
             "rhs_evals_per_s": 4 * value,
             "gpu_launches": launches,
             "clocks": clk.summary(),
-            "e2e": {"value": e2e_val, "unit": "cell-updates/s", "h2d_bytes_per_step": 12 * cfg.n / e2e_steps,
-                    "d2h_bytes_per_step": 12 * cfg.n / e2e_steps, "steps": e2e_steps},
+            "e2e": {"value": e2e_val, "unit": "cell-updates/s", "h2d_bytes_per_step": 12 * cfg.n * jobs / e2e_steps,
+                    "d2h_bytes_per_step": 12 * cfg.n * jobs / e2e_steps, "steps": e2e_steps},
         }
         if world == 1 and not args.no_cpu_baseline:
             res["cpu_baseline"] = cpu_baseline(cfg)

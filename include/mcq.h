@@ -25,8 +25,17 @@
  *    simulation state unchanged (except MCQ_ECUDA, after which the context must be destroyed).
  *  - Device work is enqueued on the context's stream (mcq_set_stream; default: a library-owned
  *    stream).  mcq_run / mcq_relax / setters are stream-ordered; getters synchronise.
- *  - Single GPU in this build (dist == NULL or world == 1); z-slab decomposition is planned
- *     and rejected with MCQ_EINVAL for world > 1.  Multi-GPU runs use replicas.
+ *  - z-slab decomposition, selected by mcq_dist at creation:
+ *      world == 1 (or dist NULL): one context holds the whole grid on one GPU;
+ *      world > 1, rank >= 0: one process per GPU holds planes [rank*nz/world, (rank+1)*nz/world);
+ *        the demag transpose (NCCL grouped send/recv, one all-to-all per direction per stage),
+ *        the one-plane halos and the W partials (all-gather) go over NCCL; every rank must make
+ *        the same calls in the same order (collective semantics) with the same arguments;
+ *      world > 1, rank < 0 ("loopback"): all `world` slabs live in this one context on one GPU
+ *        and the exchanges are device copies — the same decomposed schedule without a network,
+ *        bitwise equal to world == 1.
+ *    Host arrays are ALWAYS the global grid (3 nx ny nz floats); under NCCL each rank reads /
+ *    writes only its own planes of them.
  */
 #ifndef MCQ_H
 #define MCQ_H
@@ -46,7 +55,7 @@ extern "C" {
 #define MCQ_ESTATE (-2)  /* call not valid in the current state (e.g. run before set_m) */
 #define MCQ_ENOMEM (-3)  /* device allocation failed */
 #define MCQ_ECUDA (-4)   /* CUDA runtime / kernel error */
-#define MCQ_ENCCL (-5)   /* reserved for the multi-GPU build */
+#define MCQ_ENCCL (-5)   /* NCCL missing (libnccl.so.2 not loadable) or an NCCL call failed */
 
 /* field-term bitmask for mcq_get_field */
 #define MCQ_TERM_ZEEMAN 1u
@@ -76,12 +85,20 @@ typedef struct {
   double kc1, c1[3], c2[3];
 } mcq_aniso;
 
-/* Distribution descriptor.  This build: world must be 1 (or pass NULL). */
+/* Distribution descriptor (z slabs, see Conventions).  world must divide nz (1 <= world <= 64).
+ * rank in [0, world) with nccl_id (128 bytes from mcq_nccl_get_unique_id on one rank, shared by
+ * the caller, e.g. via torch.distributed) = one slab per process over NCCL; rank < 0 = loopback.
+ * device >= 0 selects the CUDA device (else the current one); cuda_stream: the work stream or
+ * NULL (library-owned). */
 typedef struct {
   int rank, world, device;
   const unsigned char *nccl_id; /* 128 bytes or NULL */
   void *cuda_stream;            /* cudaStream_t or NULL */
 } mcq_dist;
+
+/* NCCL unique id for a multi-process context (128 bytes into out).  ENCCL if libnccl.so.2
+ * cannot be loaded. */
+MCQ_API int mcq_nccl_get_unique_id(unsigned char out[128]);
 
 /* Cavity state at t_n (all ranks identical).  S, C are the paper's accumulators,
  * reconstructed from alpha: S - i C = (hbar/V_c)(alpha_0 - e^{(kappa + i w_c) t} alpha). */

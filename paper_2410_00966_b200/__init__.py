@@ -36,7 +36,18 @@ def _d3(v):
 
 # ---------------------------------------------------------------- ABI-named functions
 
+def mcq_nccl_get_unique_id():
+    """128-byte NCCL unique id (bytes) for a multi-process context (include/mcq.h)."""
+    buf = (C.c_ubyte * 128)()
+    rc = lib.mcq_nccl_get_unique_id(buf)
+    if rc != 0:
+        raise MCQError(rc, "mcq_nccl_get_unique_id failed (libnccl.so.2 not loadable)")
+    return bytes(buf)
+
+
 def mcq_create(grid, cell, Ms, Aex, alpha, K=None, dist=None):
+    """dist: None or {"rank", "world", "device", "nccl_id" (bytes), "stream"}; rank < 0 = loopback
+    slabs in this process (include/mcq.h, mcq_dist)."""
     h = C.c_void_p()
     g = (C.c_int * 3)(*[int(x) for x in grid])
     c = (C.c_double * 3)(*[float(x) for x in cell])
@@ -50,9 +61,13 @@ def mcq_create(grid, cell, Ms, Aex, alpha, K=None, dist=None):
         k.c2 = _d3(K.get("c2", (0, 1, 0)))
         kp = C.pointer(k)
     dp = None
+    idbuf = None
     if dist is not None:
-        d = mcq_dist(int(dist.get("rank", 0)), int(dist.get("world", 1)), int(dist.get("device", -1)), None,
-                     dist.get("stream"))
+        nid = dist.get("nccl_id")
+        if nid is not None:
+            idbuf = (C.c_ubyte * 128).from_buffer_copy(bytes(nid))
+        d = mcq_dist(int(dist.get("rank", 0)), int(dist.get("world", 1)), int(dist.get("device", -1)),
+                     C.cast(idbuf, C.c_void_p) if idbuf is not None else None, dist.get("stream"))
         dp = C.pointer(d)
     rc = lib.mcq_create(C.byref(h), g, c, float(Ms), float(Aex), float(alpha), kp, dp)
     if rc != 0:
@@ -203,14 +218,17 @@ def mcq_destroy(ctx):
 class Solver:
     """Owns one context; methods forward to the ABI functions above."""
 
-    def __init__(self, grid, cell, Ms, Aex, alpha, aniso=None, stream=None):
+    def __init__(self, grid, cell, Ms, Aex, alpha, aniso=None, stream=None, dist=None):
         self.grid = tuple(int(g) for g in grid)
         self.n = self.grid[0] * self.grid[1] * self.grid[2]
-        self.ctx = mcq_create(grid, cell, Ms, Aex, alpha, aniso, {"stream": stream} if stream else None)
+        d = dict(dist or {})
+        if stream:
+            d["stream"] = stream
+        self.ctx = mcq_create(grid, cell, Ms, Aex, alpha, aniso, d or None)
 
     @classmethod
-    def from_config(cls, cfg, stream=None, set_state=True):
-        s = cls(cfg.grid, cfg.cell, cfg.Ms, cfg.Aex, cfg.alpha, cfg.aniso, stream)
+    def from_config(cls, cfg, stream=None, set_state=True, dist=None):
+        s = cls(cfg.grid, cfg.cell, cfg.Ms, cfg.Aex, cfg.alpha, cfg.aniso, stream, dist)
         if cfg.mask is not None:
             mcq_set_geometry(s.ctx, cfg.mask)
         mcq_set_bext(s.ctx, cfg.bext)

@@ -51,6 +51,7 @@ lib = C.CDLL(LIB_PATH)
 
 _P = C.c_void_p
 _sig = {
+    "mcq_nccl_get_unique_id": (C.c_int, [_P]),
     "mcq_create": (C.c_int, [C.POINTER(_P), C.POINTER(C.c_int), C.POINTER(C.c_double), C.c_double, C.c_double,
                              C.c_double, C.POINTER(mcq_aniso), C.POINTER(mcq_dist)]),
     "mcq_set_stream": (C.c_int, [_P, _P]),

@@ -48,7 +48,7 @@ def build(force=False, verbose=False, jobs=4):
         raise RuntimeError("nvcc failed:\n" + "\n".join(errs))
     # exported C ABI symbols need default visibility: they are marked in mcq.h via extern "C"
     cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB + ".tmp", *objs,
-           "-lcudart"]
+           "-lcudart", "-ldl"]
     subprocess.check_call(cmd)
     os.replace(LIB + ".tmp", LIB)
     for o in objs:

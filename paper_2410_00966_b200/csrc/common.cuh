@@ -14,13 +14,24 @@ constexpr int kTwMax = 1024;                     // global twiddle table length 
 //   X[c][z][y][P]    complex64 (x-spectrum of m; the demag spectrum in place), rows 16-byte aligned
 //   Y[c][z][ky][P]   complex64 (after the y transform; only the nz real z planes)
 //   Khat[g][kz][ky][P] fp32, kz <= Lz/2, ky <= Ly/2 (real, folded; g = XX,YY,ZZ,XY,XZ,YZ)
+//
+// z-slab decomposition over NS ranks: nz below is the rank's number of planes,
+// nzg the global one, zg0 the global index of local plane 0.  State arrays carry zoff (0 or 1)
+// halo planes on each side: cell (x, y, z) of component c sits at c*cs + ((z+zoff)*ny + y)*nx + x.
+// Y is kx-slab-major: Y[q][c][z][ky][KXS] with q = kx / KXS the rank owning column kx in the
+// z pass; for NS == 1 this is exactly Y[c][z][ky][P] (KXS == P).  After the forward all-to-all a
+// rank holds R[r][c][zl][ky][KXS] (r = source rank, z = r*nz + zl) for its KXS columns.
 struct Dims {
-  int nx, ny, nz;     // grid
-  int Lx, Ly, Lz;     // zero-padded FFT lengths (next pow2 >= 2n; 1 if n == 1)
+  int nx, ny, nz;     // grid (nz: local planes)
+  int Lx, Ly, Lz;     // zero-padded FFT lengths (next pow2 >= 2n; 1 if n == 1), Lz from nzg
   int N2;             // Lx / 2: complex length of the packed real x-transform
   int NKX;            // Lx / 2 + 1: x-spectrum columns (Hermitian half)
   int P;              // row pitch of the spectra (complex), NKX rounded up to 16 (128-byte rows)
-  long long N;        // nx * ny * nz
+  long long N;        // nx * ny * nz (local cells)
+  int nzg, zg0, zoff; // global planes, global z of local plane 0, halo planes per side
+  long long cs;       // component stride of the state arrays: nx * ny * (nz + 2 zoff)
+  int NS, KXS;        // kx slabs (ranks) and their width; NS * KXS >= NKX
+  int kx0;            // first kx column of this rank's slab in the z pass (rank * KXS)
 };
 
 // Cavity state on the device (fp64), advanced once per step by k_cavity (a13).
@@ -91,10 +102,10 @@ void launch_update(const UpdateArgs& a, const float2* tw, cudaStream_t s);
 int update_grid_blocks(const Dims& d);
 void launch_cavity(const CavParams& p, CavState* st, const double* partials, int n, cudaStream_t s);
 void launch_cav_prepare(const CavParams& p, CavState* st, cudaStream_t s);
-void launch_aos_to_soa(const float* in, float* out, const uint8_t* mask, long long N, int* bad,
-                       cudaStream_t s);
-void launch_soa_to_aos(const float* in, float* out, long long N, cudaStream_t s);
-void launch_deinterleave(const float* in, float* out, long long N, cudaStream_t s);
+void launch_aos_to_soa(const float* in, float* out, const uint8_t* mask, long long N, long long cs, long long off,
+                       int* bad, cudaStream_t s);
+void launch_soa_to_aos(const float* in, float* out, long long N, long long cs, long long off, cudaStream_t s);
+void launch_deinterleave(const float* in, float* out, long long N, long long cs, long long off, cudaStream_t s);
 // tensor.cu
 void launch_tensor_octant(double* oct, const Dims& d, double dx, double dy, double dz,
                           cudaStream_t s);

@@ -1,16 +1,24 @@
 // mcq.cu — host runtime and C ABI (include/mcq.h) of the B200-native Mumax3-cQED hot path.
 //
 // One step: for each RK4 stage s = 1..4
-//     [3D] K-Y (X->Y), K-Z (Y, Khat), K-YI (Y->X)   |   [nz == 1] K-Y2D (X, Khat)
+//     [z slabs > 1] halo exchange of the stage state (one plane per side)
+//     [3D] K-Y (X->Y), [slabs > 1] all-to-all Y -> R, K-Z (Khat), [slabs > 1] all-to-all back,
+//          K-YI (Y->X)                                   |   [nz == 1] K-Y2D (X, Khat)
 //     K-U(stage s): x-C2R demag + fields + torque + RK4 combine + x-R2C of m_{s+1} (+ W partials)
-// then K-CAV: fixed-order W sum, alpha_{n+1}, t_{n+1}, stage factors of the next step.
-// Steps are captured once into CUDA graphs and replayed; the host never synchronises inside
-// mcq_run.  Device memory is owned by the context (cudaMalloc); work runs on the context
-// stream (library-owned, or the caller's via mcq_set_stream).
+// then [slabs > 1] all-gather of the W partials and K-CAV: fixed-order W sum, alpha_{n+1},
+// t_{n+1}, stage factors of the next step.
+// The grid is split into z slabs: one slab per process over NCCL (one GPU each),
+// or all slabs inside one process on one GPU ("loopback": the exchanges become device copies —
+// the test vehicle of the decomposition, bitwise equal to the undecomposed run).  Steps are
+// captured once into CUDA graphs (kernels, copies and NCCL calls) and replayed; the host never
+// synchronises inside mcq_run.  Device memory is owned by the context (cudaMalloc).
 #include <cuda.h>  // CUtensorMap; cuTensorMapEncodeTiled is fetched with cudaGetDriverEntryPoint
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl is dlopen'ed when a multi-process context is created
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -25,38 +33,100 @@
 
 using namespace mcq;
 
-struct mcq_ctx {
+namespace {
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+struct Nccl {
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  const char* (*errStr)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+Nccl* nccl_api() {
+  static Nccl api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    // prefer the libnccl already loaded in this process (torch's), else the system one
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen(getenv("MCQ_NCCL_LIB") ? getenv("MCQ_NCCL_LIB") : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+#define S_(field, sym) api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, sym))
+    S_(getUniqueId, "ncclGetUniqueId");
+    S_(commInitRank, "ncclCommInitRank");
+    S_(commDestroy, "ncclCommDestroy");
+    S_(send, "ncclSend");
+    S_(recv, "ncclRecv");
+    S_(allGather, "ncclAllGather");
+    S_(allReduce, "ncclAllReduce");
+    S_(groupStart, "ncclGroupStart");
+    S_(groupEnd, "ncclGroupEnd");
+    S_(errStr, "ncclGetErrorString");
+#undef S_
+    api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.send && api.recv && api.allGather &&
+             api.allReduce && api.groupStart && api.groupEnd && api.errStr;
+  });
+  return api.ok ? &api : nullptr;
+}
+
+// One z slab: its planes of the state (with halo planes when split), its spectra and maps.
+struct Slab {
   Dims d{};
+  float *mN = nullptr, *mA = nullptr, *mB = nullptr, *acc = nullptr;  // [3][cs]
+  float2 *X = nullptr, *Y = nullptr, *R = nullptr;  // X [3][nz][ny][P]; Y, R [NS][3][nz][Ly][KXS]
+  float *brms = nullptr, *field = nullptr;          // [3][cs]
+  uint8_t* mask = nullptr;                          // [nz][ny][nx]
+  double* partials = nullptr;                       // into ctx partials (loopback) or own (NCCL)
+  int nparts = 0;
+};
+
+}  // namespace
+
+struct mcq_ctx {
+  Dims dg{};  // global dims (nz = global planes; used for the tensor and the layout report)
   double dx = 0, dy = 0, dz = 0, Ms = 0, Aex = 0, alpha = 0;
   mcq_aniso K{};
   int device = 0;
+  int NS = 1;       // slabs
+  int rank = 0;     // this process's slab (NCCL mode)
+  int mode = 0;     // 0 single, 1 loopback (all slabs here), 2 NCCL (one slab per process)
+  ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr;  // work stream (user's or own)
   cudaStream_t own = nullptr;
   cudaStream_t cap = nullptr;     // capture stream
-  float *mN = nullptr, *mA = nullptr, *mB = nullptr, *acc = nullptr;
-  float2 *X = nullptr, *Y = nullptr, *tw = nullptr;
+  std::vector<Slab> sl;
+  float2* tw = nullptr;
   float* khat = nullptr;
-  float* brms = nullptr;
   double brms_u[3] = {0, 0, 0};
+  bool brms_map = false;
   bool cav_on = false;
-  uint8_t* mask = nullptr;
+  bool have_mask = false;
   double bext[3] = {0, 0, 0};
   double fc = 1e9, kappa = 0, x0 = 0, p0 = 0, exc_amp = 0, exc_omega = 0;
   CavState* cav = nullptr;
-  double* partials = nullptr;
+  double* partials = nullptr;  // all slabs' per-CTA overlap partials in global z order
   int nparts = 0;
-  float* fieldbuf = nullptr;
   unsigned* maxbits = nullptr;
   int* bad = nullptr;
-  float* io = nullptr;
+  float* io = nullptr;  // AoS staging for the cells this context holds
   bool m_set = false;
   // graphs: [0] = 1 LLG step, [1] = kGraphSteps LLG steps, [2] = 1 relax step, [3] = relax chunk
   cudaGraphExec_t g[4] = {nullptr, nullptr, nullptr, nullptr};
   double g_dt[4] = {0, 0, 0, 0};
   long long launches = 0;
-  alignas(64) CUtensorMap tmz;  // TMA descriptor of Y for the pipelined K-Z kernel
+  alignas(64) CUtensorMap tmz;  // TMA descriptor of Y for the pipelined K-Z kernel (1 slab)
   bool have_tmz = false;
   std::string err;
+  long long cells_here() const { return (long long)sl.size() * sl[0].d.N; }
+  long long first_cell() const { return mode == 2 ? (long long)rank * sl[0].d.N : 0; }
 };
 
 namespace {
@@ -75,6 +145,12 @@ int fail(mcq_ctx* c, int code, const std::string& msg) {
     if (e_ != cudaSuccess)                                                                 \
       return fail(ctx, e_ == cudaErrorMemoryAllocation ? MCQ_ENOMEM : MCQ_ECUDA,           \
                   std::string(#call) + ": " + cudaGetErrorString(e_));                     \
+  } while (0)
+
+#define NK(ctx, call)                                                                          \
+  do {                                                                                         \
+    ncclResult_t r_ = (call);                                                                  \
+    if (r_ != ncclSuccess) return fail(ctx, MCQ_ENCCL, std::string(#call) + ": " + nccl_api()->errStr(r_)); \
   } while (0)
 
 int next_pow2(int n) {
@@ -110,11 +186,11 @@ CavParams cav_params(const mcq_ctx* c, double dt) {
   return p;
 }
 
-UpdateArgs base_args(const mcq_ctx* c) {
+UpdateArgs base_args(const mcq_ctx* c, const Slab& s) {
   UpdateArgs a{};
-  a.d = c->d;
+  a.d = s.d;
   a.terms = MCQ_TERM_ALL;
-  a.brms = c->brms;
+  a.brms = c->brms_map ? s.brms : nullptr;
   for (int i = 0; i < 3; ++i) {
     a.brms_u[i] = (float)c->brms_u[i];
     a.bext[i] = (float)c->bext[i];
@@ -148,11 +224,11 @@ UpdateArgs base_args(const mcq_ctx* c) {
   a.alpha = (float)c->alpha;
   a.gamma = (float)kGamma;
   a.cav = c->cav;
-  a.partials = c->partials;
-  a.bout = c->fieldbuf;
+  a.partials = s.partials;
+  a.bout = s.field;
   a.maxbits = c->maxbits;
-  a.X = c->X;
-  a.acc = c->acc;
+  a.X = s.X;
+  a.acc = s.acc;
   a.demag = 1;
   return a;
 }
@@ -166,6 +242,7 @@ struct Enq {
   KernelHook hook = nullptr;
   void* user = nullptr;
   long long count = 0;
+  int rc = MCQ_OK;  // first failure of a copy / NCCL call
   void pre(int k) {
     if (hook) hook(user, k, true);
   }
@@ -173,52 +250,140 @@ struct Enq {
     ++count;
     if (hook) hook(user, k, false);
   }
-  void demag() {
-    const Dims& d = c->d;
-    if (d.nz > 1) {
-      pre(MCQ_K_YFWD);
-      launch_yfwd(d, c->X, c->Y, c->tw, s);
-      post(MCQ_K_YFWD);
-      pre(MCQ_K_ZCONV);
-      // K-Z variant (measured on configs[1], 1x B200: seq 170 us, tma 180 us, plain 206 us per
-      // launch); MCQ_ZVARIANT=tma|plain selects the others (experiments / profiling)
-      static const char* zv = getenv("MCQ_ZVARIANT");
-      if (zv && !strcmp(zv, "tma") && c->have_tmz)
-        launch_zconv_tma(d, &c->tmz, c->Y, c->khat, c->tw, s);
-      else if (zv && !strcmp(zv, "plain"))
-        launch_zconv(d, c->Y, c->khat, c->tw, s);
-      else
-        launch_zconv_seq(d, c->Y, c->khat, c->tw, s);
-      post(MCQ_K_ZCONV);
-      pre(MCQ_K_YINV);
-      launch_yinv(d, c->Y, c->X, c->tw, s);
-      post(MCQ_K_YINV);
+  void copy(void* dst, const void* src, size_t bytes) {
+    if (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s) != cudaSuccess && rc == MCQ_OK)
+      rc = fail(c, MCQ_ECUDA, "slab exchange copy");
+  }
+  void nk(ncclResult_t r) {
+    if (r != ncclSuccess && rc == MCQ_OK) rc = fail(c, MCQ_ENCCL, nccl_api()->errStr(r));
+  }
+  // one plane per side of the state buffer `which` (0 mN, 1 mA, 2 mB) into the neighbours' halos
+  void halo(int which) {
+    if (c->NS == 1) return;
+    auto buf = [&](Slab& t) { return which == 0 ? t.mN : (which == 1 ? t.mA : t.mB); };
+    const Dims& d = c->sl[0].d;
+    const size_t pl = (size_t)d.nx * d.ny;
+    const size_t bytes = pl * sizeof(float);
+    if (c->mode == 1) {
+      for (int r = 0; r < c->NS; ++r)
+        for (int cc = 0; cc < 3; ++cc) {
+          float* mine = buf(c->sl[r]) + cc * d.cs;
+          if (r > 0) copy(buf(c->sl[r - 1]) + cc * d.cs + (d.nz + 1) * pl, mine + 1 * pl, bytes);
+          if (r < c->NS - 1) copy(buf(c->sl[r + 1]) + cc * d.cs, mine + d.nz * pl, bytes);
+        }
     } else {
-      pre(MCQ_K_Y2D);
-      launch_y2d(d, c->X, c->khat, c->tw, s);
-      post(MCQ_K_Y2D);
+      Nccl* n = nccl_api();
+      float* b = buf(c->sl[0]);
+      nk(n->groupStart());
+      for (int cc = 0; cc < 3; ++cc) {
+        float* mine = b + cc * d.cs;
+        if (c->rank > 0) {
+          nk(n->send(mine + pl, pl, ncclFloat, c->rank - 1, c->comm, s));
+          nk(n->recv(mine, pl, ncclFloat, c->rank - 1, c->comm, s));
+        }
+        if (c->rank < c->NS - 1) {
+          nk(n->send(mine + d.nz * pl, pl, ncclFloat, c->rank + 1, c->comm, s));
+          nk(n->recv(mine + (d.nz + 1) * pl, pl, ncclFloat, c->rank + 1, c->comm, s));
+        }
+      }
+      nk(n->groupEnd());
     }
   }
-  void update(UpdateArgs a) {
+  // Y[q] of every slab r  <->  R[r] of slab q  (the z-slab <-> kx-slab transpose)
+  void alltoall(bool forward) {
+    const Dims& d = c->sl[0].d;
+    const size_t blk = (size_t)3 * d.nz * d.Ly * d.KXS;  // complex per (source, destination) block
+    if (c->mode == 1) {
+      for (int r = 0; r < c->NS; ++r)
+        for (int q = 0; q < c->NS; ++q) {
+          float2* y = c->sl[r].Y + q * blk;
+          float2* rr = c->sl[q].R + r * blk;
+          if (forward)
+            copy(rr, y, blk * sizeof(float2));
+          else
+            copy(y, rr, blk * sizeof(float2));
+        }
+    } else {
+      Nccl* n = nccl_api();
+      Slab& sl = c->sl[0];
+      nk(n->groupStart());
+      for (int q = 0; q < c->NS; ++q) {
+        float2* y = sl.Y + q * blk;
+        float2* rr = sl.R + q * blk;
+        nk(n->send(forward ? (const void*)y : (const void*)rr, 2 * blk, ncclFloat, q, c->comm, s));
+        nk(n->recv(forward ? (void*)rr : (void*)y, 2 * blk, ncclFloat, q, c->comm, s));
+      }
+      nk(n->groupEnd());
+    }
+  }
+  void demag() {
+    const int NS = c->NS;
+    const Dims& d0 = c->sl[0].d;
+    if (d0.nzg > 1) {
+      for (auto& sl : c->sl) {
+        pre(MCQ_K_YFWD);
+        launch_yfwd(sl.d, sl.X, sl.Y, c->tw, s);
+        post(MCQ_K_YFWD);
+      }
+      if (NS > 1) alltoall(true);
+      for (auto& sl : c->sl) {
+        float2* Z = NS > 1 ? sl.R : sl.Y;
+        pre(MCQ_K_ZCONV);
+        // K-Z variant (measured on configs[1], 1x B200: seq 170 us, tma 180 us, plain 206 us per
+        // launch); MCQ_ZVARIANT=tma|plain selects the others (single slab only)
+        static const char* zv = getenv("MCQ_ZVARIANT");
+        if (NS == 1 && zv && !strcmp(zv, "tma") && c->have_tmz)
+          launch_zconv_tma(sl.d, &c->tmz, Z, c->khat, c->tw, s);
+        else if (NS == 1 && zv && !strcmp(zv, "plain"))
+          launch_zconv(sl.d, Z, c->khat, c->tw, s);
+        else
+          launch_zconv_seq(sl.d, Z, c->khat, c->tw, s);
+        post(MCQ_K_ZCONV);
+      }
+      if (NS > 1) alltoall(false);
+      for (auto& sl : c->sl) {
+        pre(MCQ_K_YINV);
+        launch_yinv(sl.d, sl.Y, sl.X, c->tw, s);
+        post(MCQ_K_YINV);
+      }
+    } else {
+      for (auto& sl : c->sl) {
+        pre(MCQ_K_Y2D);
+        launch_y2d(sl.d, sl.X, c->khat, c->tw, s);
+        post(MCQ_K_Y2D);
+      }
+    }
+  }
+  void update(const UpdateArgs& a) {
     pre(MCQ_K_UPDATE);
     launch_update(a, c->tw, s);
     post(MCQ_K_UPDATE);
   }
   void stage(int st, double dt, int mode, unsigned terms) {
-    UpdateArgs a = base_args(c);
-    a.mode = mode;
-    a.stage = st;
-    a.terms = terms;
-    a.mN = c->mN;
-    a.mS = st == 1 ? c->mN : (st == 2 ? c->mA : (st == 3 ? c->mB : c->mA));
-    a.mOut = st == 1 ? c->mA : (st == 2 ? c->mB : (st == 3 ? c->mA : c->mN));
-    a.h = (float)(st == 3 ? dt : 0.5 * dt);
-    a.dt6 = (float)(dt / 6.0);
+    const int sin_ = st == 1 ? 0 : (st == 2 ? 1 : (st == 3 ? 2 : 1));  // stage state buffer
+    halo(sin_);
     demag();
-    update(a);
+    for (auto& sl : c->sl) {
+      UpdateArgs a = base_args(c, sl);
+      a.mode = mode;
+      a.stage = st;
+      a.terms = terms;
+      a.mN = sl.mN;
+      a.mS = st == 1 ? sl.mN : (st == 2 ? sl.mA : (st == 3 ? sl.mB : sl.mA));
+      a.mOut = st == 1 ? sl.mA : (st == 2 ? sl.mB : (st == 3 ? sl.mA : sl.mN));
+      a.h = (float)(st == 3 ? dt : 0.5 * dt);
+      a.dt6 = (float)(dt / 6.0);
+      update(a);
+    }
+  }
+  void gather_partials() {
+    if (c->mode != 2) return;  // single / loopback: every slab already wrote into c->partials
+    Slab& sl = c->sl[0];
+    nk(nccl_api()->allGather(sl.partials, c->partials, sl.nparts, ncclDouble, c->comm, s));
   }
   void llg_step(double dt) {
     for (int st = 1; st <= 4; ++st) stage(st, dt, MODE_LLG, MCQ_TERM_ALL);
+    gather_partials();
     const CavParams p = cav_params(c, dt);
     pre(MCQ_K_CAVITY);
     launch_cavity(p, c->cav, c->partials, c->nparts, s);
@@ -228,25 +393,30 @@ struct Enq {
     for (int st = 1; st <= 4; ++st)
       stage(st, dt, MODE_RELAX, MCQ_TERM_ALL & ~(MCQ_TERM_CAVITY | MCQ_TERM_EXCITATION));
   }
-  void x0() {  // X <- R2C(m_n)
-    UpdateArgs a = base_args(c);
-    a.mode = MODE_X0;
-    a.stage = 1;
-    a.mS = c->mN;
-    a.mN = c->mN;
-    a.mOut = c->mN;
-    update(a);
+  void x0() {  // X <- R2C(m_n) in every slab
+    for (auto& sl : c->sl) {
+      UpdateArgs a = base_args(c, sl);
+      a.mode = MODE_X0;
+      a.stage = 1;
+      a.mS = sl.mN;
+      a.mN = sl.mN;
+      a.mOut = sl.mN;
+      update(a);
+    }
   }
   void eval(int mode, unsigned terms) {  // field / max-torque of m_n at stage 1, then restore X
-    UpdateArgs a = base_args(c);
-    a.mode = mode;
-    a.stage = 1;
-    a.terms = terms;
-    a.mS = c->mN;
-    a.mN = c->mN;
-    a.mOut = c->mN;
+    halo(0);
     demag();
-    update(a);
+    for (auto& sl : c->sl) {
+      UpdateArgs a = base_args(c, sl);
+      a.mode = mode;
+      a.stage = 1;
+      a.terms = terms;
+      a.mS = sl.mN;
+      a.mN = sl.mN;
+      a.mOut = sl.mN;
+      update(a);
+    }
     x0();
   }
 };
@@ -268,9 +438,10 @@ int capture(mcq_ctx* c, int which, double dt, int steps) {
   cudaGraph_t graph = nullptr;
   cudaError_t e1 = cudaStreamEndCapture(c->cap, &graph);
   cudaError_t e2 = cudaPeekAtLastError();
-  if (e1 != cudaSuccess || e2 != cudaSuccess || !graph) {
+  if (e1 != cudaSuccess || e2 != cudaSuccess || !graph || q.rc != MCQ_OK) {
     if (graph) cudaGraphDestroy(graph);
     cudaGetLastError();
+    if (q.rc != MCQ_OK) return q.rc;
     return fail(c, MCQ_ECUDA, std::string("graph capture failed: ") + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
   }
   cudaError_t e3 = cudaGraphInstantiate(&c->g[which], graph, 0);
@@ -280,12 +451,9 @@ int capture(mcq_ctx* c, int which, double dt, int steps) {
   return MCQ_OK;
 }
 
-int demag_kernels(const mcq_ctx* c) {
-  return c->d.nz > 1 ? 3 : 1;
-}
-
 long long kernels_per_step(const mcq_ctx* c, bool llg) {
-  return 4LL * (demag_kernels(c) + 1) + (llg ? 1 : 0);
+  const int demag = c->dg.nz > 1 ? 3 : 1;
+  return (long long)c->sl.size() * 4 * (demag + 1) + (llg ? 1 : 0);
 }
 
 int set_cav_state(mcq_ctx* c, double re, double im, double t, long long step) {
@@ -319,9 +487,9 @@ void axis_matrices(int L, std::vector<double>& Tc, std::vector<double>& Ts) {
     }
 }
 
-// K-TEN: octant -> x, y, z cosine/sine sums -> folded, scaled fp32 Khat
+// K-TEN: octant -> x, y, z cosine/sine sums -> folded, scaled fp32 Khat (global grid)
 int build_khat(mcq_ctx* c, double* oct_out /* optional host copy of the octant */) {
-  const Dims& d = c->d;
+  const Dims& d = c->dg;
   const int m0 = d.Lx / 2 + 1, m1 = d.Ly / 2 + 1, m2 = d.Lz / 2 + 1;
   const size_t n = 6ULL * m0 * m1 * m2;
   double *a = nullptr, *b = nullptr, *T = nullptr;
@@ -370,21 +538,29 @@ int build_khat(mcq_ctx* c, double* oct_out /* optional host copy of the octant *
 
 void free_all(mcq_ctx* c) {
   invalidate_graphs(c);
-  void* ptrs[] = {c->mN, c->mA, c->mB, c->acc, c->X, c->Y, c->tw, c->khat, c->brms, c->mask,
-                  c->cav, c->partials, c->fieldbuf, c->maxbits, c->bad, c->io};
+  for (auto& s : c->sl) {
+    void* ptrs[] = {s.mN, s.mA, s.mB, s.acc, s.X, s.Y, s.R, s.brms, s.field, s.mask};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    if (c->mode == 2 && s.partials) cudaFree(s.partials);
+  }
+  c->sl.clear();
+  void* ptrs[] = {c->tw, c->khat, c->cav, c->partials, c->maxbits, c->bad, c->io};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (c->comm) nccl_api()->commDestroy(c->comm);
+  c->comm = nullptr;
   if (c->own) cudaStreamDestroy(c->own);
   if (c->cap) cudaStreamDestroy(c->cap);
 }
 
 // TMA descriptor of Y[3][nz][Ly][P] viewed as a 3D tensor (P, Ly, 3 nz) of 8-byte elements;
-// box (C, 1, nz) = one component's z column block of a K-Z tile.  Without it (nz > 256, or no
-// driver entry point) K-Z falls back to plain loads.
+// box (C, 1, nz) = one component's z column block of a K-Z tile (single slab only).
 void make_y_tensor_map(mcq_ctx* c) {
-  const Dims& d = c->d;
   c->have_tmz = false;
-  if (d.nz < 2 || d.nz > 256 || !c->Y) return;
+  if (c->NS != 1) return;
+  const Dims& d = c->sl[0].d;
+  if (d.nz < 2 || d.nz > 256 || !c->sl[0].Y) return;
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   if (!enc) {
     void* fn = nullptr;
@@ -400,10 +576,34 @@ void make_y_tensor_map(mcq_ctx* c) {
   const cuuint32_t box[3] = {(cuuint32_t)zconv_tma_box_c(d.Lz), 1, (cuuint32_t)d.nz};
   const cuuint32_t es[3] = {1, 1, 1};
   if (box[0] == 0) return;
-  const CUresult r = enc(&c->tmz, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->Y, dims, strides, box, es,
+  const CUresult r = enc(&c->tmz, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->sl[0].Y, dims, strides, box, es,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   c->have_tmz = (r == CUDA_SUCCESS);
+}
+
+int alloc_slab(mcq_ctx* c, Slab& s) {
+  const Dims& d = s.d;
+  const size_t st = 3ULL * d.cs;
+  const size_t nX = 3ULL * d.nz * d.ny * d.P;
+  const size_t nY = d.nzg > 1 ? (size_t)d.NS * 3 * d.nz * d.Ly * d.KXS : 0;
+  bool ok = cudaMalloc(&s.mN, st * 4) == cudaSuccess && cudaMalloc(&s.mA, st * 4) == cudaSuccess &&
+            cudaMalloc(&s.mB, st * 4) == cudaSuccess && cudaMalloc(&s.acc, st * 4) == cudaSuccess &&
+            cudaMalloc(&s.X, nX * 8) == cudaSuccess && (nY == 0 || cudaMalloc(&s.Y, nY * 8) == cudaSuccess) &&
+            (nY == 0 || d.NS == 1 || cudaMalloc(&s.R, nY * 8) == cudaSuccess);
+  if (!ok) {
+    cudaGetLastError();
+    return fail(c, MCQ_ENOMEM, "slab buffers");
+  }
+  // zero everything once (halo planes at the global boundary and padding columns stay finite)
+  CK(c, cudaMemsetAsync(s.mN, 0, st * 4, c->stream));
+  CK(c, cudaMemsetAsync(s.mA, 0, st * 4, c->stream));
+  CK(c, cudaMemsetAsync(s.mB, 0, st * 4, c->stream));
+  CK(c, cudaMemsetAsync(s.acc, 0, st * 4, c->stream));
+  CK(c, cudaMemsetAsync(s.X, 0, nX * 8, c->stream));
+  if (nY) CK(c, cudaMemsetAsync(s.Y, 0, nY * 8, c->stream));
+  if (s.R) CK(c, cudaMemsetAsync(s.R, 0, nY * 8, c->stream));
+  return MCQ_OK;
 }
 
 std::once_flag g_cfg_once;
@@ -413,6 +613,17 @@ std::once_flag g_cfg_once;
 // ====================================================================== C ABI
 extern "C" {
 
+int mcq_nccl_get_unique_id(unsigned char out[128]) {
+  if (!out) return MCQ_EINVAL;
+  Nccl* n = nccl_api();
+  if (!n) return MCQ_ENCCL;
+  ncclUniqueId id;
+  if (n->getUniqueId(&id) != ncclSuccess) return MCQ_ENCCL;
+  static_assert(sizeof(id.internal) == 128, "ncclUniqueId size");
+  std::memcpy(out, id.internal, 128);
+  return MCQ_OK;
+}
+
 int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms, double Aex, double alpha,
                const mcq_aniso* K, const mcq_dist* dist) {
   if (!out || !grid || !cell) return MCQ_EINVAL;
@@ -420,7 +631,9 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
   if (grid[0] < 2 || grid[1] < 2 || grid[2] < 1 || grid[0] > 512 || grid[1] > 512 || grid[2] > 512) return MCQ_EINVAL;
   if (!(cell[0] > 0 && cell[1] > 0 && cell[2] > 0)) return MCQ_EINVAL;
   if (!(Ms > 0) || !(Aex >= 0) || !(alpha >= 0)) return MCQ_EINVAL;
-  if (dist && dist->world > 1) return MCQ_EINVAL;  // z-slab decomposition: not in this build
+  const int world = dist ? dist->world : 1;
+  if (world < 1 || world > 64 || grid[2] % world || (world > 1 && grid[2] / world < 1)) return MCQ_EINVAL;
+  if (world > 1 && dist->rank >= 0 && (dist->rank >= world || !dist->nccl_id)) return MCQ_EINVAL;
   mcq_ctx* c = new (std::nothrow) mcq_ctx();
   if (!c) return MCQ_ENOMEM;
   c->dx = cell[0];
@@ -430,17 +643,27 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
   c->Aex = Aex;
   c->alpha = alpha;
   if (K) c->K = *K;
-  Dims& d = c->d;
-  d.nx = grid[0];
-  d.ny = grid[1];
-  d.nz = grid[2];
-  d.Lx = padded(d.nx);
-  d.Ly = padded(d.ny);
-  d.Lz = padded(d.nz);
-  d.N2 = d.Lx / 2;
-  d.NKX = d.N2 + 1;
-  d.P = (d.NKX + 15) / 16 * 16;  // 128-byte aligned spectrum rows: whole-sector column tiles, TMA rows
-  d.N = (long long)d.nx * d.ny * d.nz;
+  c->NS = world;
+  c->mode = world == 1 ? 0 : (dist->rank < 0 ? 1 : 2);
+  c->rank = c->mode == 2 ? dist->rank : 0;
+  Dims& g = c->dg;
+  g.nx = grid[0];
+  g.ny = grid[1];
+  g.nz = grid[2];
+  g.Lx = padded(g.nx);
+  g.Ly = padded(g.ny);
+  g.Lz = padded(g.nz);
+  g.N2 = g.Lx / 2;
+  g.NKX = g.N2 + 1;
+  g.P = (g.NKX + 15) / 16 * 16;  // 128-byte aligned spectrum rows: whole-sector column tiles, TMA rows
+  g.N = (long long)g.nx * g.ny * g.nz;
+  g.nzg = g.nz;
+  g.zg0 = 0;
+  g.zoff = 0;
+  g.cs = g.N;
+  g.NS = 1;
+  g.KXS = g.P;
+  g.kx0 = 0;
   auto bail = [&](int code) {
     free_all(c);
     delete c;
@@ -458,29 +681,57 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
       cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess)
     return bail(MCQ_ECUDA);
   c->stream = (dist && dist->cuda_stream) ? (cudaStream_t)dist->cuda_stream : c->own;
-  const size_t N3 = 3ULL * d.N;
-  const size_t nX = 3ULL * d.nz * d.ny * d.P;
-  const size_t nY = d.nz > 1 ? 3ULL * d.nz * d.Ly * d.P : 0;
-  const size_t nK = 6ULL * (d.Lz / 2 + 1) * (d.Ly / 2 + 1) * d.P;
-  c->nparts = update_grid_blocks(d);
-  bool ok = cudaMalloc(&c->mN, N3 * 4) == cudaSuccess && cudaMalloc(&c->mA, N3 * 4) == cudaSuccess &&
-            cudaMalloc(&c->mB, N3 * 4) == cudaSuccess && cudaMalloc(&c->acc, N3 * 4) == cudaSuccess &&
-            cudaMalloc(&c->X, nX * 8) == cudaSuccess && (nY == 0 || cudaMalloc(&c->Y, nY * 8) == cudaSuccess) &&
-            cudaMalloc(&c->khat, nK * 4) == cudaSuccess && cudaMalloc(&c->tw, kTwMax * 8) == cudaSuccess &&
-            cudaMalloc(&c->cav, sizeof(CavState)) == cudaSuccess &&
+  if (c->mode == 2) {
+    Nccl* n = nccl_api();
+    if (!n) {
+      c->err = "libnccl.so.2 not found";
+      return bail(MCQ_ENCCL);
+    }
+    ncclUniqueId id;
+    std::memcpy(id.internal, dist->nccl_id, 128);
+    if (n->commInitRank(&c->comm, world, id, c->rank) != ncclSuccess) return bail(MCQ_ENCCL);
+  }
+  // slabs
+  const int nzl = g.nz / world;
+  const int kxs = world == 1 ? g.P : ((g.NKX + world - 1) / world + 15) / 16 * 16;
+  const int first = c->mode == 2 ? c->rank : 0, count = c->mode == 1 ? world : 1;
+  c->sl.resize(count);
+  Dims probe = g;
+  probe.nz = nzl;
+  c->nparts = update_grid_blocks(probe) * world;
+  for (int i = 0; i < count; ++i) {
+    Slab& s = c->sl[i];
+    const int r = first + i;
+    s.d = g;
+    s.d.nz = nzl;
+    s.d.N = (long long)g.nx * g.ny * nzl;
+    s.d.zg0 = r * nzl;
+    s.d.zoff = world > 1 ? 1 : 0;
+    s.d.cs = (long long)g.nx * g.ny * (nzl + 2 * s.d.zoff);
+    s.d.NS = world;
+    s.d.KXS = kxs;
+    s.d.kx0 = r * kxs;
+    s.nparts = update_grid_blocks(s.d);
+    if (alloc_slab(c, s) != MCQ_OK) return bail(MCQ_ENOMEM);
+  }
+  bool ok = cudaMalloc(&c->khat, 6ULL * (g.Lz / 2 + 1) * (g.Ly / 2 + 1) * g.P * 4) == cudaSuccess &&
+            cudaMalloc(&c->tw, kTwMax * 8) == cudaSuccess && cudaMalloc(&c->cav, sizeof(CavState)) == cudaSuccess &&
             cudaMalloc(&c->partials, (size_t)c->nparts * 8) == cudaSuccess &&
             cudaMalloc(&c->maxbits, 4) == cudaSuccess && cudaMalloc(&c->bad, 4) == cudaSuccess &&
-            cudaMalloc(&c->io, N3 * 4) == cudaSuccess;
+            cudaMalloc(&c->io, 3ULL * c->cells_here() * 4) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
     return bail(MCQ_ENOMEM);
   }
-  // zero the spectra once (columns beyond NKX are never touched, keep them finite)
-  if (cudaMemsetAsync(c->X, 0, nX * 8, c->stream) != cudaSuccess ||
-      (nY && cudaMemsetAsync(c->Y, 0, nY * 8, c->stream) != cudaSuccess) ||
-      cudaMemsetAsync(c->khat, 0, nK * 4, c->stream) != cudaSuccess ||
-      cudaMemsetAsync(c->mN, 0, N3 * 4, c->stream) != cudaSuccess ||
-      cudaMemsetAsync(c->acc, 0, N3 * 4, c->stream) != cudaSuccess)
+  for (int i = 0; i < count; ++i) {
+    Slab& s = c->sl[i];
+    if (c->mode == 2) {
+      if (cudaMalloc(&s.partials, (size_t)s.nparts * 8) != cudaSuccess) return bail(MCQ_ENOMEM);
+    } else {
+      s.partials = c->partials + (size_t)i * s.nparts;  // global z order = slab order
+    }
+  }
+  if (cudaMemsetAsync(c->khat, 0, 6ULL * (g.Lz / 2 + 1) * (g.Ly / 2 + 1) * g.P * 4, c->stream) != cudaSuccess)
     return bail(MCQ_ECUDA);
   // twiddles w_1024^m = exp(-2 pi i m / 1024), generated in fp64
   {
@@ -505,41 +756,60 @@ int mcq_set_stream(mcq_ctx* c, void* stream) {
   return MCQ_OK;
 }
 
+// the cells of slab i inside the global host arrays (x fastest): offset and count
+static long long slab_cell0(const mcq_ctx* c, int i) { return (long long)c->sl[i].d.zg0 * c->dg.nx * c->dg.ny; }
+
 int mcq_set_geometry(mcq_ctx* c, const unsigned char* mask) {
   if (!c) return MCQ_EINVAL;
   if (!mask) {
-    if (c->mask) cudaFree(c->mask);
-    c->mask = nullptr;
+    for (auto& s : c->sl) {
+      if (s.mask) cudaFree(s.mask);
+      s.mask = nullptr;
+    }
+    c->have_mask = false;
     return MCQ_OK;
   }
-  if (!c->mask) CK(c, cudaMalloc(&c->mask, c->d.N));
-  CK(c, cudaMemcpyAsync(c->mask, mask, c->d.N, cudaMemcpyHostToDevice, c->stream));
+  for (int i = 0; i < (int)c->sl.size(); ++i) {
+    Slab& s = c->sl[i];
+    if (!s.mask) CK(c, cudaMalloc(&s.mask, s.d.N));
+    CK(c, cudaMemcpyAsync(s.mask, mask + slab_cell0(c, i), s.d.N, cudaMemcpyHostToDevice, c->stream));
+  }
   CK(c, cudaStreamSynchronize(c->stream));
+  c->have_mask = true;
   if (c->m_set) {  // zero m in vacuum now
-    const long long N = c->d.N;
-    launch_soa_to_aos(c->mN, c->io, N, c->stream);
-    CK(c, cudaMemsetAsync(c->bad, 0, 4, c->stream));
-    launch_aos_to_soa(c->io, c->mN, c->mask, N, c->bad, c->stream);
+    for (int i = 0; i < (int)c->sl.size(); ++i) {
+      Slab& s = c->sl[i];
+      const long long off = (long long)s.d.zoff * s.d.nx * s.d.ny;
+      float* io = c->io + 3 * i * s.d.N;
+      launch_soa_to_aos(s.mN, io, s.d.N, s.d.cs, off, c->stream);
+      CK(c, cudaMemsetAsync(c->bad, 0, 4, c->stream));
+      launch_aos_to_soa(io, s.mN, s.mask, s.d.N, s.d.cs, off, c->bad, c->stream);
+      c->launches += 2;
+    }
     Enq q{c, c->stream};
     q.x0();
-    c->launches += q.count + 2;
+    c->launches += q.count;
     CK(c, cudaStreamSynchronize(c->stream));
   }
   return MCQ_OK;
 }
 
-static int set_m_common(mcq_ctx* c, const float* src_dev) {
-  const long long N = c->d.N;
+// io holds the AoS cells of this context (all slabs in order); convert, validate, commit
+static int set_m_from_io(mcq_ctx* c) {
   CK(c, cudaMemsetAsync(c->bad, 0, 4, c->stream));
-  launch_aos_to_soa(src_dev, c->mA, c->mask, N, c->bad, c->stream);
+  for (int i = 0; i < (int)c->sl.size(); ++i) {
+    Slab& s = c->sl[i];
+    const long long off = (long long)s.d.zoff * s.d.nx * s.d.ny;
+    launch_aos_to_soa(c->io + 3 * i * s.d.N, s.mA, s.mask, s.d.N, s.d.cs, off, c->bad, c->stream);
+  }
   int bad = 0;
   CK(c, cudaMemcpyAsync(&bad, c->bad, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
   if (bad) return fail(c, MCQ_EINVAL, std::to_string(bad) + " magnetic cells with a zero or non-finite vector");
-  CK(c, cudaMemcpyAsync(c->mN, c->mA, 3ULL * N * 4, cudaMemcpyDeviceToDevice, c->stream));
+  for (auto& s : c->sl) CK(c, cudaMemcpyAsync(s.mN, s.mA, 3ULL * s.d.cs * 4, cudaMemcpyDeviceToDevice, c->stream));
   Enq q{c, c->stream};
   q.x0();
-  c->launches += q.count + 1;
+  c->launches += q.count + (long long)c->sl.size();
   CK(c, cudaGetLastError());
   c->m_set = true;
   return MCQ_OK;
@@ -547,13 +817,16 @@ static int set_m_common(mcq_ctx* c, const float* src_dev) {
 
 int mcq_set_m(mcq_ctx* c, const float* m) {
   if (!c || !m) return MCQ_EINVAL;
-  CK(c, cudaMemcpyAsync(c->io, m, 3ULL * c->d.N * 4, cudaMemcpyHostToDevice, c->stream));
-  return set_m_common(c, c->io);
+  CK(c, cudaMemcpyAsync(c->io, m + 3 * c->first_cell(), 3ULL * c->cells_here() * 4, cudaMemcpyHostToDevice,
+                        c->stream));
+  return set_m_from_io(c);
 }
 
 int mcq_set_m_device(mcq_ctx* c, const float* d_m) {
   if (!c || !d_m) return MCQ_EINVAL;
-  return set_m_common(c, d_m);
+  CK(c, cudaMemcpyAsync(c->io, d_m + 3 * c->first_cell(), 3ULL * c->cells_here() * 4, cudaMemcpyDeviceToDevice,
+                        c->stream));
+  return set_m_from_io(c);
 }
 
 int mcq_set_bext(mcq_ctx* c, const double B[3]) {
@@ -567,25 +840,37 @@ int mcq_set_bext(mcq_ctx* c, const double B[3]) {
 
 int mcq_set_brms(mcq_ctx* c, const float* map, const double uniform[3]) {
   if (!c || (!map && !uniform)) return MCQ_EINVAL;
-  const long long N = c->d.N;
+  const long long Nall = c->dg.N;
   if (map) {
     bool nz = false;
-    for (long long i = 0; i < 3 * N; ++i) {
+    for (long long i = 0; i < 3 * Nall; ++i) {  // the enable flag is a property of the whole map
       if (!std::isfinite(map[i])) return fail(c, MCQ_EINVAL, "B_rms map not finite");
       nz = nz || map[i] != 0.f;
     }
-    if (!c->brms) CK(c, cudaMalloc(&c->brms, 3ULL * N * 4));
-    CK(c, cudaMemcpyAsync(c->io, map, 3ULL * N * 4, cudaMemcpyHostToDevice, c->stream));
-    launch_deinterleave(c->io, c->brms, N, c->stream);  // AoS -> SoA, no normalisation
-    c->launches += 1;
+    CK(c, cudaMemcpyAsync(c->io, map + 3 * c->first_cell(), 3ULL * c->cells_here() * 4, cudaMemcpyHostToDevice,
+                          c->stream));
+    for (int i = 0; i < (int)c->sl.size(); ++i) {
+      Slab& s = c->sl[i];
+      if (!s.brms) {
+        CK(c, cudaMalloc(&s.brms, 3ULL * s.d.cs * 4));
+        CK(c, cudaMemsetAsync(s.brms, 0, 3ULL * s.d.cs * 4, c->stream));
+      }
+      launch_deinterleave(c->io + 3 * i * s.d.N, s.brms, s.d.N, s.d.cs, (long long)s.d.zoff * s.d.nx * s.d.ny,
+                          c->stream);
+      c->launches += 1;
+    }
     CK(c, cudaStreamSynchronize(c->stream));
     c->brms_u[0] = c->brms_u[1] = c->brms_u[2] = 0.0;
+    c->brms_map = true;
     c->cav_on = nz;
   } else {
     for (int i = 0; i < 3; ++i)
       if (!std::isfinite(uniform[i])) return fail(c, MCQ_EINVAL, "B_rms not finite");
-    if (c->brms) cudaFree(c->brms);
-    c->brms = nullptr;
+    for (auto& s : c->sl) {
+      if (s.brms) cudaFree(s.brms);
+      s.brms = nullptr;
+    }
+    c->brms_map = false;
     for (int i = 0; i < 3; ++i) c->brms_u[i] = uniform[i];
     c->cav_on = uniform[0] != 0 || uniform[1] != 0 || uniform[2] != 0;
   }
@@ -655,7 +940,10 @@ int mcq_relax(mcq_ctx* c, double dt, double tol, long long max_steps, long long*
     CK(c, cudaMemsetAsync(c->maxbits, 0, 4, c->stream));
     Enq q{c, c->stream};
     q.eval(MODE_MAXTORQUE, MCQ_TERM_ALL & ~(MCQ_TERM_CAVITY | MCQ_TERM_EXCITATION));
+    if (q.rc != MCQ_OK) return q.rc;
     c->launches += q.count;
+    if (c->mode == 2)  // max over ranks (non-negative floats: the float order is the bit order)
+      NK(c, nccl_api()->allReduce(c->maxbits, c->maxbits, 1, ncclFloat, ncclMax, c->comm, c->stream));
     unsigned bits = 0;
     CK(c, cudaMemcpyAsync(&bits, c->maxbits, 4, cudaMemcpyDeviceToHost, c->stream));
     CK(c, cudaStreamSynchronize(c->stream));
@@ -674,19 +962,30 @@ int mcq_synchronize(mcq_ctx* c) {
   return MCQ_OK;
 }
 
+// SoA slab contents -> io (AoS, slab order)
+static void slabs_to_io(mcq_ctx* c, bool field) {
+  for (int i = 0; i < (int)c->sl.size(); ++i) {
+    Slab& s = c->sl[i];
+    launch_soa_to_aos(field ? s.field : s.mN, c->io + 3 * i * s.d.N, s.d.N, s.d.cs,
+                      (long long)s.d.zoff * s.d.nx * s.d.ny, c->stream);
+  }
+  c->launches += (long long)c->sl.size();
+}
+
 int mcq_get_m(mcq_ctx* c, float* m_out) {
   if (!c || !m_out) return MCQ_EINVAL;
-  launch_soa_to_aos(c->mN, c->io, c->d.N, c->stream);
-  c->launches += 1;
-  CK(c, cudaMemcpyAsync(m_out, c->io, 3ULL * c->d.N * 4, cudaMemcpyDeviceToHost, c->stream));
+  slabs_to_io(c, false);
+  CK(c, cudaMemcpyAsync(m_out + 3 * c->first_cell(), c->io, 3ULL * c->cells_here() * 4, cudaMemcpyDeviceToHost,
+                        c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
   return MCQ_OK;
 }
 
 int mcq_get_m_device(mcq_ctx* c, float* d_out) {
   if (!c || !d_out) return MCQ_EINVAL;
-  launch_soa_to_aos(c->mN, d_out, c->d.N, c->stream);
-  c->launches += 1;
+  slabs_to_io(c, false);
+  CK(c, cudaMemcpyAsync(d_out + 3 * c->first_cell(), c->io, 3ULL * c->cells_here() * 4, cudaMemcpyDeviceToDevice,
+                        c->stream));
   CK(c, cudaGetLastError());
   return MCQ_OK;
 }
@@ -694,15 +993,21 @@ int mcq_get_m_device(mcq_ctx* c, float* d_out) {
 int mcq_get_field(mcq_ctx* c, float* b_out, unsigned terms) {
   if (!c || !b_out) return MCQ_EINVAL;
   if (!c->m_set) return fail(c, MCQ_ESTATE, "mcq_get_field before mcq_set_m");
-  const long long N = c->d.N;
-  if (!c->fieldbuf) CK(c, cudaMalloc(&c->fieldbuf, 3ULL * N * 4));
+  for (auto& s : c->sl) {
+    if (!s.field) {
+      CK(c, cudaMalloc(&s.field, 3ULL * s.d.cs * 4));
+      CK(c, cudaMemsetAsync(s.field, 0, 3ULL * s.d.cs * 4, c->stream));
+    }
+  }
   const CavParams p = cav_params(c, 1e-12);
   launch_cav_prepare(p, c->cav, c->stream);
   Enq q{c, c->stream};
   q.eval(MODE_FIELD, terms & MCQ_TERM_ALL);
-  launch_soa_to_aos(c->fieldbuf, c->io, N, c->stream);
-  c->launches += q.count + 2;
-  CK(c, cudaMemcpyAsync(b_out, c->io, 3ULL * N * 4, cudaMemcpyDeviceToHost, c->stream));
+  if (q.rc != MCQ_OK) return q.rc;
+  c->launches += q.count + 1;
+  slabs_to_io(c, true);
+  CK(c, cudaMemcpyAsync(b_out + 3 * c->first_cell(), c->io, 3ULL * c->cells_here() * 4, cudaMemcpyDeviceToHost,
+                        c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
   return MCQ_OK;
 }
@@ -773,6 +1078,7 @@ int mcq_profile_run(mcq_ctx* c, double dt, long long steps, double* kernel_ms, i
   Prof pr{c->stream};
   Enq q{c, c->stream, prof_hook, &pr};
   for (long long i = 0; i < steps; ++i) q.llg_step(dt);
+  if (q.rc != MCQ_OK) return q.rc;
   c->launches += q.count + 1;
   CK(c, cudaStreamSynchronize(c->stream));
   double tot[MCQ_NKCLASS] = {0};
@@ -795,11 +1101,11 @@ int mcq_profile_run(mcq_ctx* c, double dt, long long steps, double* kernel_ms, i
 
 int mcq_debug_layout(const mcq_ctx* c, long long out[6]) {
   if (!c || !out) return MCQ_EINVAL;
-  out[0] = c->d.Lx;
-  out[1] = c->d.Ly;
-  out[2] = c->d.Lz;
-  out[3] = c->d.NKX;
-  out[4] = c->d.P;
+  out[0] = c->dg.Lx;
+  out[1] = c->dg.Ly;
+  out[2] = c->dg.Lz;
+  out[3] = c->dg.NKX;
+  out[4] = c->dg.P;
   out[5] = c->nparts;
   return MCQ_OK;
 }
@@ -811,7 +1117,7 @@ int mcq_debug_tensor_octant(mcq_ctx* c, double* out) {
 
 int mcq_debug_khat(mcq_ctx* c, float* out) {
   if (!c || !out) return MCQ_EINVAL;
-  const size_t nK = 6ULL * (c->d.Lz / 2 + 1) * (c->d.Ly / 2 + 1) * c->d.P;
+  const size_t nK = 6ULL * (c->dg.Lz / 2 + 1) * (c->dg.Ly / 2 + 1) * c->dg.P;
   CK(c, cudaMemcpyAsync(out, c->khat, nK * 4, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
   return MCQ_OK;

@@ -72,22 +72,28 @@ __global__ void __launch_bounds__(PassCfg<L>::NT) k_ypass(const float2* __restri
   const int kx = blockIdx.x * C + c, z = blockIdx.y, comp = blockIdx.z;
   const bool ok = kx < d.NKX;
   const int nin = INV ? L : d.ny, nout = INV ? d.ny : L;
-  const size_t plane_in = (size_t)(comp * d.nz + z) * (INV ? L : d.ny);
-  const size_t plane_out = (size_t)(comp * d.nz + z) * (INV ? d.ny : L);
-  const float2* src = in + plane_in * d.P + kx;
+  // X side: X[c][z][y][P]; Y side: kx-slab-major Y[q][c][z][ky][KXS] (common.cuh)
+  const int q = kx / d.KXS, kxl = kx - q * d.KXS;
+  const size_t xoff = ((size_t)(comp * d.nz + z) * d.ny) * d.P + kx;
+  const size_t yoff = ((size_t)(q * 3 + comp) * d.nz + z) * (size_t)L * d.KXS + kxl;
+  const float2* src = in + (INV ? yoff : xoff);
+  const size_t sin_ = INV ? d.KXS : d.P, sout = INV ? d.P : d.KXS;
   float2 v[1][E];
 #pragma unroll
   for (int i = 0; i < E; ++i) {
     const int p = t + TL * i;
-    v[0][i] = (ok && p < nin) ? src[(size_t)p * d.P] : make_float2(0.f, 0.f);
+    // zero padding: forward input rows >= ny <= Ly/2 are zero, i.e. every i >= E/2 (p >= L/2)
+    // statically, so the first stage's butterflies fold those operands away
+    v[0][i] = (!INV && 2 * i >= E) ? make_float2(0.f, 0.f)
+                                  : ((ok && p < nin) ? src[(size_t)p * sin_] : make_float2(0.f, 0.f));
   }
   reg_fft<L, E, 1, INV>(v, sm + L, ColAddr<L, C>{c}, tw, t);
   if (ok) {
-    float2* dst = out + plane_out * d.P + kx;
+    float2* dst = out + (INV ? xoff : yoff);
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       const int p = t + TL * i;
-      if (p < nout) dst[(size_t)p * d.P] = v[0][i];
+      if ((!INV || 2 * i < E) && p < nout) dst[(size_t)p * sout] = v[0][i];  // inverse: rows < ny only
     }
   }
 }
@@ -140,7 +146,7 @@ __global__ void __launch_bounds__(ZCfg<L>::NT) k_conv(float2* __restrict__ Y, co
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       const int p = t + TL * i;
-      v[g][i] = (ok && p < nin) ? base[g * cstr + p * lstride] : make_float2(0.f, 0.f);
+      v[g][i] = (2 * i < E && ok && p < nin) ? base[g * cstr + p * lstride] : make_float2(0.f, 0.f);
     }
   const ColAddr<L, C> A{c};
   reg_fft<L, E, 3, false>(v, sm + L, A, tw, t);
@@ -159,7 +165,7 @@ __global__ void __launch_bounds__(ZCfg<L>::NT) k_conv(float2* __restrict__ Y, co
 #pragma unroll
       for (int i = 0; i < E; ++i) {
         const int p = t + TL * i;
-        if (p < nin) base[g * cstr + p * lstride] = v[g][i];
+        if (2 * i < E && p < nin) base[g * cstr + p * lstride] = v[g][i];
       }
   }
 }
@@ -183,7 +189,7 @@ struct ZSCfg {
   static constexpr size_t SMEM = (size_t)(L + 3 * L * C) * sizeof(float2);
 };
 
-template <int L>
+template <int L, bool SPLIT>
 __global__ void __launch_bounds__(ZSCfg<L>::NT) k_zconv_seq(float2* __restrict__ Y, const float* __restrict__ khat,
                                                             Dims d, const float2* __restrict__ gtw) {
   using Cf = ZSCfg<L>;
@@ -193,11 +199,24 @@ __global__ void __launch_bounds__(ZSCfg<L>::NT) k_zconv_seq(float2* __restrict__
   float2* xch = sm + L;  // [3][L][C]
   load_tw<L>(tw, gtw);
   const int c = threadIdx.x % C, t = threadIdx.x / C;
-  const int kx = blockIdx.x * C + c, ky = blockIdx.y;
-  const bool ok = kx < d.NKX;
-  const int nz = d.nz;
-  const size_t plane = (size_t)d.Ly * d.P, cstr = (size_t)nz * plane;
-  float2* base = Y + (size_t)ky * d.P + kx;
+  // columns kxl of this rank's kx slab (global kx = kx0 + kxl); z runs over all nzg planes,
+  // held as [source rank r][c][zl][ky][KXS] with z = r * nz + zl (NS == 1: Y[c][z][ky][P])
+  const int kxl = blockIdx.x * C + c, ky = blockIdx.y, kx = d.kx0 + kxl;
+  const bool ok = kxl < d.KXS && kx < d.NKX;
+  const int nz = d.nzg, nzl = d.nz;
+  const size_t row = d.KXS, plane = (size_t)d.Ly * row;
+  float2* base = Y + (size_t)ky * row + kxl;
+  // ((r * 3 + g) * nzl + z - r * nzl) planes = g * nzl + z + 2 nzl r with r = z / nzl (SPLIT
+  // only: the single-slab instance keeps the plain strength-reduced addressing)
+  const size_t cstr = (size_t)nzl * plane;
+  // z / nzl in fp32: (z + 1/2) / nzl is >= 1/(2 nzl) >= 1e-3 away from an integer and the
+  // rounding error is ~1e-7 relative, so the truncation is exact (z < 1024)
+  const float inv_nzl = 1.f / (float)nzl;
+  auto zaddr = [&](int g, int z) -> size_t {
+    size_t a = (size_t)g * cstr + (size_t)z * plane;
+    if constexpr (SPLIT) a += (size_t)(2 * nzl * __float2int_rz(((float)z + 0.5f) * inv_nzl)) * plane;
+    return a;
+  };
   struct GA {
     int g, c;
     __device__ __forceinline__ int operator()(int, int pos) const { return (g * L + pos) * C + c; }
@@ -208,7 +227,7 @@ __global__ void __launch_bounds__(ZSCfg<L>::NT) k_zconv_seq(float2* __restrict__
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       const int p = t + TL * i;
-      v[0][i] = (ok && p < nz) ? base[g * cstr + p * plane] : make_float2(0.f, 0.f);
+      v[0][i] = (2 * i < E && ok && p < nz) ? base[zaddr(g, p)] : make_float2(0.f, 0.f);  // nz <= L/2
     }
     const GA A{g, c};
     reg_fft<L, E, 1, false>(v, xch, A, tw, t);
@@ -238,7 +257,7 @@ __global__ void __launch_bounds__(ZSCfg<L>::NT) k_zconv_seq(float2* __restrict__
 #pragma unroll
       for (int i = 0; i < E; ++i) {
         const int p = t + TL * i;
-        if (p < nz) base[g * cstr + p * plane] = v[0][i];
+        if (2 * i < E && p < nz) base[zaddr(g, p)] = v[0][i];
       }
     }
   }
@@ -309,7 +328,7 @@ __global__ void __launch_bounds__(ZTCfg<L>::NT, MINB) k_zconv_tma(const __grid_c
 #pragma unroll
       for (int i = 0; i < E; ++i) {
         const int p = t + TL * i;
-        v[g][i] = p < nz ? in[g * Cf::GS + p * C + c] : make_float2(0.f, 0.f);
+        v[g][i] = (2 * i < E && p < nz) ? in[g * Cf::GS + p * C + c] : make_float2(0.f, 0.f);
       }
     reg_fft<L, E, 3, false>(v, xch, A, tw, t);
     const bool ok = kx < d.NKX;
@@ -328,7 +347,7 @@ __global__ void __launch_bounds__(ZTCfg<L>::NT, MINB) k_zconv_tma(const __grid_c
 #pragma unroll
         for (int i = 0; i < E; ++i) {
           const int p = t + TL * i;
-          if (p < nz) base[g * cstr + p * plane] = v[g][i];
+          if (2 * i < E && p < nz) base[g * cstr + p * plane] = v[g][i];
         }
     }
     __syncthreads();  // stage b and xch are free for the next issue / tile
@@ -378,8 +397,13 @@ void launch_zconv(const Dims& d, float2* Y, const float* khat, const float2* tw,
 void launch_zconv_seq(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t st) {
   MCQ_DISPATCH_L(d.Lz, {
     using Cf = ZSCfg<L>;
-    dim3 grid((d.NKX + Cf::C - 1) / Cf::C, d.Ly);
-    k_zconv_seq<L><<<grid, Cf::NT, Cf::SMEM, st>>>(Y, khat, d, tw);
+    const int cols = d.NKX - d.kx0 < d.KXS ? d.NKX - d.kx0 : d.KXS;  // valid columns of this slab
+    if (cols <= 0) return;
+    dim3 grid((cols + Cf::C - 1) / Cf::C, d.Ly);
+    if (d.NS > 1)
+      k_zconv_seq<L, true><<<grid, Cf::NT, Cf::SMEM, st>>>(Y, khat, d, tw);
+    else
+      k_zconv_seq<L, false><<<grid, Cf::NT, Cf::SMEM, st>>>(Y, khat, d, tw);
   })
 }
 
@@ -433,7 +457,8 @@ void configure_pass_kernels() {
       cudaFuncSetAttribute(k_conv<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZCfg<L>::SMEM);
       cudaFuncSetAttribute(k_conv<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZCfg<L>::SMEM);
       cudaFuncSetAttribute(k_zconv_tma<L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZTCfg<L>::SMEM);
-      cudaFuncSetAttribute(k_zconv_seq<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZSCfg<L>::SMEM);
+      cudaFuncSetAttribute(k_zconv_seq<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZSCfg<L>::SMEM);
+      cudaFuncSetAttribute(k_zconv_seq<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZSCfg<L>::SMEM);
       cudaFuncSetAttribute(k_zconv_tma<L, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZTCfg<L>::SMEM);
     })
   }

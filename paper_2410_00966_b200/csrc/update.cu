@@ -186,8 +186,10 @@ __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const flo
 
   const Dims& d = a.d;
   const int nx = d.nx, ny = d.ny, nz = d.nz;
-  const long long N = d.N;
-  const int y0 = blockIdx.x * RY, z = blockIdx.y;
+  const long long N = d.cs;                        // component stride of the state arrays
+  const int y0 = blockIdx.x * RY, z = blockIdx.y;  // z: local plane (X rows, partials)
+  const int zs = z + d.zoff;                       // storage plane of the (halo'd) state arrays
+  const bool zlo = d.zg0 + z > 0, zhi = d.zg0 + z < d.nzg - 1;  // global z neighbours exist
   const int nrow = min(RY, ny - y0);
   const int ylo = y0 > 0 ? y0 - 1 : 0, yhi = min(y0 + RY, ny - 1);  // staged m_s rows at z
   const int nxp = nx + (nx & 1);                                     // tile row pitch (8-byte pairs)
@@ -212,12 +214,12 @@ __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const flo
           tma_load_1d(xs + (c * RY + r) * PITCH, a.X + ((size_t)(c * nz + z) * ny + y0 + r) * d.P, bx, &bars[0]);
     }
     const uint32_t bc = (uint32_t)(yhi - ylo + 1) * nx * 4, bz = (uint32_t)nrow * nx * 4;
-    mbar_arrive_expect_tx(&bars[1], 3 * (bc + (z > 0 ? bz : 0) + (z < nz - 1 ? bz : 0)));
+    mbar_arrive_expect_tx(&bars[1], 3 * (bc + (zlo ? bz : 0) + (zhi ? bz : 0)));
     for (int c = 0; c < 3; ++c) {
       const float* src = a.mS + c * N;
-      tma_load_1d(tc + c * csc + (ylo - (y0 - 1)) * nx, src + ((long long)z * ny + ylo) * nx, bc, &bars[1]);
-      if (z > 0) tma_load_1d(tzm + c * csz, src + ((long long)(z - 1) * ny + y0) * nx, bz, &bars[1]);
-      if (z < nz - 1) tma_load_1d(tzp + c * csz, src + ((long long)(z + 1) * ny + y0) * nx, bz, &bars[1]);
+      tma_load_1d(tc + c * csc + (ylo - (y0 - 1)) * nx, src + ((long long)zs * ny + ylo) * nx, bc, &bars[1]);
+      if (zlo) tma_load_1d(tzm + c * csz, src + ((long long)(zs - 1) * ny + y0) * nx, bz, &bars[1]);
+      if (zhi) tma_load_1d(tzp + c * csz, src + ((long long)(zs + 1) * ny + y0) * nx, bz, &bars[1]);
     }
   }
   if (!tma) {  // fallback (unaligned rows): cooperative coalesced loads into the same layout
@@ -230,12 +232,12 @@ __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const flo
       const float* src = a.mS + c * N;
       for (int e = threadIdx.x; e < (yhi - ylo + 1) * nx; e += NT) {
         const int r = e / nx, x = e - r * nx;
-        tc[c * csc + (ylo - (y0 - 1) + r) * nxp + x] = src[((long long)z * ny + ylo) * nx + e];
+        tc[c * csc + (ylo - (y0 - 1) + r) * nxp + x] = src[((long long)zs * ny + ylo) * nx + e];
       }
       for (int e = threadIdx.x; e < nrow * nx; e += NT) {
         const int r = e / nx, x = e - r * nx;
-        if (z > 0) tzm[c * csz + r * nxp + x] = src[((long long)(z - 1) * ny + y0) * nx + e];
-        if (z < nz - 1) tzp[c * csz + r * nxp + x] = src[((long long)(z + 1) * ny + y0) * nx + e];
+        if (zlo) tzm[c * csz + r * nxp + x] = src[((long long)(zs - 1) * ny + y0) * nx + e];
+        if (zhi) tzp[c * csz + r * nxp + x] = src[((long long)(zs + 1) * ny + y0) * nx + e];
       }
     }
     __syncthreads();
@@ -285,7 +287,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const flo
   const float gsum = gc + ge;
   double wacc = 0.0;
   float tmax = 0.f;
-  const long long rowbase = (long long)nx * (y + (long long)ny * z);
+  const long long rowbase = (long long)nx * (y + (long long)ny * zs);
   const float* trow = tc + (yl + 1) * nxp;  // this row inside the z tile
   const bool vec = (nx & 1) == 0;           // global pairs are 8-byte aligned
   const bool st = a.mode == MODE_LLG || a.mode == MODE_RELAX;
@@ -294,6 +296,11 @@ __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const flo
 #pragma unroll
   for (int i = 0; i < E; ++i) {
     const int x0 = 2 * (t + TL * i);
+    if (2 * i >= E) {  // x0 >= N2 >= nx: zero padding, statically (prunes the C2R's last stage
+#pragma unroll       // outputs and the R2C's first-stage inputs)
+      for (int c = 0; c < 3; ++c) v[c][i] = make_float2(0.f, 0.f);
+      continue;
+    }
     float2 o[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
     if (rowok && x0 < nx) {
       const bool two = x0 + 1 < nx;
@@ -307,8 +314,8 @@ __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const flo
         mc[c] = sm_pair(r + x0);
         ym[c] = y > 0 ? sm_pair(r - nxp + x0) : mc[c];
         yp[c] = y < ny - 1 ? sm_pair(r + nxp + x0) : mc[c];
-        zm[c] = z > 0 ? sm_pair(tzm + c * csz + yl * nxp + x0) : mc[c];
-        zp[c] = z < nz - 1 ? sm_pair(tzp + c * csz + yl * nxp + x0) : mc[c];
+        zm[c] = zlo ? sm_pair(tzm + c * csz + yl * nxp + x0) : mc[c];
+        zp[c] = zhi ? sm_pair(tzp + c * csz + yl * nxp + x0) : mc[c];
         xl[c] = x0 > 0 ? r[x0 - 1] : 0.f;
         xr[c] = x0 + 2 < nx ? r[x0 + 2] : 0.f;
         mn2[c] = need_mn ? ld_pair(a.mN + c * N, idx, vec, two) : make_float2(0.f, 0.f);
@@ -323,7 +330,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const flo
         const int x = x0 + h;
 #define MCQ_PICK(p) (h ? (p).y : (p).x)
         const float3 m = make_float3(MCQ_PICK(mc[0]), MCQ_PICK(mc[1]), MCQ_PICK(mc[2]));
-        const bool ok[6] = {x > 0, x < nx - 1, y > 0, y < ny - 1, z > 0, z < nz - 1};
+        const bool ok[6] = {x > 0, x < nx - 1, y > 0, y < ny - 1, zlo, zhi};
         float3 nb[6];
         nb[0] = h ? make_float3(mc[0].x, mc[1].x, mc[2].x) : make_float3(xl[0], xl[1], xl[2]);
         nb[1] = h ? make_float3(xr[0], xr[1], xr[2]) : make_float3(mc[0].y, mc[1].y, mc[2].y);
@@ -523,10 +530,12 @@ void launch_cav_prepare(const CavParams& p, CavState* st, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------- K-IO
-// interleaved (AoS) -> SoA, normalise, apply the geometry mask; *bad counts magnetic cells
-// with a zero vector (EINVAL).
+// AoS (interleaved, x fastest) <-> SoA state layout.  `N` cells; the SoA side has component
+// stride `cs` and starts `off` cells into each component (halo planes of a z slab).
+// aos_to_soa normalises, applies the geometry mask and counts magnetic cells with a zero
+// vector in *bad (EINVAL).
 __global__ void k_aos_to_soa(const float* __restrict__ in, float* __restrict__ out, const uint8_t* __restrict__ mask,
-                             long long N, int* bad) {
+                             long long N, long long cs, long long off, int* bad) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
     float3 v = make_float3(in[3 * i], in[3 * i + 1], in[3 * i + 2]);
     const bool mag = mask ? (mask[i] != 0) : true;
@@ -542,25 +551,27 @@ __global__ void k_aos_to_soa(const float* __restrict__ in, float* __restrict__ o
         v = make_float3(v.x * r, v.y * r, v.z * r);
       }
     }
-    out[i] = v.x;
-    out[N + i] = v.y;
-    out[2 * N + i] = v.z;
+    out[off + i] = v.x;
+    out[cs + off + i] = v.y;
+    out[2 * cs + off + i] = v.z;
   }
 }
 
-__global__ void k_soa_to_aos(const float* __restrict__ in, float* __restrict__ out, long long N) {
+__global__ void k_soa_to_aos(const float* __restrict__ in, float* __restrict__ out, long long N, long long cs,
+                             long long off) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
-    out[3 * i] = in[i];
-    out[3 * i + 1] = in[N + i];
-    out[3 * i + 2] = in[2 * N + i];
+    out[3 * i] = in[off + i];
+    out[3 * i + 1] = in[cs + off + i];
+    out[3 * i + 2] = in[2 * cs + off + i];
   }
 }
 
-__global__ void k_deinterleave(const float* __restrict__ in, float* __restrict__ out, long long N) {
+__global__ void k_deinterleave(const float* __restrict__ in, float* __restrict__ out, long long N, long long cs,
+                               long long off) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
-    out[i] = in[3 * i];
-    out[N + i] = in[3 * i + 1];
-    out[2 * N + i] = in[3 * i + 2];
+    out[off + i] = in[3 * i];
+    out[cs + off + i] = in[3 * i + 1];
+    out[2 * cs + off + i] = in[3 * i + 2];
   }
 }
 
@@ -569,16 +580,17 @@ static int io_blocks(long long N) {
   return (int)(b < 148 * 16 ? (b < 1 ? 1 : b) : 148 * 16);
 }
 
-void launch_aos_to_soa(const float* in, float* out, const uint8_t* mask, long long N, int* bad, cudaStream_t s) {
-  k_aos_to_soa<<<io_blocks(N), 256, 0, s>>>(in, out, mask, N, bad);
+void launch_aos_to_soa(const float* in, float* out, const uint8_t* mask, long long N, long long cs, long long off,
+                       int* bad, cudaStream_t s) {
+  k_aos_to_soa<<<io_blocks(N), 256, 0, s>>>(in, out, mask, N, cs, off, bad);
 }
 
-void launch_soa_to_aos(const float* in, float* out, long long N, cudaStream_t s) {
-  k_soa_to_aos<<<io_blocks(N), 256, 0, s>>>(in, out, N);
+void launch_soa_to_aos(const float* in, float* out, long long N, long long cs, long long off, cudaStream_t s) {
+  k_soa_to_aos<<<io_blocks(N), 256, 0, s>>>(in, out, N, cs, off);
 }
 
-void launch_deinterleave(const float* in, float* out, long long N, cudaStream_t s) {
-  k_deinterleave<<<io_blocks(N), 256, 0, s>>>(in, out, N);
+void launch_deinterleave(const float* in, float* out, long long N, long long cs, long long off, cudaStream_t s) {
+  k_deinterleave<<<io_blocks(N), 256, 0, s>>>(in, out, N, cs, off);
 }
 
 }  // namespace mcq
