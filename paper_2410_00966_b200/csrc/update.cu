@@ -171,7 +171,10 @@ __device__ __forceinline__ void st_pair(float* __restrict__ p, long long i, floa
 __device__ __forceinline__ float2 sm_pair(const float* p) { return *reinterpret_cast<const float2*>(p); }
 
 template <int N2>
-__global__ void __launch_bounds__(UCfg<N2>::NT) k_update(UpdateArgs a, const float2* __restrict__ gtw) {
+#ifndef MCQ_UMINB
+#define MCQ_UMINB 5  // min resident CTAs per SM requested from ptxas (96-register cap: 84.8 vs 86.8 us on configs[1])
+#endif
+__global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a, const float2* __restrict__ gtw) {
   using Cf = UCfg<N2>;
   constexpr int E = Cf::E, TL = Cf::TL, RY = Cf::RY, NT = Cf::NT, LX = 2 * N2, PITCH = Cf::PITCH;
   extern __shared__ __align__(16) float2 sm[];

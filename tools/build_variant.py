@@ -16,5 +16,5 @@ for src in b.SOURCES:
     procs.append(subprocess.Popen(["/usr/local/cuda/bin/nvcc", *b.FLAGS, *defs, "-c", os.path.join(b.CSRC, src), "-o", obj]))
     objs.append(obj)
 assert all(p.wait() == 0 for p in procs)
-subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", out, *objs, "-lcudart"])
+subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", out, *objs, "-lcudart", "-ldl"])
 print(out)
