@@ -194,7 +194,7 @@ MCQ_API int mcq_debug_layout(const mcq_ctx *, long long out[6]);
 /* Real-space demag tensor octant, fp64 (6, Lz/2+1, Ly/2+1, Lx/2+1) in XX,YY,ZZ,XY,XZ,YZ
  * order, for index offsets (i, j, k); zero where i >= nx, j >= ny or k >= nz. */
 MCQ_API int mcq_debug_tensor_octant(mcq_ctx *, double *out);
-/* Folded kernel spectrum, fp32 (6, Lz/2+1, Ly/2+1, P), kx fastest:
+/* Folded kernel spectrum, fp32 (Lz/2+1, Ly/2+1, P, 6), the 6 components (XX,YY,ZZ,XY,XZ,YZ) fastest:
  * Khat = -mu0 Ms/(Lx Ly Lz) DFT(N) (real: every component is even or odd along each axis). */
 MCQ_API int mcq_debug_khat(mcq_ctx *, float *out);
 

@@ -199,10 +199,10 @@ def mcq_debug_tensor_octant(ctx):
 
 def mcq_debug_khat(ctx):
     L = mcq_debug_layout(ctx)
-    shape = (6, L["Lz"] // 2 + 1, L["Ly"] // 2 + 1, L["P"])
+    shape = (L["Lz"] // 2 + 1, L["Ly"] // 2 + 1, L["P"], 6)
     out = np.empty(shape, np.float32)
     _check(ctx, lib.mcq_debug_khat(ctx, out.ctypes.data))
-    return out[..., :L["NKX"]]
+    return np.moveaxis(out, 3, 0)[..., :L["NKX"]]      # (6, kz, ky, kx) view
 
 
 def mcq_last_error(ctx):

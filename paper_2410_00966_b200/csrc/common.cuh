@@ -13,7 +13,8 @@ constexpr int kTwMax = 1024;                     // global twiddle table length 
 // Sizes of one context's padded spectral layout.  Row layout, kx fastest:
 //   X[c][z][y][P]    complex64 (x-spectrum of m; the demag spectrum in place), rows 16-byte aligned
 //   Y[c][z][ky][P]   complex64 (after the y transform; only the nz real z planes)
-//   Khat[g][kz][ky][P] fp32, kz <= Lz/2, ky <= Ly/2 (real, folded; g = XX,YY,ZZ,XY,XZ,YZ)
+//   Khat[kz][ky][P][g] fp32, kz <= Lz/2, ky <= Ly/2 (real, folded; g = XX,YY,ZZ,XY,XZ,YZ
+//                       interleaved: one multiply reads 24 contiguous bytes, three 8-byte loads)
 //
 // z-slab decomposition over NS ranks: nz below is the rank's number of planes,
 // nzg the global one, zg0 the global index of local plane 0.  State arrays carry zoff (0 or 1)

@@ -46,9 +46,17 @@ struct ZCfg {  // three-component passes with the Khat multiply (K-Z, K-Y2D)
   static constexpr size_t SMEM = (size_t)(L + (TL > 1 ? 3 * L * C : 0)) * sizeof(float2);
 };
 
-template <int L>
+template <int L, int NT = 0>
 __device__ __forceinline__ void load_tw(float2* tw, const float2* __restrict__ gtw) {
-  for (int m = threadIdx.x; m < L; m += blockDim.x) tw[m] = gtw[m * (kTwMax / L)];
+  if constexpr (NT > 0) {  // compile-time trip count: no division, unrolled
+#pragma unroll
+    for (int j = 0; j < (L + NT - 1) / NT; ++j) {
+      const int m = threadIdx.x + j * NT;
+      if (m < L) tw[m] = gtw[m * (kTwMax / L)];
+    }
+  } else {
+    for (int m = threadIdx.x; m < L; m += blockDim.x) tw[m] = gtw[m * (kTwMax / L)];
+  }
   __syncthreads();
 }
 
@@ -67,17 +75,19 @@ __global__ void __launch_bounds__(PassCfg<L>::NT) k_ypass(const float2* __restri
   constexpr int E = Cf::E, TL = Cf::TL, C = Cf::C;
   extern __shared__ float2 sm[];
   float2* tw = sm;
-  load_tw<L>(tw, gtw);
+  load_tw<L, Cf::NT>(tw, gtw);
   const int c = threadIdx.x % C, t = threadIdx.x / C;
   const int kx = blockIdx.x * C + c, z = blockIdx.y, comp = blockIdx.z;
   const bool ok = kx < d.NKX;
   const int nin = INV ? L : d.ny, nout = INV ? d.ny : L;
   // X side: X[c][z][y][P]; Y side: kx-slab-major Y[q][c][z][ky][KXS] (common.cuh)
-  const int q = kx / d.KXS, kxl = kx - q * d.KXS;
-  const size_t xoff = ((size_t)(comp * d.nz + z) * d.ny) * d.P + kx;
-  const size_t yoff = ((size_t)(q * 3 + comp) * d.nz + z) * (size_t)L * d.KXS + kxl;
-  const float2* src = in + (INV ? yoff : xoff);
-  const size_t sin_ = INV ? d.KXS : d.P, sout = INV ? d.P : d.KXS;
+  const int q = d.NS > 1 ? kx / d.KXS : 0, kxl = kx - q * d.KXS;  // kx slab (NS == 1: 0)
+  // 32-bit element indices (every buffer holds < 2^32 elements): an access costs one IMAD and
+  // one IMAD.WIDE.U32 instead of a 64-bit multiply-add chain
+  const unsigned xoff = ((unsigned)(comp * d.nz + z) * d.ny) * d.P + kx;
+  const unsigned yoff = ((unsigned)(q * 3 + comp) * d.nz + z) * (unsigned)L * d.KXS + kxl;
+  const unsigned ioff = INV ? yoff : xoff, ooff = INV ? xoff : yoff;
+  const unsigned sin_ = INV ? d.KXS : d.P, sout = INV ? d.P : d.KXS;
   float2 v[1][E];
 #pragma unroll
   for (int i = 0; i < E; ++i) {
@@ -85,22 +95,21 @@ __global__ void __launch_bounds__(PassCfg<L>::NT) k_ypass(const float2* __restri
     // zero padding: forward input rows >= ny <= Ly/2 are zero, i.e. every i >= E/2 (p >= L/2)
     // statically, so the first stage's butterflies fold those operands away
     v[0][i] = (!INV && 2 * i >= E) ? make_float2(0.f, 0.f)
-                                  : ((ok && p < nin) ? src[(size_t)p * sin_] : make_float2(0.f, 0.f));
+                                  : ((ok && p < nin) ? in[ioff + (unsigned)p * sin_] : make_float2(0.f, 0.f));
   }
   reg_fft<L, E, 1, INV>(v, sm + L, ColAddr<L, C>{c}, tw, t);
   if (ok) {
-    float2* dst = out + (INV ? xoff : yoff);
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       const int p = t + TL * i;
-      if ((!INV || 2 * i < E) && p < nout) dst[(size_t)p * sout] = v[0][i];  // inverse: rows < ny only
+      if ((!INV || 2 * i < E) && p < nout) out[ooff + (unsigned)p * sout] = v[0][i];  // inverse: rows < ny only
     }
   }
 }
 
 // ---------------------------------------------------------------- Khat multiply
-// Khat is real and stored folded: [6][Lz/2+1][Ly/2+1][P]; off-diagonal components flip sign
-// across the half axis they are odd in (XY: x,y; XZ: x,z; YZ: y,z).  kx is never folded.
+// Khat is real and stored folded and interleaved: [Lz/2+1][Ly/2+1][P][6]; off-diagonal components
+// flip sign across the half axis they are odd in (XY: x,y; XZ: x,z; YZ: y,z).  kx is never folded.
 __device__ __forceinline__ void khat_apply(const float* __restrict__ khat, const Dims& d, int kx, int ky, int kz,
                                            float2& mx, float2& my, float2& mz) {
   const int hy = d.Ly / 2, hz = d.Lz / 2;
@@ -108,12 +117,13 @@ __device__ __forceinline__ void khat_apply(const float* __restrict__ khat, const
   const int kzf = kz <= hz ? kz : d.Lz - kz;
   const float sy = ky <= hy ? 1.f : -1.f;
   const float sz = kz <= hz ? 1.f : -1.f;
-  const size_t cs = (size_t)(hz + 1) * (hy + 1) * d.P;
-  const size_t b = ((size_t)kzf * (hy + 1) + kyf) * d.P + kx;
-  const float kxx = __ldg(khat + b), kyy = __ldg(khat + cs + b), kzz = __ldg(khat + 2 * cs + b);
-  const float kxy = sy * __ldg(khat + 3 * cs + b);
-  const float kxz = sz * __ldg(khat + 4 * cs + b);
-  const float kyz = sy * sz * __ldg(khat + 5 * cs + b);
+  const unsigned b = (((unsigned)kzf * (hy + 1) + kyf) * d.P + kx) * 3;  // float2 index
+  const float2* k2 = reinterpret_cast<const float2*>(khat) + b;
+  const float2 k01 = __ldg(k2), k23 = __ldg(k2 + 1), k45 = __ldg(k2 + 2);
+  const float kxx = k01.x, kyy = k01.y, kzz = k23.x;
+  const float kxy = sy * k23.y;
+  const float kxz = sz * k45.x;
+  const float kyz = sy * sz * k45.y;
   const float2 bx = make_float2(kxx * mx.x + kxy * my.x + kxz * mz.x, kxx * mx.y + kxy * my.y + kxz * mz.y);
   const float2 by = make_float2(kxy * mx.x + kyy * my.x + kyz * mz.x, kxy * mx.y + kyy * my.y + kyz * mz.y);
   const float2 bz = make_float2(kxz * mx.x + kyz * my.x + kzz * mz.x, kxz * mx.y + kyz * my.y + kzz * mz.y);
@@ -137,16 +147,16 @@ __global__ void __launch_bounds__(ZCfg<L>::NT) k_conv(float2* __restrict__ Y, co
   const int kx = blockIdx.x * C + c, ky = Y2D ? 0 : blockIdx.y;
   const bool ok = kx < d.NKX;
   const int nin = Y2D ? d.ny : d.nz;
-  const size_t lstride = Y2D ? (size_t)d.P : (size_t)d.Ly * d.P;        // between line elements
-  const size_t cstr = Y2D ? (size_t)d.ny * d.P : (size_t)d.nz * d.Ly * d.P;  // between components
-  float2* base = Y + (size_t)ky * d.P + kx;
+  const unsigned lstride = Y2D ? (unsigned)d.P : (unsigned)d.Ly * d.P;        // between line elements
+  const unsigned cstr = Y2D ? (unsigned)d.ny * d.P : (unsigned)d.nz * d.Ly * d.P;  // between components
+  const unsigned base = (unsigned)ky * d.P + kx;
   float2 v[3][E];
 #pragma unroll
   for (int g = 0; g < 3; ++g)
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       const int p = t + TL * i;
-      v[g][i] = (2 * i < E && ok && p < nin) ? base[g * cstr + p * lstride] : make_float2(0.f, 0.f);
+      v[g][i] = (2 * i < E && ok && p < nin) ? Y[base + g * cstr + p * lstride] : make_float2(0.f, 0.f);
     }
   const ColAddr<L, C> A{c};
   reg_fft<L, E, 3, false>(v, sm + L, A, tw, t);
@@ -165,7 +175,7 @@ __global__ void __launch_bounds__(ZCfg<L>::NT) k_conv(float2* __restrict__ Y, co
 #pragma unroll
       for (int i = 0; i < E; ++i) {
         const int p = t + TL * i;
-        if (2 * i < E && p < nin) base[g * cstr + p * lstride] = v[g][i];
+        if (2 * i < E && p < nin) Y[base + g * cstr + p * lstride] = v[g][i];
       }
   }
 }
@@ -197,24 +207,25 @@ __global__ void __launch_bounds__(ZSCfg<L>::NT) k_zconv_seq(float2* __restrict__
   extern __shared__ float2 sm[];
   float2* tw = sm;
   float2* xch = sm + L;  // [3][L][C]
-  load_tw<L>(tw, gtw);
+  load_tw<L, Cf::NT>(tw, gtw);
   const int c = threadIdx.x % C, t = threadIdx.x / C;
   // columns kxl of this rank's kx slab (global kx = kx0 + kxl); z runs over all nzg planes,
   // held as [source rank r][c][zl][ky][KXS] with z = r * nz + zl (NS == 1: Y[c][z][ky][P])
   const int kxl = blockIdx.x * C + c, ky = blockIdx.y, kx = d.kx0 + kxl;
   const bool ok = kxl < d.KXS && kx < d.NKX;
   const int nz = d.nzg, nzl = d.nz;
-  const size_t row = d.KXS, plane = (size_t)d.Ly * row;
-  float2* base = Y + (size_t)ky * row + kxl;
+  // 32-bit element indices (Y holds < 2^32 elements)
+  const unsigned row = d.KXS, plane = (unsigned)d.Ly * row;
+  const unsigned cbase = (unsigned)ky * row + kxl;
   // ((r * 3 + g) * nzl + z - r * nzl) planes = g * nzl + z + 2 nzl r with r = z / nzl (SPLIT
   // only: the single-slab instance keeps the plain strength-reduced addressing)
-  const size_t cstr = (size_t)nzl * plane;
+  const unsigned cstr = (unsigned)nzl * plane;
   // z / nzl in fp32: (z + 1/2) / nzl is >= 1/(2 nzl) >= 1e-3 away from an integer and the
   // rounding error is ~1e-7 relative, so the truncation is exact (z < 1024)
   const float inv_nzl = 1.f / (float)nzl;
-  auto zaddr = [&](int g, int z) -> size_t {
-    size_t a = (size_t)g * cstr + (size_t)z * plane;
-    if constexpr (SPLIT) a += (size_t)(2 * nzl * __float2int_rz(((float)z + 0.5f) * inv_nzl)) * plane;
+  auto zaddr = [&](int g, int z) -> unsigned {
+    unsigned a = cbase + (unsigned)g * cstr + (unsigned)z * plane;
+    if constexpr (SPLIT) a += (unsigned)(2 * nzl * __float2int_rz(((float)z + 0.5f) * inv_nzl)) * plane;
     return a;
   };
   struct GA {
@@ -227,7 +238,7 @@ __global__ void __launch_bounds__(ZSCfg<L>::NT) k_zconv_seq(float2* __restrict__
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       const int p = t + TL * i;
-      v[0][i] = (2 * i < E && ok && p < nz) ? base[zaddr(g, p)] : make_float2(0.f, 0.f);  // nz <= L/2
+      v[0][i] = (2 * i < E && ok && p < nz) ? Y[zaddr(g, p)] : make_float2(0.f, 0.f);  // nz <= L/2
     }
     const GA A{g, c};
     reg_fft<L, E, 1, false>(v, xch, A, tw, t);
@@ -257,7 +268,7 @@ __global__ void __launch_bounds__(ZSCfg<L>::NT) k_zconv_seq(float2* __restrict__
 #pragma unroll
       for (int i = 0; i < E; ++i) {
         const int p = t + TL * i;
-        if (2 * i < E && p < nz) base[zaddr(g, p)] = v[0][i];
+        if (2 * i < E && p < nz) Y[zaddr(g, p)] = v[0][i];
       }
     }
   }

@@ -141,7 +141,7 @@ __global__ void k_khat_finalize(const double* __restrict__ in, float* __restrict
     const int i0 = (int)(r % m0);
     const long long row = r / m0;            // kz * m1 + ky
     const double sgn = c >= 3 ? -1.0 : 1.0;  // (-i)^2 of the two odd axes
-    khat[(c * (long long)m1 * m2 + row) * P + i0] = (float)(scale * sgn * in[e]);
+    khat[(row * P + i0) * 6 + c] = (float)(scale * sgn * in[e]);  // [kz][ky][P][6]: 6 adjacent floats
   }
 }
 

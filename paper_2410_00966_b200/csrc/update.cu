@@ -156,11 +156,11 @@ __device__ __forceinline__ float3 cell_core(const UpdateArgs& a, float3 m, const
 
 // paired access to cells (x, x+1) of an SoA component: one 8-byte access when the index is even
 // (nx even), else two 4-byte ones; `two` = the second cell exists.
-__device__ __forceinline__ float2 ld_pair(const float* __restrict__ p, long long i, bool vec, bool two) {
+__device__ __forceinline__ float2 ld_pair(const float* __restrict__ p, unsigned i, bool vec, bool two) {
   if (vec) return __ldg(reinterpret_cast<const float2*>(p + i));
   return make_float2(__ldg(p + i), two ? __ldg(p + i + 1) : 0.f);
 }
-__device__ __forceinline__ void st_pair(float* __restrict__ p, long long i, float2 v, bool vec, bool two) {
+__device__ __forceinline__ void st_pair(float* __restrict__ p, unsigned i, float2 v, bool vec, bool two) {
   if (vec) {
     *reinterpret_cast<float2*>(p + i) = v;
   } else {
@@ -290,7 +290,8 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
   const float gsum = gc + ge;
   double wacc = 0.0;
   float tmax = 0.f;
-  const long long rowbase = (long long)nx * (y + (long long)ny * zs);
+  const unsigned rowbase = (unsigned)nx * (y + (unsigned)ny * zs);  // 32-bit indices (< 2^32 elements)
+  const unsigned Nu = (unsigned)N;
   const float* trow = tc + (yl + 1) * nxp;  // this row inside the z tile
   const bool vec = (nx & 1) == 0;           // global pairs are 8-byte aligned
   const bool st = a.mode == MODE_LLG || a.mode == MODE_RELAX;
@@ -307,7 +308,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
     float2 o[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
     if (rowok && x0 < nx) {
       const bool two = x0 + 1 < nx;
-      const long long idx = rowbase + x0;
+      const unsigned idx = rowbase + x0;
       // the pair (x0, x0+1) and its neighbours from the staged tile; m_n, acc, B_rms from HBM
       float2 mc[3], ym[3], yp[3], zm[3], zp[3], mn2[3], ap2[3], br2[3];
       float xl[3], xr[3];
@@ -321,9 +322,9 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
         zp[c] = zhi ? sm_pair(tzp + c * csz + yl * nxp + x0) : mc[c];
         xl[c] = x0 > 0 ? r[x0 - 1] : 0.f;
         xr[c] = x0 + 2 < nx ? r[x0 + 2] : 0.f;
-        mn2[c] = need_mn ? ld_pair(a.mN + c * N, idx, vec, two) : make_float2(0.f, 0.f);
-        ap2[c] = need_acc ? ld_pair(a.acc + c * N, idx, vec, two) : make_float2(0.f, 0.f);
-        br2[c] = need_br ? ld_pair(a.brms + c * N, idx, vec, two)
+        mn2[c] = need_mn ? ld_pair(a.mN, c * Nu + idx, vec, two) : make_float2(0.f, 0.f);
+        ap2[c] = need_acc ? ld_pair(a.acc, c * Nu + idx, vec, two) : make_float2(0.f, 0.f);
+        br2[c] = need_br ? ld_pair(a.brms, c * Nu + idx, vec, two)
                          : make_float2(a.brms_u[c], a.brms_u[c]);
       }
       float2 acc2[3], bf2[3];
@@ -368,10 +369,10 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
       }
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        if (a.mode == MODE_FIELD) st_pair(a.bout + c * N, idx, bf2[c], vec, two);
+        if (a.mode == MODE_FIELD) st_pair(a.bout, c * Nu + idx, bf2[c], vec, two);
         if (st) {
-          st_pair(a.mOut + c * N, idx, o[c], vec, two);
-          if (a.stage < 4) st_pair(a.acc + c * N, idx, acc2[c], vec, two);
+          st_pair(a.mOut, c * Nu + idx, o[c], vec, two);
+          if (a.stage < 4) st_pair(a.acc, c * Nu + idx, acc2[c], vec, two);
         }
       }
     }
