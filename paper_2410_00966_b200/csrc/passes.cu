@@ -26,6 +26,24 @@
 
 namespace mcq {
 
+// twiddles of the y / z passes: the plan table of regfft.cuh (MCQ_REGTAB, default) or the base
+// table tw[m] = exp(-2 pi i m / L)
+constexpr int PASS_TWS = MCQ_REGTAB ? 0 : 1;
+template <int L, int E>
+__host__ __device__ constexpr int pass_twn() { return MCQ_REGTAB ? reg_tw_size<L, E>() : (L < 2 ? 2 : L); }
+template <int L, int E, int NT>
+__device__ __forceinline__ void pass_tw(float2* tw, const float2* __restrict__ gtw) {
+  if constexpr (MCQ_REGTAB) {
+    reg_tw_build<L, E, NT>(tw, gtw);
+  } else {
+#pragma unroll
+    for (int j = 0; j < (L + NT - 1) / NT; ++j) {
+      const int m = threadIdx.x + j * NT;
+      if (m < L) tw[m] = gtw[m * (kTwMax / L)];
+    }
+  }
+}
+
 template <int L>
 struct PassCfg {  // single-component passes (K-Y, K-YI)
   static constexpr int E = L < 16 ? L : 16;
@@ -33,7 +51,8 @@ struct PassCfg {  // single-component passes (K-Y, K-YI)
   static constexpr int C0 = 256 / TL;
   static constexpr int C = C0 < 8 ? 8 : (C0 > 64 ? 64 : C0);
   static constexpr int NT = C * TL;
-  static constexpr size_t SMEM = (size_t)(L + (TL > 1 ? L * C : 0)) * sizeof(float2);
+  static constexpr int TWN = pass_twn<L, E>();  // twiddle table (complex)
+  static constexpr size_t SMEM = (size_t)(TWN + (TL > 1 ? L * C : 0)) * sizeof(float2);
 };
 
 template <int L>
@@ -43,22 +62,9 @@ struct ZCfg {  // three-component passes with the Khat multiply (K-Z, K-Y2D)
   static constexpr int C0 = 256 / TL;
   static constexpr int C = C0 < 4 ? 4 : (C0 > 64 ? 64 : C0);
   static constexpr int NT = C * TL;
-  static constexpr size_t SMEM = (size_t)(L + (TL > 1 ? 3 * L * C : 0)) * sizeof(float2);
+  static constexpr int TWN = pass_twn<L, E>();
+  static constexpr size_t SMEM = (size_t)(TWN + (TL > 1 ? 3 * L * C : 0)) * sizeof(float2);
 };
-
-template <int L, int NT = 0>
-__device__ __forceinline__ void load_tw(float2* tw, const float2* __restrict__ gtw) {
-  if constexpr (NT > 0) {  // compile-time trip count: no division, unrolled
-#pragma unroll
-    for (int j = 0; j < (L + NT - 1) / NT; ++j) {
-      const int m = threadIdx.x + j * NT;
-      if (m < L) tw[m] = gtw[m * (kTwMax / L)];
-    }
-  } else {
-    for (int m = threadIdx.x; m < L; m += blockDim.x) tw[m] = gtw[m * (kTwMax / L)];
-  }
-  __syncthreads();
-}
 
 // shared-memory address of (line l, position pos) for column c: [l][pos][c]
 template <int L, int C>
@@ -73,9 +79,10 @@ __global__ void __launch_bounds__(PassCfg<L>::NT) k_ypass(const float2* __restri
                                                           Dims d, const float2* __restrict__ gtw) {
   using Cf = PassCfg<L>;
   constexpr int E = Cf::E, TL = Cf::TL, C = Cf::C;
-  extern __shared__ float2 sm[];
-  float2* tw = sm;
-  load_tw<L, Cf::NT>(tw, gtw);
+  extern __shared__ __align__(16) float2 sm[];
+  float2* tw = sm;  // plan twiddles
+  pass_tw<L, E, Cf::NT>(tw, gtw);
+  __syncthreads();
   const int c = threadIdx.x % C, t = threadIdx.x / C;
   const int kx = blockIdx.x * C + c, z = blockIdx.y, comp = blockIdx.z;
   const bool ok = kx < d.NKX;
@@ -97,7 +104,7 @@ __global__ void __launch_bounds__(PassCfg<L>::NT) k_ypass(const float2* __restri
     v[0][i] = (!INV && 2 * i >= E) ? make_float2(0.f, 0.f)
                                   : ((ok && p < nin) ? in[ioff + (unsigned)p * sin_] : make_float2(0.f, 0.f));
   }
-  reg_fft<L, E, 1, INV>(v, sm + L, ColAddr<L, C>{c}, tw, t);
+  reg_fft<L, E, 1, INV, PASS_TWS>(v, sm + Cf::TWN, ColAddr<L, C>{c}, tw, t);
   if (ok) {
 #pragma unroll
     for (int i = 0; i < E; ++i) {
@@ -140,9 +147,10 @@ __global__ void __launch_bounds__(ZCfg<L>::NT) k_conv(float2* __restrict__ Y, co
                                                       const float2* __restrict__ gtw) {
   using Cf = ZCfg<L>;
   constexpr int E = Cf::E, TL = Cf::TL, C = Cf::C;
-  extern __shared__ float2 sm[];
+  extern __shared__ __align__(16) float2 sm[];
   float2* tw = sm;
-  load_tw<L>(tw, gtw);
+  pass_tw<L, E, Cf::NT>(tw, gtw);
+  __syncthreads();
   const int c = threadIdx.x % C, t = threadIdx.x / C;
   const int kx = blockIdx.x * C + c, ky = Y2D ? 0 : blockIdx.y;
   const bool ok = kx < d.NKX;
@@ -159,7 +167,7 @@ __global__ void __launch_bounds__(ZCfg<L>::NT) k_conv(float2* __restrict__ Y, co
       v[g][i] = (2 * i < E && ok && p < nin) ? Y[base + g * cstr + p * lstride] : make_float2(0.f, 0.f);
     }
   const ColAddr<L, C> A{c};
-  reg_fft<L, E, 3, false>(v, sm + L, A, tw, t);
+  reg_fft<L, E, 3, false, PASS_TWS>(v, sm + Cf::TWN, A, tw, t);
   if (ok) {
 #pragma unroll
     for (int i = 0; i < E; ++i) {
@@ -168,7 +176,7 @@ __global__ void __launch_bounds__(ZCfg<L>::NT) k_conv(float2* __restrict__ Y, co
       if ((i & 1) == 1) asm volatile("" ::: "memory");  // bound load hoisting (register budget)
     }
   }
-  reg_fft<L, E, 3, true>(v, sm + L, A, tw, t);
+  reg_fft<L, E, 3, true, PASS_TWS>(v, sm + Cf::TWN, A, tw, t);
   if (ok) {
 #pragma unroll
     for (int g = 0; g < 3; ++g)
@@ -196,7 +204,8 @@ struct ZSCfg {
   static constexpr int C0 = 256 / TL;
   static constexpr int C = C0 < 4 ? 4 : (C0 > 64 ? 64 : C0);
   static constexpr int NT = C * TL;
-  static constexpr size_t SMEM = (size_t)(L + 3 * L * C) * sizeof(float2);
+  static constexpr int TWN = pass_twn<L, E>();
+  static constexpr size_t SMEM = (size_t)(TWN + 3 * L * C) * sizeof(float2);
 };
 
 template <int L, bool SPLIT>
@@ -204,10 +213,11 @@ __global__ void __launch_bounds__(ZSCfg<L>::NT) k_zconv_seq(float2* __restrict__
                                                             Dims d, const float2* __restrict__ gtw) {
   using Cf = ZSCfg<L>;
   constexpr int E = Cf::E, TL = Cf::TL, C = Cf::C;
-  extern __shared__ float2 sm[];
+  extern __shared__ __align__(16) float2 sm[];
   float2* tw = sm;
-  float2* xch = sm + L;  // [3][L][C]
-  load_tw<L, Cf::NT>(tw, gtw);
+  float2* xch = sm + Cf::TWN;  // [3][L][C]
+  pass_tw<L, E, Cf::NT>(tw, gtw);
+  __syncthreads();
   const int c = threadIdx.x % C, t = threadIdx.x / C;
   // columns kxl of this rank's kx slab (global kx = kx0 + kxl); z runs over all nzg planes,
   // held as [source rank r][c][zl][ky][KXS] with z = r * nz + zl (NS == 1: Y[c][z][ky][P])
@@ -241,7 +251,7 @@ __global__ void __launch_bounds__(ZSCfg<L>::NT) k_zconv_seq(float2* __restrict__
       v[0][i] = (2 * i < E && ok && p < nz) ? Y[zaddr(g, p)] : make_float2(0.f, 0.f);  // nz <= L/2
     }
     const GA A{g, c};
-    reg_fft<L, E, 1, false>(v, xch, A, tw, t);
+    reg_fft<L, E, 1, false, PASS_TWS>(v, xch, A, tw, t);
 #pragma unroll
     for (int i = 0; i < E; ++i) xch[A(0, t + TL * i)] = v[0][i];
   }
@@ -263,7 +273,7 @@ __global__ void __launch_bounds__(ZSCfg<L>::NT) k_zconv_seq(float2* __restrict__
 #pragma unroll
     for (int i = 0; i < E; ++i) v[0][i] = xch[A(0, t + TL * i)];
     __syncthreads();  // region g is read before its exchanges overwrite it
-    reg_fft<L, E, 1, true>(v, xch, A, tw, t);
+    reg_fft<L, E, 1, true, PASS_TWS>(v, xch, A, tw, t);
     if (ok) {
 #pragma unroll
       for (int i = 0; i < E; ++i) {
@@ -289,7 +299,7 @@ struct ZTCfg {
   static constexpr int C0 = 256 / TL;
   static constexpr int C = C0 < 4 ? 4 : (C0 > 64 ? 64 : C0);
   static constexpr int NT = C * TL;
-  static constexpr int TWP = (L + 15) / 16 * 16;           // twiddle slots, keeps the stages 128 B aligned
+  static constexpr int TWP = (pass_twn<L, E>() + 15) / 16 * 16;  // twiddle slots, keeps the stages 128 B aligned
   static constexpr int GS = ((L / 2) * C + 15) / 16 * 16;  // per-component box stride (128 B aligned)
   static constexpr int STAGE = 3 * GS;                     // complex per input stage (nz <= L/2)
   static constexpr size_t SMEM = (size_t)(TWP + 2 * STAGE + (TL > 1 ? 3 * L * C : 0)) * sizeof(float2);
@@ -314,7 +324,7 @@ __global__ void __launch_bounds__(ZTCfg<L>::NT, MINB) k_zconv_tma(const __grid_c
     mbar_init(&bar[1], 1);
     fence_mbar_init();
   }
-  for (int m = threadIdx.x; m < L; m += blockDim.x) tw[m] = gtw[m * (kTwMax / L)];
+  pass_tw<L, E, Cf::NT>(tw, gtw);
   __syncthreads();
   auto issue = [&](int tile, int b) {
     const int kx0 = (tile % nkt) * C, ky = tile / nkt;
@@ -341,7 +351,7 @@ __global__ void __launch_bounds__(ZTCfg<L>::NT, MINB) k_zconv_tma(const __grid_c
         const int p = t + TL * i;
         v[g][i] = (2 * i < E && p < nz) ? in[g * Cf::GS + p * C + c] : make_float2(0.f, 0.f);
       }
-    reg_fft<L, E, 3, false>(v, xch, A, tw, t);
+    reg_fft<L, E, 3, false, PASS_TWS>(v, xch, A, tw, t);
     const bool ok = kx < d.NKX;
     if (ok) {
 #pragma unroll
@@ -350,7 +360,7 @@ __global__ void __launch_bounds__(ZTCfg<L>::NT, MINB) k_zconv_tma(const __grid_c
         if ((i & 1) == 1) asm volatile("" ::: "memory");
       }
     }
-    reg_fft<L, E, 3, true>(v, xch, A, tw, t);
+    reg_fft<L, E, 3, true, PASS_TWS>(v, xch, A, tw, t);
     if (ok) {
       float2* base = Y + (size_t)ky * d.P + kx;
 #pragma unroll

@@ -10,7 +10,11 @@
 //     v[r] = x[b + r L/R] * w_{Ns R}^{r k},  v = DFT_R(v),  y[(b - k) R + k + r Ns] = v[r]
 // Thread t runs butterflies b = t + q*TL (q < E/R) whose inputs are exactly its positions
 // p_{q + r E/R}; in the last stage (Ns R = L) the outputs land on the same positions.
+// Twiddles come from a per-plan table in shared memory (reg_tw_build): for every stage with
+// Ns > 1 the R factors w_{Ns R}^{r k} of butterfly class k are contiguous, so a butterfly reads
+// them with R/2 16-byte loads at immediate offsets from one base address.
 #pragma once
+#include "common.cuh"  // kTwMax
 #include "fft.cuh"
 
 namespace mcq {
@@ -24,11 +28,47 @@ __host__ __device__ constexpr int reg_radix(int Ns) {
   return Ns == 1 ? first : RMAX;
 }
 
+// offset of stage Ns's twiddle block in the plan table, and the table size (complex entries)
+template <int L, int E>
+__host__ __device__ constexpr int reg_tw_off(int Ns) {
+  int off = 0;
+  for (int n = 1; n < Ns && n < L;) {
+    const int R = reg_radix<L, E>(n);
+    if (n > 1) off += n * R;
+    n *= R;
+  }
+  return off;
+}
+template <int L, int E>
+__host__ __device__ constexpr int reg_tw_size() {
+  const int s = reg_tw_off<L, E>(L);
+  return s < 2 ? 2 : s;
+}
+
+// Fill the plan table from the global fp64-generated table gtw[m] = exp(-2 pi i m / kTwMax)
+// (stage Ns, radix R, class k < Ns, factor r < R: w_{Ns R}^{r k}).  Caller synchronises.
+template <int L, int E, int NT, int Ns = 1, int OFF = 0>
+__device__ __forceinline__ void reg_tw_build(float2* st, const float2* __restrict__ gtw) {
+  if constexpr (Ns < L) {
+    constexpr int R = reg_radix<L, E>(Ns);
+    if constexpr (Ns > 1) {
+#pragma unroll
+      for (int j = 0; j < (Ns * R + NT - 1) / NT; ++j) {
+        const int e = threadIdx.x + j * NT;
+        if (e < Ns * R) st[OFF + e] = gtw[((e & (R - 1)) * (e / R)) * (kTwMax / (Ns * R))];
+      }
+    }
+    reg_tw_build<L, E, NT, Ns * R, OFF + (Ns > 1 ? Ns * R : 0)>(st, gtw);
+  }
+}
+
 // v[l][i]: NLT lines per thread.  A(l, pos): shared-memory index of element pos of the
-// thread's line l.  tw[m * TWS] = exp(-2 pi i m / L).
+// thread's line l.  TWS == 0: st is the plan's twiddle table (reg_tw_build), 16-byte aligned;
+// TWS > 0: st is a base table, st[m * TWS] = exp(-2 pi i m / L) (fewer live registers when a
+// thread runs many small-radix butterflies).
 template <int L, int E, int NLT, bool INV, int TWS, int Ns, class Addr>
 __device__ __forceinline__ void reg_stage(float2 (&v)[NLT][E], float2* __restrict__ sm, const Addr& A,
-                                          const float2* __restrict__ tw, int t) {
+                                          const float2* __restrict__ st, int t) {
   if constexpr (Ns < L) {
     constexpr int R = reg_radix<L, E>(Ns);
     constexpr int TL = L / E;
@@ -40,10 +80,18 @@ __device__ __forceinline__ void reg_stage(float2 (&v)[NLT][E], float2* __restric
       const int k = b & (Ns - 1);
       // twiddles depend only on the butterfly, so all NLT lines of the thread share them
       float2 w[R];
+      if constexpr (Ns > 1 && TWS == 0) {  // plan table: R/2 16-byte loads from one base
+        const float4* w4 = reinterpret_cast<const float4*>(st + reg_tw_off<L, E>(Ns) + k * R);
 #pragma unroll
-      for (int r = 1; r < R; ++r) {
-        if (Ns > 1) {
-          w[r] = tw[(r * k * (L / (Ns * R))) * TWS];
+        for (int r2 = 0; r2 < R / 2; ++r2) {
+          const float4 p = w4[r2];
+          w[2 * r2] = make_float2(p.x, INV ? -p.y : p.y);
+          w[2 * r2 + 1] = make_float2(p.z, INV ? -p.w : p.w);
+        }
+      } else if constexpr (Ns > 1) {  // base table st[m * TWS] = exp(-2 pi i m / L)
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+          w[r] = st[(r * k * (L / (Ns * R))) * TWS];
           if (INV) w[r].y = -w[r].y;
         }
       }
@@ -73,16 +121,19 @@ __device__ __forceinline__ void reg_stage(float2 (&v)[NLT][E], float2* __restric
 #pragma unroll
         for (int i = 0; i < E; ++i) v[l][i] = sm[A(l, t + TL * i)];
       __syncthreads();  // the next stage stores into the same buffer
-      reg_stage<L, E, NLT, INV, TWS, Ns * R, Addr>(v, sm, A, tw, t);
+      reg_stage<L, E, NLT, INV, TWS, Ns * R, Addr>(v, sm, A, st, t);
     }
   }
 }
 
-template <int L, int E, int NLT, bool INV, int TWS = 1, class Addr>
+#ifndef MCQ_REGTAB
+#define MCQ_REGTAB 0  // plan twiddle tables in the y / z passes (measured: K-Y 37.6 vs 35.3 us, K-Z equal)
+#endif
+template <int L, int E, int NLT, bool INV, int TWS = 0, class Addr>
 __device__ __forceinline__ void reg_fft(float2 (&v)[NLT][E], float2* __restrict__ sm, const Addr& A,
-                                        const float2* __restrict__ tw, int t) {
+                                        const float2* __restrict__ st, int t) {
   static_assert((L & (L - 1)) == 0 && E <= L && L % E == 0, "plan");
-  reg_stage<L, E, NLT, INV, TWS, 1, Addr>(v, sm, A, tw, t);
+  reg_stage<L, E, NLT, INV, TWS, 1, Addr>(v, sm, A, st, t);
 }
 
 }  // namespace mcq

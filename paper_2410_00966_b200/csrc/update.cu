@@ -178,7 +178,9 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
   using Cf = UCfg<N2>;
   constexpr int E = Cf::E, TL = Cf::TL, RY = Cf::RY, NT = Cf::NT, LX = 2 * N2, PITCH = Cf::PITCH;
   extern __shared__ __align__(16) float2 sm[];
-  float2* tw = sm;       // w_Lx^m, m < Lx
+  // w_Lx^m, m < Lx: packing / unpacking of the real transforms and, every other entry, the
+  // row FFTs' twiddles (base table, TWS = 2: fewer live registers than a plan table here)
+  float2* tw = sm;
   float2* xs = sm + LX;  // [3][RY][PITCH]: X rows (staged by TMA), then the FFT exchange buffer
   float* tc = reinterpret_cast<float*>(reinterpret_cast<char*>(sm) + Cf::XS_BYTES);  // [3][RY+2][nx]
   float* tzm = tc + Cf::TILE_C;                                                       // [3][RY][nx]
