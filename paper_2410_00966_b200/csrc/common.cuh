@@ -19,9 +19,12 @@ constexpr int kTwMax = 1024;                     // global twiddle table length 
 // z-slab decomposition over NS ranks: nz below is the rank's number of planes,
 // nzg the global one, zg0 the global index of local plane 0.  State arrays carry zoff (0 or 1)
 // halo planes on each side: cell (x, y, z) of component c sits at c*cs + ((z+zoff)*ny + y)*nx + x.
-// Y is kx-slab-major: Y[q][c][z][ky][KXS] with q = kx / KXS the rank owning column kx in the
-// z pass; for NS == 1 this is exactly Y[c][z][ky][P] (KXS == P).  After the forward all-to-all a
-// rank holds R[r][c][zl][ky][KXS] (r = source rank, z = r*nz + zl) for its KXS columns.
+// Y is kx-slab-major: Y[q][c][z][ky][KXS] with q = kx_owner(kx) the rank owning column kx in the
+// z pass (columns [kx_first(q), kx_first(q+1)), KXS >= every rank's width); for NS == 1 this is
+// exactly Y[c][z][ky][P] (KXS == P).  After the forward all-to-all a rank holds
+// R[r][c][zl][ky][KXS] (r = source rank, z = r*nz + zl) for its kxw columns.
+// kx split: blocks of KG columns (KG = 16 when NKX >= 16 NS, else the largest power of two with
+// NKX / KG >= NS), KB = NKX / KG blocks spread evenly, the last rank also takes the tail columns.
 struct Dims {
   int nx, ny, nz;     // grid (nz: local planes)
   int Lx, Ly, Lz;     // zero-padded FFT lengths (next pow2 >= 2n; 1 if n == 1), Lz from nzg
@@ -31,9 +34,22 @@ struct Dims {
   long long N;        // nx * ny * nz (local cells)
   int nzg, zg0, zoff; // global planes, global z of local plane 0, halo planes per side
   long long cs;       // component stride of the state arrays: nx * ny * (nz + 2 zoff)
-  int NS, KXS;        // kx slabs (ranks) and their width; NS * KXS >= NKX
-  int kx0;            // first kx column of this rank's slab in the z pass (rank * KXS)
+  int NS, KXS;        // kx slabs (ranks) and their storage width (KXS >= every slab's width)
+  int kx0, kxw;       // first kx column and width of this rank's slab in the z pass
+  int KG, KB;         // kx split: block size (power of two) and number of whole blocks
 };
+
+// owner of column kx and first column of rank q under the kx split above
+__host__ __device__ __forceinline__ int kx_first(const Dims& d, int q) {
+  return q >= d.NS ? d.NKX : d.KG * ((q * d.KB) / d.NS);
+}
+__host__ __device__ __forceinline__ int kx_owner(const Dims& d, int kx) {
+  if (d.NS == 1) return 0;
+  const int blk = kx / d.KG;
+  if (blk >= d.KB) return d.NS - 1;
+  const int q = ((blk + 1) * d.NS - 1) / d.KB;
+  return q < d.NS - 1 ? q : d.NS - 1;
+}
 
 // Cavity state on the device (fp64), advanced once per step by k_cavity (a13).
 struct CavState {
@@ -89,14 +105,16 @@ struct UpdateArgs {
 // ---------------------------------------------------------------- launchers
 // passes.cu
 void configure_pass_kernels();
-void launch_yfwd(const Dims& d, const float2* X, float2* Y, const float2* tw, cudaStream_t s);
-void launch_zconv(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t s);
-void launch_zconv_seq(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t s);
+// (pass launchers return the number of kernels they launched: a narrow tail launch covers the
+// last kx columns beyond the final full column tile)
+int launch_yfwd(const Dims& d, const float2* X, float2* Y, const float2* tw, cudaStream_t s);
+int launch_zconv(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t s);
+int launch_zconv_seq(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t s);
 int zconv_tma_box_c(int Lz);  // kx columns per K-Z tile of the TMA-pipelined variant
-void launch_zconv_tma(const Dims& d, const void* tmap /* CUtensorMap over Y */, float2* Y, const float* khat,
-                      const float2* tw, cudaStream_t s);
-void launch_yinv(const Dims& d, const float2* Y, float2* X, const float2* tw, cudaStream_t s);
-void launch_y2d(const Dims& d, float2* X, const float* khat, const float2* tw, cudaStream_t s);
+int launch_zconv_tma(const Dims& d, const void* tmap /* CUtensorMap over Y */, float2* Y, const float* khat,
+                     const float2* tw, cudaStream_t s);
+int launch_yinv(const Dims& d, const float2* Y, float2* X, const float2* tw, cudaStream_t s);
+int launch_y2d(const Dims& d, float2* X, const float* khat, const float2* tw, cudaStream_t s);
 // update.cu
 void configure_update_kernels();
 void launch_update(const UpdateArgs& a, const float2* tw, cudaStream_t s);

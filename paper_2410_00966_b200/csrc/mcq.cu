@@ -121,6 +121,7 @@ struct mcq_ctx {
   // graphs: [0] = 1 LLG step, [1] = kGraphSteps LLG steps, [2] = 1 relax step, [3] = relax chunk
   cudaGraphExec_t g[4] = {nullptr, nullptr, nullptr, nullptr};
   double g_dt[4] = {0, 0, 0, 0};
+  long long g_launches[4] = {0, 0, 0, 0};
   long long launches = 0;
   alignas(64) CUtensorMap tmz;  // TMA descriptor of Y for the pipelined K-Z kernel (1 slab)
   bool have_tmz = false;
@@ -246,8 +247,8 @@ struct Enq {
   void pre(int k) {
     if (hook) hook(user, k, true);
   }
-  void post(int k) {
-    ++count;
+  void post(int k, int n = 1) {  // n: kernels the launcher issued
+    count += n;
     if (hook) hook(user, k, false);
   }
   void copy(void* dst, const void* src, size_t bytes) {
@@ -322,8 +323,8 @@ struct Enq {
     if (d0.nzg > 1) {
       for (auto& sl : c->sl) {
         pre(MCQ_K_YFWD);
-        launch_yfwd(sl.d, sl.X, sl.Y, c->tw, s);
-        post(MCQ_K_YFWD);
+        const int n = launch_yfwd(sl.d, sl.X, sl.Y, c->tw, s);
+        post(MCQ_K_YFWD, n);
       }
       if (NS > 1) alltoall(true);
       for (auto& sl : c->sl) {
@@ -332,25 +333,26 @@ struct Enq {
         // K-Z variant (measured on configs[1], 1x B200: seq 170 us, tma 180 us, plain 206 us per
         // launch); MCQ_ZVARIANT=tma|plain selects the others (single slab only)
         static const char* zv = getenv("MCQ_ZVARIANT");
+        int n;
         if (NS == 1 && zv && !strcmp(zv, "tma") && c->have_tmz)
-          launch_zconv_tma(sl.d, &c->tmz, Z, c->khat, c->tw, s);
+          n = launch_zconv_tma(sl.d, &c->tmz, Z, c->khat, c->tw, s);
         else if (NS == 1 && zv && !strcmp(zv, "plain"))
-          launch_zconv(sl.d, Z, c->khat, c->tw, s);
+          n = launch_zconv(sl.d, Z, c->khat, c->tw, s);
         else
-          launch_zconv_seq(sl.d, Z, c->khat, c->tw, s);
-        post(MCQ_K_ZCONV);
+          n = launch_zconv_seq(sl.d, Z, c->khat, c->tw, s);
+        post(MCQ_K_ZCONV, n);
       }
       if (NS > 1) alltoall(false);
       for (auto& sl : c->sl) {
         pre(MCQ_K_YINV);
-        launch_yinv(sl.d, sl.Y, sl.X, c->tw, s);
-        post(MCQ_K_YINV);
+        const int n = launch_yinv(sl.d, sl.Y, sl.X, c->tw, s);
+        post(MCQ_K_YINV, n);
       }
     } else {
       for (auto& sl : c->sl) {
         pre(MCQ_K_Y2D);
-        launch_y2d(sl.d, sl.X, c->khat, c->tw, s);
-        post(MCQ_K_Y2D);
+        const int n = launch_y2d(sl.d, sl.X, c->khat, c->tw, s);
+        post(MCQ_K_Y2D, n);
       }
     }
   }
@@ -427,7 +429,8 @@ int capture(mcq_ctx* c, int which, double dt, int steps) {
     cudaGraphExecDestroy(c->g[which]);
     c->g[which] = nullptr;
   }
-  CK(c, cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
+  // NCCL contexts: relaxed mode (NCCL may make capture-unsafe runtime calls on its own threads)
+  CK(c, cudaStreamBeginCapture(c->cap, c->mode == 2 ? cudaStreamCaptureModeRelaxed : cudaStreamCaptureModeThreadLocal));
   Enq q{c, c->cap};
   for (int i = 0; i < steps; ++i) {
     if (which < 2)
@@ -448,12 +451,8 @@ int capture(mcq_ctx* c, int which, double dt, int steps) {
   cudaGraphDestroy(graph);
   if (e3 != cudaSuccess) return fail(c, MCQ_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e3));
   c->g_dt[which] = dt;
+  c->g_launches[which] = q.count;  // kernels one replay launches (the gpu_launches claim)
   return MCQ_OK;
-}
-
-long long kernels_per_step(const mcq_ctx* c, bool llg) {
-  const int demag = c->dg.nz > 1 ? 3 : 1;
-  return (long long)c->sl.size() * 4 * (demag + 1) + (llg ? 1 : 0);
 }
 
 int set_cav_state(mcq_ctx* c, double re, double im, double t, long long step) {
@@ -664,6 +663,9 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
   g.NS = 1;
   g.KXS = g.P;
   g.kx0 = 0;
+  g.kxw = g.NKX;
+  g.KG = 16;
+  g.KB = g.NKX / 16;
   auto bail = [&](int code) {
     free_all(c);
     delete c;
@@ -693,7 +695,16 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
   }
   // slabs
   const int nzl = g.nz / world;
-  const int kxs = world == 1 ? g.P : ((g.NKX + world - 1) / world + 15) / 16 * 16;
+  // kx split (common.cuh): the largest block KG <= 16 giving every rank at least one block
+  int kg = 16;
+  while (kg > 1 && g.NKX / kg < world) kg /= 2;
+  Dims split = g;
+  split.NS = world;
+  split.KG = kg;
+  split.KB = g.NKX / kg;
+  int kxs = 0;
+  for (int q = 0; q < world; ++q) kxs = std::max(kxs, kx_first(split, q + 1) - kx_first(split, q));
+  kxs = world == 1 ? g.P : (kxs + 3) / 4 * 4;  // 32-byte rows
   const int first = c->mode == 2 ? c->rank : 0, count = c->mode == 1 ? world : 1;
   c->sl.resize(count);
   Dims probe = g;
@@ -710,7 +721,10 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
     s.d.cs = (long long)g.nx * g.ny * (nzl + 2 * s.d.zoff);
     s.d.NS = world;
     s.d.KXS = kxs;
-    s.d.kx0 = r * kxs;
+    s.d.KG = split.KG;
+    s.d.KB = split.KB;
+    s.d.kx0 = kx_first(split, r);
+    s.d.kxw = kx_first(split, r + 1) - s.d.kx0;
     s.nparts = update_grid_blocks(s.d);
     if (alloc_slab(c, s) != MCQ_OK) return bail(MCQ_ENOMEM);
   }
@@ -731,7 +745,9 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
       s.partials = c->partials + (size_t)i * s.nparts;  // global z order = slab order
     }
   }
-  if (cudaMemsetAsync(c->khat, 0, 6ULL * (g.Lz / 2 + 1) * (g.Ly / 2 + 1) * g.P * 4, c->stream) != cudaSuccess)
+  if (cudaMemsetAsync(c->khat, 0, 6ULL * (g.Lz / 2 + 1) * (g.Ly / 2 + 1) * g.P * 4, c->stream) != cudaSuccess ||
+      cudaMemsetAsync(c->partials, 0, (size_t)c->nparts * 8, c->stream) != cudaSuccess ||
+      cudaMemsetAsync(c->maxbits, 0, 4, c->stream) != cudaSuccess)
     return bail(MCQ_ECUDA);
   // twiddles w_1024^m = exp(-2 pi i m / 1024), generated in fp64
   {
@@ -744,6 +760,19 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
   }
   if (build_khat(c, nullptr) != MCQ_OK) return bail(MCQ_ECUDA);
   make_y_tensor_map(c);
+  if (c->mode == 2) {
+    // one eager round of every exchange (on zeroed buffers): NCCL sets up its peer connections
+    // here, outside any graph capture
+    Enq q{c, c->stream};
+    q.halo(0);
+    if (g.nz > 1) {
+      q.alltoall(true);
+      q.alltoall(false);
+    }
+    q.nk(nccl_api()->allGather(c->sl[0].partials, c->partials, c->sl[0].nparts, ncclDouble, c->comm, c->stream));
+    q.nk(nccl_api()->allReduce(c->maxbits, c->maxbits, 1, ncclFloat, ncclMax, c->comm, c->stream));
+    if (q.rc != MCQ_OK || cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(MCQ_ENCCL);
+  }
   if (reset_memory(c) != MCQ_OK) return bail(MCQ_ECUDA);
   *out = c;
   return MCQ_OK;
@@ -916,7 +945,7 @@ int mcq_run(mcq_ctx* c, double dt, long long steps) {
   if (steps % kGraphSteps && (rc = capture(c, 0, dt, 1)) != MCQ_OK) return rc;
   for (long long i = 0; i < steps / kGraphSteps; ++i) CK(c, cudaGraphLaunch(c->g[1], c->stream));
   for (long long i = 0; i < steps % kGraphSteps; ++i) CK(c, cudaGraphLaunch(c->g[0], c->stream));
-  c->launches += steps * kernels_per_step(c, true);
+  c->launches += (steps / kGraphSteps) * c->g_launches[1] + (steps % kGraphSteps) * c->g_launches[0];
   return MCQ_OK;
 }
 
@@ -935,7 +964,7 @@ int mcq_relax(mcq_ctx* c, double dt, double tol, long long max_steps, long long*
       if ((rc = capture(c, 2, dt, 1)) != MCQ_OK) return rc;
       for (long long i = 0; i < k; ++i) CK(c, cudaGraphLaunch(c->g[2], c->stream));
     }
-    c->launches += k * kernels_per_step(c, false);
+    c->launches += k == kRelaxCheck ? c->g_launches[3] : k * c->g_launches[2];
     done += k;
     CK(c, cudaMemsetAsync(c->maxbits, 0, 4, c->stream));
     Enq q{c, c->stream};

@@ -44,12 +44,15 @@ __device__ __forceinline__ void pass_tw(float2* tw, const float2* __restrict__ g
   }
 }
 
-template <int L>
+// CW > 0: a configuration with CW columns per CTA (a separate narrow launch for the last kx
+// column beyond the final 16-column tile was measured slower: the extra kernel boundary costs
+// more than the mostly idle tile it replaces)
+template <int L, int CW = 0>
 struct PassCfg {  // single-component passes (K-Y, K-YI)
   static constexpr int E = L < 16 ? L : 16;
   static constexpr int TL = L / E;
   static constexpr int C0 = 256 / TL;
-  static constexpr int C = C0 < 8 ? 8 : (C0 > 64 ? 64 : C0);
+  static constexpr int C = CW > 0 ? CW : (C0 < 8 ? 8 : (C0 > 64 ? 64 : C0));
   static constexpr int NT = C * TL;
   static constexpr int TWN = pass_twn<L, E>();  // twiddle table (complex)
   static constexpr size_t SMEM = (size_t)(TWN + (TL > 1 ? L * C : 0)) * sizeof(float2);
@@ -74,21 +77,29 @@ struct ColAddr {
 };
 
 // ---------------------------------------------------------------- K-Y forward / inverse
-template <int L, bool INV>
-__global__ void __launch_bounds__(PassCfg<L>::NT) k_ypass(const float2* __restrict__ in, float2* __restrict__ out,
-                                                          Dims d, const float2* __restrict__ gtw) {
-  using Cf = PassCfg<L>;
+template <int L, bool INV, int CW = 0>
+__global__ void __launch_bounds__(PassCfg<L, CW>::NT) k_ypass(const float2* __restrict__ in, float2* __restrict__ out,
+                                                              Dims d, const float2* __restrict__ gtw, int nfull) {
+  using Cf = PassCfg<L, CW>;
   constexpr int E = Cf::E, TL = Cf::TL, C = Cf::C;
-  extern __shared__ __align__(16) float2 sm[];
+  extern __shared__ __align__(128) float2 sm[];
   float2* tw = sm;  // plan twiddles
   pass_tw<L, E, Cf::NT>(tw, gtw);
   __syncthreads();
   const int c = threadIdx.x % C, t = threadIdx.x / C;
-  const int kx = blockIdx.x * C + c, z = blockIdx.y, comp = blockIdx.z;
-  const bool ok = kx < d.NKX;
+  // the first nlone CTAs are "lone column" CTAs whose C lanes take C planes of the last column
+  // (NKX = C * nfull + 1), so that column costs nz / C CTAs instead of nz mostly idle ones
+  // (scheduled first: as the last wave they would extend the kernel's tail); the others are
+  // column tile (b % nfull) at plane b / nfull
+  const int nlone = (gridDim.x - nfull * d.nz), comp = blockIdx.y;
+  const bool lone = (int)blockIdx.x < nlone;
+  const int b = blockIdx.x - nlone;
+  const int kx = lone ? d.NKX - 1 : (b % nfull) * C + c;
+  const int z = lone ? blockIdx.x * C + c : b / nfull;
+  const bool ok = kx < d.NKX && z < d.nz;
   const int nin = INV ? L : d.ny, nout = INV ? d.ny : L;
   // X side: X[c][z][y][P]; Y side: kx-slab-major Y[q][c][z][ky][KXS] (common.cuh)
-  const int q = d.NS > 1 ? kx / d.KXS : 0, kxl = kx - q * d.KXS;  // kx slab (NS == 1: 0)
+  const int q = kx_owner(d, kx), kxl = kx - (q > 0 ? kx_first(d, q) : 0);  // kx slab (NS == 1: 0)
   // 32-bit element indices (every buffer holds < 2^32 elements): an access costs one IMAD and
   // one IMAD.WIDE.U32 instead of a 64-bit multiply-add chain
   const unsigned xoff = ((unsigned)(comp * d.nz + z) * d.ny) * d.P + kx;
@@ -147,7 +158,7 @@ __global__ void __launch_bounds__(ZCfg<L>::NT) k_conv(float2* __restrict__ Y, co
                                                       const float2* __restrict__ gtw) {
   using Cf = ZCfg<L>;
   constexpr int E = Cf::E, TL = Cf::TL, C = Cf::C;
-  extern __shared__ __align__(16) float2 sm[];
+  extern __shared__ __align__(128) float2 sm[];
   float2* tw = sm;
   pass_tw<L, E, Cf::NT>(tw, gtw);
   __syncthreads();
@@ -197,36 +208,54 @@ __global__ void __launch_bounds__(ZCfg<L>::NT) k_conv(float2* __restrict__ Y, co
 #ifndef MCQ_ZSE
 #define MCQ_ZSE 16  // points per thread per line in the component-sequential K-Z
 #endif
-template <int L>
+#ifndef MCQ_ZTAB
+#define MCQ_ZTAB 1  // plan twiddle table in K-Z (fewer registers: 64 vs 104)
+#endif
+#ifndef MCQ_ZPF
+#define MCQ_ZPF 1   // load component g+1 before transforming g (with ZTAB: 123.3 vs 127.3 us)
+#endif
+template <int L, int CW = 0>
 struct ZSCfg {
   static constexpr int E = L <= MCQ_ZSE ? L : MCQ_ZSE;
   static constexpr int TL = L / E;
   static constexpr int C0 = 256 / TL;
-  static constexpr int C = C0 < 4 ? 4 : (C0 > 64 ? 64 : C0);
+  static constexpr int C = CW > 0 ? CW : (C0 < 4 ? 4 : (C0 > 64 ? 64 : C0));
   static constexpr int NT = C * TL;
-  static constexpr int TWN = pass_twn<L, E>();
+  static constexpr int TWS = MCQ_ZTAB ? 0 : 1;
+  static constexpr int TWN = MCQ_ZTAB ? reg_tw_size<L, E>() : (L < 2 ? 2 : L);
   static constexpr size_t SMEM = (size_t)(TWN + 3 * L * C) * sizeof(float2);
 };
 
-template <int L, bool SPLIT>
-__global__ void __launch_bounds__(ZSCfg<L>::NT) k_zconv_seq(float2* __restrict__ Y, const float* __restrict__ khat,
-                                                            Dims d, const float2* __restrict__ gtw) {
-  using Cf = ZSCfg<L>;
+template <int L, bool SPLIT, int CW = 0>
+__global__ void __launch_bounds__(ZSCfg<L, CW>::NT) k_zconv_seq(float2* __restrict__ Y, const float* __restrict__ khat,
+                                                                Dims d, const float2* __restrict__ gtw, int nfull) {
+  using Cf = ZSCfg<L, CW>;
   constexpr int E = Cf::E, TL = Cf::TL, C = Cf::C;
-  extern __shared__ __align__(16) float2 sm[];
+  extern __shared__ __align__(128) float2 sm[];
   float2* tw = sm;
   float2* xch = sm + Cf::TWN;  // [3][L][C]
-  pass_tw<L, E, Cf::NT>(tw, gtw);
+  if constexpr (Cf::TWS == 0) {
+    reg_tw_build<L, E, Cf::NT>(tw, gtw);
+  } else {
+    for (int m = threadIdx.x; m < L; m += Cf::NT) tw[m] = gtw[m * (kTwMax / L)];
+  }
   __syncthreads();
   const int c = threadIdx.x % C, t = threadIdx.x / C;
   // columns kxl of this rank's kx slab (global kx = kx0 + kxl); z runs over all nzg planes,
   // held as [source rank r][c][zl][ky][KXS] with z = r * nz + zl (NS == 1: Y[c][z][ky][P])
-  const int kxl = blockIdx.x * C + c, ky = blockIdx.y, kx = d.kx0 + kxl;
-  const bool ok = kxl < d.KXS && kx < d.NKX;
+  // the first nlone CTAs are lone-column CTAs whose C lanes take C rows ky of this slab's last
+  // column (kxw = C * nfull + 1); the others are column tile (b % nfull) at row b / nfull
+  const int nlone = gridDim.x - nfull * d.Ly;
+  const bool lone = (int)blockIdx.x < nlone;
+  const int b = blockIdx.x - nlone;
+  const int kxl = lone ? d.kxw - 1 : (b % nfull) * C + c, kx = d.kx0 + kxl;
+  const int ky = lone ? blockIdx.x * C + c : b / nfull;
+  const bool ok = kxl < d.kxw && ky < d.Ly;
+  const int kyc = ky < d.Ly ? ky : d.Ly - 1;  // in-range row for address arithmetic
   const int nz = d.nzg, nzl = d.nz;
   // 32-bit element indices (Y holds < 2^32 elements)
   const unsigned row = d.KXS, plane = (unsigned)d.Ly * row;
-  const unsigned cbase = (unsigned)ky * row + kxl;
+  const unsigned cbase = (unsigned)kyc * row + kxl;
   // ((r * 3 + g) * nzl + z - r * nzl) planes = g * nzl + z + 2 nzl r with r = z / nzl (SPLIT
   // only: the single-slab instance keeps the plain strength-reduced addressing)
   const unsigned cstr = (unsigned)nzl * plane;
@@ -242,16 +271,37 @@ __global__ void __launch_bounds__(ZSCfg<L>::NT) k_zconv_seq(float2* __restrict__
     int g, c;
     __device__ __forceinline__ int operator()(int, int pos) const { return (g * L + pos) * C + c; }
   };
+  constexpr int EH = E / 2 > 0 ? E / 2 : 1;  // a thread's nonzero inputs (nz <= L/2)
+  float2 pf[EH];
+  if constexpr (MCQ_ZPF) {
+#pragma unroll
+    for (int i = 0; i < EH; ++i) {
+      const int p = t + TL * i;
+      pf[i] = (ok && p < nz) ? Y[zaddr(0, p)] : make_float2(0.f, 0.f);
+    }
+  }
 #pragma unroll 1
   for (int g = 0; g < 3; ++g) {
     float2 v[1][E];
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       const int p = t + TL * i;
-      v[0][i] = (2 * i < E && ok && p < nz) ? Y[zaddr(g, p)] : make_float2(0.f, 0.f);  // nz <= L/2
+      if constexpr (MCQ_ZPF)
+        v[0][i] = 2 * i < E ? pf[i < EH ? i : 0] : make_float2(0.f, 0.f);
+      else
+        v[0][i] = (2 * i < E && ok && p < nz) ? Y[zaddr(g, p)] : make_float2(0.f, 0.f);
+    }
+    if constexpr (MCQ_ZPF) {
+      if (g < 2) {
+#pragma unroll
+        for (int i = 0; i < EH; ++i) {
+          const int p = t + TL * i;
+          pf[i] = (ok && p < nz) ? Y[zaddr(g + 1, p)] : make_float2(0.f, 0.f);
+        }
+      }
     }
     const GA A{g, c};
-    reg_fft<L, E, 1, false, PASS_TWS>(v, xch, A, tw, t);
+    reg_fft<L, E, 1, false, Cf::TWS>(v, xch, A, tw, t);
 #pragma unroll
     for (int i = 0; i < E; ++i) xch[A(0, t + TL * i)] = v[0][i];
   }
@@ -273,7 +323,7 @@ __global__ void __launch_bounds__(ZSCfg<L>::NT) k_zconv_seq(float2* __restrict__
 #pragma unroll
     for (int i = 0; i < E; ++i) v[0][i] = xch[A(0, t + TL * i)];
     __syncthreads();  // region g is read before its exchanges overwrite it
-    reg_fft<L, E, 1, true, PASS_TWS>(v, xch, A, tw, t);
+    reg_fft<L, E, 1, true, Cf::TWS>(v, xch, A, tw, t);
     if (ok) {
 #pragma unroll
       for (int i = 0; i < E; ++i) {
@@ -391,41 +441,56 @@ __global__ void __launch_bounds__(ZTCfg<L>::NT, MINB) k_zconv_tma(const __grid_c
     default: break;                                            \
   }
 
-void launch_yfwd(const Dims& d, const float2* X, float2* Y, const float2* tw, cudaStream_t st) {
+int launch_yfwd(const Dims& d, const float2* X, float2* Y, const float2* tw, cudaStream_t st) {
+  int n = 0;
   MCQ_DISPATCH_L(d.Ly, {
     using Cf = PassCfg<L>;
-    dim3 grid((d.NKX + Cf::C - 1) / Cf::C, d.nz, 3);
-    k_ypass<L, false><<<grid, Cf::NT, Cf::SMEM, st>>>(X, Y, d, tw);
+    // (lone-column CTAs as in K-Z measured slower here: 38.9 / 37.8 vs 37.8 / 35.6 us)
+    const int nfull = (d.NKX + Cf::C - 1) / Cf::C;
+    k_ypass<L, false><<<dim3(nfull * d.nz, 3), Cf::NT, Cf::SMEM, st>>>(X, Y, d, tw, nfull), ++n;
   })
+  return n;
 }
 
-void launch_yinv(const Dims& d, const float2* Y, float2* X, const float2* tw, cudaStream_t st) {
+int launch_yinv(const Dims& d, const float2* Y, float2* X, const float2* tw, cudaStream_t st) {
+  int n = 0;
   MCQ_DISPATCH_L(d.Ly, {
     using Cf = PassCfg<L>;
-    dim3 grid((d.NKX + Cf::C - 1) / Cf::C, d.nz, 3);
-    k_ypass<L, true><<<grid, Cf::NT, Cf::SMEM, st>>>(Y, X, d, tw);
+    // (lone-column CTAs as in K-Z measured slower here: 38.9 / 37.8 vs 37.8 / 35.6 us)
+    const int nfull = (d.NKX + Cf::C - 1) / Cf::C;
+    k_ypass<L, true><<<dim3(nfull * d.nz, 3), Cf::NT, Cf::SMEM, st>>>(Y, X, d, tw, nfull), ++n;
   })
+  return n;
 }
 
-void launch_zconv(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t st) {
+int launch_zconv(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t st) {
+  int n = 0;
   MCQ_DISPATCH_L(d.Lz, {
     using Cf = ZCfg<L>;
     dim3 grid((d.NKX + Cf::C - 1) / Cf::C, d.Ly);
-    k_conv<L, false><<<grid, Cf::NT, Cf::SMEM, st>>>(Y, khat, d, tw);
+    k_conv<L, false><<<grid, Cf::NT, Cf::SMEM, st>>>(Y, khat, d, tw), ++n;
   })
+  return n;
 }
 
-void launch_zconv_seq(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t st) {
+template <int L, bool SPLIT>
+static int zconv_seq_cols(const Dims& d, float2* Y, const float* khat, const float2* tw, int cols, cudaStream_t st) {
+  using Cf = ZSCfg<L>;
+  const bool lone = cols % Cf::C == 1 && cols > Cf::C;
+  const int nfull = lone ? cols / Cf::C : (cols + Cf::C - 1) / Cf::C;
+  const int nb = nfull * d.Ly + (lone ? (d.Ly + Cf::C - 1) / Cf::C : 0);
+  k_zconv_seq<L, SPLIT><<<nb, Cf::NT, Cf::SMEM, st>>>(Y, khat, d, tw, nfull);
+  return 1;
+}
+
+int launch_zconv_seq(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t st) {
+  const int cols = d.kxw;  // valid columns of this slab
+  if (cols <= 0) return 0;
+  int n = 0;
   MCQ_DISPATCH_L(d.Lz, {
-    using Cf = ZSCfg<L>;
-    const int cols = d.NKX - d.kx0 < d.KXS ? d.NKX - d.kx0 : d.KXS;  // valid columns of this slab
-    if (cols <= 0) return;
-    dim3 grid((cols + Cf::C - 1) / Cf::C, d.Ly);
-    if (d.NS > 1)
-      k_zconv_seq<L, true><<<grid, Cf::NT, Cf::SMEM, st>>>(Y, khat, d, tw);
-    else
-      k_zconv_seq<L, false><<<grid, Cf::NT, Cf::SMEM, st>>>(Y, khat, d, tw);
+    n = d.NS > 1 ? zconv_seq_cols<L, true>(d, Y, khat, tw, cols, st) : zconv_seq_cols<L, false>(d, Y, khat, tw, cols, st);
   })
+  return n;
 }
 
 int zconv_tma_box_c(int Lz) {
@@ -434,8 +499,9 @@ int zconv_tma_box_c(int Lz) {
   return c;
 }
 
-void launch_zconv_tma(const Dims& d, const void* tmap, float2* Y, const float* khat, const float2* tw,
-                      cudaStream_t st) {
+int launch_zconv_tma(const Dims& d, const void* tmap, float2* Y, const float* khat, const float2* tw,
+                     cudaStream_t st) {
+  int n = 0;
   static int nsm = 0;
   if (!nsm) {
     int dev = 0;
@@ -458,15 +524,19 @@ void launch_zconv_tma(const Dims& d, const void* tmap, float2* Y, const float* k
       k_zconv_tma<L, 3><<<grid, Cf::NT, Cf::SMEM, st>>>(tmr, Y, khat, d, tw, ntiles);
     else
       k_zconv_tma<L, 1><<<grid, Cf::NT, Cf::SMEM, st>>>(tmr, Y, khat, d, tw, ntiles);
+    n = 1;
   })
+  return n;
 }
 
-void launch_y2d(const Dims& d, float2* X, const float* khat, const float2* tw, cudaStream_t st) {
+int launch_y2d(const Dims& d, float2* X, const float* khat, const float2* tw, cudaStream_t st) {
+  int n = 0;
   MCQ_DISPATCH_L(d.Ly, {
     using Cf = ZCfg<L>;
     dim3 grid((d.NKX + Cf::C - 1) / Cf::C);
-    k_conv<L, true><<<grid, Cf::NT, Cf::SMEM, st>>>(X, khat, d, tw);
+    k_conv<L, true><<<grid, Cf::NT, Cf::SMEM, st>>>(X, khat, d, tw), ++n;
   })
+  return n;
 }
 
 // Opt every instantiation into the shared memory it needs (once per process).

@@ -23,6 +23,10 @@
 #ifndef MCQ_UE
 #define MCQ_UE 4   // packed row positions per thread in K-U (register budget: 4 beat 8 by 27%)
 #endif
+#ifndef MCQ_UROWS
+#define MCQ_UROWS 0  // stage the m_n / acc / B_rms rows by TMA too (measured slower: 91 vs 82 us,
+                     // the extra 18 KB per CTA costs a resident CTA per SM)
+#endif
 
 namespace mcq {
 
@@ -40,7 +44,9 @@ struct UCfg {
   static constexpr int TILE_C = 3 * (RY + 2) * N2;
   static constexpr int TILE_Z = 3 * RY * N2;
   static constexpr size_t XS_BYTES = (size_t)(2 * N2 + 3 * RY * PITCH) * sizeof(float2);
-  static constexpr size_t SMEM = XS_BYTES + (size_t)(TILE_C + 2 * TILE_Z) * sizeof(float);
+  // + the CTA's rows of m_n, the RK4 accumulator and the B_rms map ([3][RY][nx] each, TMA path),
+  // so every HBM read of the kernel is in flight while phase A runs
+  static constexpr size_t SMEM = XS_BYTES + (size_t)(TILE_C + (MCQ_UROWS ? 5 : 2) * TILE_Z) * sizeof(float);
 };
 
 __device__ __forceinline__ float3 cross3(float3 a, float3 b) {
@@ -185,6 +191,9 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
   float* tc = reinterpret_cast<float*>(reinterpret_cast<char*>(sm) + Cf::XS_BYTES);  // [3][RY+2][nx]
   float* tzm = tc + Cf::TILE_C;                                                       // [3][RY][nx]
   float* tzp = tzm + Cf::TILE_Z;
+  float* tmn = tzp + Cf::TILE_Z;  // [3][RY][nx]: m_n, acc, B_rms rows (TMA path)
+  float* tap = tmn + Cf::TILE_Z;
+  float* tbr = tap + Cf::TILE_Z;
   __shared__ __align__(8) uint64_t bars[2];
   __shared__ double red[32];
   __shared__ float redf[32];
@@ -201,16 +210,19 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
   const int csc = (RY + 2) * nxp, csz = RY * nxp;                    // component pitches of the tiles
   const bool use_demag = a.demag && (a.terms & MCQ_TERM_DEMAG) && a.mode != MODE_X0;
   const bool tma = (nx & 3) == 0 && (d.P & 1) == 0;
+  const bool trows = tma && MCQ_UROWS;
+  const bool st_mode = a.mode == MODE_LLG || a.mode == MODE_RELAX;
+  const bool ld_mn = trows && st_mode && a.stage > 1;  // m_n and the accumulator: stages 2-4
+  const bool ld_br = trows && a.brms && (a.mode == MODE_LLG || a.mode == MODE_FIELD);
 
   // ---------------- 0: TMA staging (bars[0]: X rows, bars[1]: m_s tile) ----------------
-  if (threadIdx.x == 0 && tma) {
+  // thread 0 initialises the barriers and issues every copy at once, so the copies' latency
+  // overlaps the twiddle-table load below; the other threads see the initialised barriers
+  // after the __syncthreads and only then wait on them
+  if (tma && threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     fence_mbar_init();
-  }
-  for (int m = threadIdx.x; m < LX; m += NT) tw[m] = gtw[m * (kTwMax / LX)];
-  __syncthreads();
-  if (tma && threadIdx.x == 0) {
     if (use_demag) {
       const uint32_t bx = (uint32_t)(N2 + 2) * 8;  // N2+1 columns rounded to 16 bytes (<= PITCH)
       mbar_arrive_expect_tx(&bars[0], 3u * nrow * bx);
@@ -219,14 +231,23 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
           tma_load_1d(xs + (c * RY + r) * PITCH, a.X + ((size_t)(c * nz + z) * ny + y0 + r) * d.P, bx, &bars[0]);
     }
     const uint32_t bc = (uint32_t)(yhi - ylo + 1) * nx * 4, bz = (uint32_t)nrow * nx * 4;
-    mbar_arrive_expect_tx(&bars[1], 3 * (bc + (zlo ? bz : 0) + (zhi ? bz : 0)));
+    mbar_arrive_expect_tx(&bars[1], 3 * (bc + (zlo ? bz : 0) + (zhi ? bz : 0) + (ld_mn ? 2 * bz : 0) +
+                                         (ld_br ? bz : 0)));
+    const long long rows = ((long long)zs * ny + y0) * nx;  // the CTA's rows at z (contiguous)
     for (int c = 0; c < 3; ++c) {
       const float* src = a.mS + c * N;
       tma_load_1d(tc + c * csc + (ylo - (y0 - 1)) * nx, src + ((long long)zs * ny + ylo) * nx, bc, &bars[1]);
       if (zlo) tma_load_1d(tzm + c * csz, src + ((long long)(zs - 1) * ny + y0) * nx, bz, &bars[1]);
       if (zhi) tma_load_1d(tzp + c * csz, src + ((long long)(zs + 1) * ny + y0) * nx, bz, &bars[1]);
+      if (ld_mn) {
+        tma_load_1d(tmn + c * csz, a.mN + c * N + rows, bz, &bars[1]);
+        tma_load_1d(tap + c * csz, a.acc + c * N + rows, bz, &bars[1]);
+      }
+      if (ld_br) tma_load_1d(tbr + c * csz, a.brms + c * N + rows, bz, &bars[1]);
     }
   }
+  for (int m = threadIdx.x; m < LX; m += NT) tw[m] = gtw[m * (kTwMax / LX)];
+  __syncthreads();
   if (!tma) {  // fallback (unaligned rows): cooperative coalesced loads into the same layout
     for (int c = 0; c < 3; ++c) {
       if (use_demag)
@@ -324,9 +345,10 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
         zp[c] = zhi ? sm_pair(tzp + c * csz + yl * nxp + x0) : mc[c];
         xl[c] = x0 > 0 ? r[x0 - 1] : 0.f;
         xr[c] = x0 + 2 < nx ? r[x0 + 2] : 0.f;
-        mn2[c] = need_mn ? ld_pair(a.mN, c * Nu + idx, vec, two) : make_float2(0.f, 0.f);
-        ap2[c] = need_acc ? ld_pair(a.acc, c * Nu + idx, vec, two) : make_float2(0.f, 0.f);
-        br2[c] = need_br ? ld_pair(a.brms, c * Nu + idx, vec, two)
+        const int so = c * csz + yl * nxp + x0;  // staged rows (TMA path)
+        mn2[c] = need_mn ? (trows ? sm_pair(tmn + so) : ld_pair(a.mN, c * Nu + idx, vec, two)) : make_float2(0.f, 0.f);
+        ap2[c] = need_acc ? (trows ? sm_pair(tap + so) : ld_pair(a.acc, c * Nu + idx, vec, two)) : make_float2(0.f, 0.f);
+        br2[c] = need_br ? (trows ? sm_pair(tbr + so) : ld_pair(a.brms, c * Nu + idx, vec, two))
                          : make_float2(a.brms_u[c], a.brms_u[c]);
       }
       float2 acc2[3], bf2[3];

@@ -32,6 +32,7 @@ CASES = [
     ("sphere", (16, 16, 16), CUBIC),
     ("disc", (48, 40, 3), UNI),
     ("sphere", (30, 18, 5), None),
+    ("disc", (40, 72, 3), UNI),      # NKX = 65 = 4 full 16-column tiles + a 1-column tile
 ]
 
 

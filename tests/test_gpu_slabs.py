@@ -30,6 +30,8 @@ CASES = [
     ("sphere", (30, 18, 6), CUBIC, (2, 3, 6)),
     ("disc", (32, 32, 2), None, (2,)),
     ("film", (64, 24, 16), None, (4, 16)),
+    ("film", (2, 8, 4), None, (2, 4)),          # NKX = 3 < world: empty kx slabs
+    ("disc", (40, 72, 6), None, (3, 6)),        # NKX = 65 split 16/16/33 and 8-column blocks
 ]
 
 
