@@ -3,6 +3,12 @@
 Follows SURVEY §8(c) "Oracle algorithm": field B'(m, t) (step 3), torque (4), RK4 (5),
 memory update after the step on the new state (6), relax (7).  Inputs come in as the
 CUDA path receives them (fp32 m, B_rms), widened to fp64.
+
+Multimode (P:24 runs each mode separately and calls a native multimode
+cavity "straightforward"): reading C-MM — every extra mode k is its own damped oscillator with
+its own B_rms,k, f_k, kappa_k, x0_k, p0_k and excitation; it is driven by its own overlap
+W_k = sum_i M_s m_i . B_rms,k(r_i) through the same recursion, and the field gains
+a_k sinc(w_k t) B_rms,k + B_rms,k Gamma_k(t).  The modes couple only through m.
 """
 from __future__ import annotations
 
@@ -25,7 +31,7 @@ class Simulation:
     def __init__(self, grid, cell, Ms, Aex, alpha, m0, mask=None, bext=(0.0, 0.0, 0.0),
                  brms_map=None, brms_uniform=(0.0, 0.0, 0.0), f_c=1e9, kappa=0.0, x0=0.0, p0=0.0,
                  exc_amp=0.0, exc_omega=0.0, aniso=None, demag="auto", octant=None, hbar=HBAR,
-                 gamma=GAMMA, terms=ALL):
+                 gamma=GAMMA, terms=ALL, modes=()):
         self.grid = tuple(int(g) for g in grid)
         nx, ny, nz = self.grid
         self.shape = (nz, ny, nx)
@@ -44,6 +50,17 @@ class Simulation:
         self.aniso = aniso or {}
         self.exc_amp, self.exc_omega = float(exc_amp), float(exc_omega)
         self.mem = CavityMemory(2 * math.pi * f_c, kappa, x0, p0, self.vcell, hbar)
+        # extra modes k >= 1 (reading C-MM): dicts with brms_map | brms_uniform, f_c, kappa,
+        # x0, p0, exc_amp, exc_omega
+        self.extra = []
+        for md in modes:
+            if md.get("brms_map") is not None:
+                b = np.asarray(md["brms_map"], dtype=np.float64).reshape(self.shape + (3,))
+            else:
+                b = F.zeeman(self.shape, md.get("brms_uniform", (0.0, 0.0, 0.0)))
+            mem = CavityMemory(2 * math.pi * md.get("f_c", 1e9), md.get("kappa", 0.0), md.get("x0", 0.0),
+                               md.get("p0", 0.0), self.vcell, hbar)
+            self.extra.append((b, mem, float(md.get("exc_amp", 0.0)), float(md.get("exc_omega", 0.0))))
         n = nx * ny * nz
         self.demag_mode = ("brute" if n <= 4096 else "dft") if demag == "auto" else demag
         self._octant = octant
@@ -93,6 +110,11 @@ class Simulation:
             B += self.exc_amp * float(F.sinc(self.exc_omega * t)) * self.brms
         if terms & CAVITY and self.cavity_enabled:
             B += self.brms * self.mem.gamma(t)
+        for b, mem, a_k, w_k in self.extra:          # modes k >= 1, in order (C-MM)
+            if terms & EXCITATION and a_k != 0.0:
+                B += a_k * float(F.sinc(w_k * t)) * b
+            if terms & CAVITY and np.any(b != 0):
+                B += b * mem.gamma(t)
         return np.where(self.mag[..., None], B, 0.0)
 
     def W(self, m):
@@ -107,6 +129,9 @@ class Simulation:
         self.m = rk4_step(self.rhs, self.m, self.mem.t, dt)
         W = self.W(self.m) if self.cavity_enabled else 0.0
         self.mem.update(W, dt)
+        for b, mem, _, _ in self.extra:              # every mode advances on its own overlap
+            Wk = float(np.sum(self.Ms * np.sum(self.m * b, axis=-1) * self.mag)) if np.any(b != 0) else 0.0
+            mem.update(Wk, dt)
 
     def run(self, dt, steps):
         for _ in range(int(steps)):
@@ -136,11 +161,13 @@ class Simulation:
             steps += k
             if self.max_torque() < tol:
                 break
-        self.mem.reset()
+        self.reset_memory()
         return steps
 
     def reset_memory(self):
         self.mem.reset()
+        for _, mem, _, _ in self.extra:
+            mem.reset()
 
     # ---------------------------------------------------------------- diagnostics (pins)
     def energy(self, m=None):
