@@ -28,6 +28,16 @@ sys.path.insert(0, ROOT)
 METRIC = "LLG cell-updates/sec & % HBM roofline at 1/2/4/8 B200"
 
 
+def ncu_traffic(config, kernel):
+    """Per-launch DRAM bytes of `kernel` from the committed ncu capture (tools/ncu_traffic.py), or
+    None; the file names the report it came from."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[f"config{config}"]
+        return d.get(kernel), d.get("_source")
+    except Exception:
+        return None, None
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -259,6 +269,7 @@ def main():
     pk = peaks()
     achieved = ab[top] / (prof[top][0] * 1e-3) / 1e9
     step_bytes = step_alg_bytes(L, cfg.grid, cfg.brms_map is not None, ns)
+    traffic, traffic_src = ncu_traffic(args.config, top) if (world == 1 and args.loopback <= 1) else (None, None)
     ms_step = ms_max / args.steps
 
     if rank == 0:
@@ -274,7 +285,9 @@ def main():
                        "l2": "working set > 126 MB L2 every step (no flush needed)",
                        "padded_fft": [L["Lx"], L["Ly"], L["Lz"]]},
             "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": pk["hbm_gbs"],
-                         "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                         "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
+                         "traffic_source": (f"profiles/{traffic_src} (ncu --set full, dram bytes read+write per launch)"
+                                            if traffic_src else None),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("_fallback") else "fallback",
                          "alg_bytes_per_launch": ab[top], "ms_per_launch": prof[top][0]},
             "step_roofline": {"alg_bytes_per_step": step_bytes, "achieved_gbs": step_bytes / (ms_step * 1e-3) / 1e9,

@@ -182,6 +182,22 @@ MCQ_API int mcq_cavity_status(const mcq_ctx *);
 /* Number of library kernels launched so far (graph replays count every kernel node). */
 MCQ_API long long mcq_kernel_launches(const mcq_ctx *);
 
+/* On-device trace of the per-step observables (the spectra of P:172 are
+ * the numerical FT of the spatially averaged m).  After every `every`-th completed LLG step the
+ * cavity kernel appends one row of MCQ_TRACE_COLS doubles:
+ *     t_{n+1} (s), <m_x>, <m_y>, <m_z> (mean over magnetic cells, from the same fixed-order
+ *     per-CTA fp64 partials as W), Re alpha, Im alpha, W (A/m T), n+1
+ * into a device buffer of `capacity` rows (0 disables; rows beyond the capacity are counted but
+ * not stored).  No host synchronisation per step.  The row count restarts on every reset of the
+ * cavity memory (mcq_reset_memory, mcq_set_brms, mcq_set_cavity, mcq_relax) and here.
+ * EINVAL: capacity < 0 or > 2^28, every < 1; ENOMEM. */
+#define MCQ_TRACE_COLS 8
+MCQ_API int mcq_set_trace(mcq_ctx *, long long capacity, int every);
+/* Copies min(stored, max_rows) rows (row-major, MCQ_TRACE_COLS doubles each) to the host array
+ * out, stored = min(rows recorded since the last reset, capacity); *rows (may be NULL) receives
+ * stored.  max_rows = 0 with out = NULL queries the count. */
+MCQ_API int mcq_get_trace(mcq_ctx *, double *out, long long max_rows, long long *rows);
+
 /* Measurement hook: runs `steps` steps with CUDA events around every kernel (no graph) and
  * writes the mean device time (ms) per launch of each MCQ_K_* class to kernel_ms[MCQ_NKCLASS]
  * (0 for classes not launched) and launches per step to per_step[MCQ_NKCLASS] (may be NULL). */

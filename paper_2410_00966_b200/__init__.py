@@ -172,6 +172,27 @@ def mcq_cavity_status(ctx):
     return rc
 
 
+TRACE_COLS = ("t", "mx", "my", "mz", "re_alpha", "im_alpha", "W", "step")
+
+
+def mcq_set_trace(ctx, capacity, every=1):
+    """Record the per-step observables on the device (include/mcq.h, NEXT-3)."""
+    _check(ctx, lib.mcq_set_trace(ctx, int(capacity), int(every)))
+
+
+def mcq_get_trace(ctx, max_rows=None):
+    """Recorded trace rows as an (n, 8) float64 array, columns TRACE_COLS."""
+    n = C.c_longlong()
+    _check(ctx, lib.mcq_get_trace(ctx, None, 0, C.byref(n)))
+    rows = n.value if max_rows is None else min(n.value, int(max_rows))
+    out = np.zeros((max(rows, 0), len(TRACE_COLS)), np.float64)
+    got = C.c_longlong()
+    if rows > 0:
+        _check(ctx, lib.mcq_get_trace(ctx, out.ctypes.data, rows, C.byref(got)))
+        out = out[:min(rows, got.value)]
+    return out
+
+
 def mcq_kernel_launches(ctx):
     return int(lib.mcq_kernel_launches(ctx))
 
@@ -256,6 +277,13 @@ class Solver:
 
     def cavity(self):
         return mcq_get_cavity(self.ctx)
+
+    def trace(self, capacity=None, every=1):
+        """trace(capacity): start recording; trace(): the rows recorded so far."""
+        if capacity is not None:
+            mcq_set_trace(self.ctx, capacity, every)
+            return None
+        return mcq_get_trace(self.ctx)
 
     def sync(self):
         mcq_synchronize(self.ctx)

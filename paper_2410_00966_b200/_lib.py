@@ -73,6 +73,8 @@ _sig = {
     "mcq_set_cavity_state": (C.c_int, [_P, C.POINTER(mcq_cavity_state)]),
     "mcq_cavity_status": (C.c_int, [_P]),
     "mcq_kernel_launches": (C.c_longlong, [_P]),
+    "mcq_set_trace": (C.c_int, [_P, C.c_longlong, C.c_int]),
+    "mcq_get_trace": (C.c_int, [_P, _P, C.c_longlong, C.POINTER(C.c_longlong)]),
     "mcq_profile_run": (C.c_int, [_P, C.c_double, C.c_longlong, C.POINTER(C.c_double), C.POINTER(C.c_int)]),
     "mcq_debug_layout": (C.c_int, [_P, C.POINTER(C.c_longlong)]),
     "mcq_debug_tensor_octant": (C.c_int, [_P, _P]),

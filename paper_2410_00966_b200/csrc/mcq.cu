@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -112,8 +113,12 @@ struct mcq_ctx {
   double bext[3] = {0, 0, 0};
   double fc = 1e9, kappa = 0, x0 = 0, p0 = 0, exc_amp = 0, exc_omega = 0;
   CavState* cav = nullptr;
-  double* partials = nullptr;  // all slabs' per-CTA overlap partials in global z order
-  int nparts = 0;
+  double* partials = nullptr;  // all slabs' per-CTA partials [CTA][kNPart] in global z order
+  int nparts = 0;              // CTAs of one stage-4 update (all slabs)
+  double* trace = nullptr;     // NEXT-3 observables [trace_cap][kTraceCols]
+  long long trace_cap = 0;
+  int trace_every = 1;
+  long long n_magnetic = 0;
   unsigned* maxbits = nullptr;
   int* bad = nullptr;
   float* io = nullptr;  // AoS staging for the cells this context holds
@@ -133,6 +138,7 @@ struct mcq_ctx {
 namespace {
 
 constexpr int kGraphSteps = 8;
+constexpr long long kPdlMaxCells = 1 << 16;  // PDL only where the step is launch-latency bound
 constexpr int kRelaxCheck = 50;
 
 int fail(mcq_ctx* c, int code, const std::string& msg) {
@@ -184,6 +190,11 @@ CavParams cav_params(const mcq_ctx* c, double dt) {
   p.exc_amp = c->exc_amp;
   p.exc_omega = c->exc_omega;
   p.cav_on = c->cav_on ? 1 : 0;
+  p.trace = c->trace_cap > 0 ? c->trace : nullptr;
+  p.trace_cap = c->trace_cap;
+  p.trace_every = c->trace_every;
+  p.inv_nmag = c->n_magnetic > 0 ? 1.0 / (double)c->n_magnetic : 0.0;
+  p.pdl = c->sl.empty() ? 0 : c->sl[0].d.pdl;
   return p;
 }
 
@@ -231,6 +242,7 @@ UpdateArgs base_args(const mcq_ctx* c, const Slab& s) {
   a.X = s.X;
   a.acc = s.acc;
   a.demag = 1;
+  a.trace = c->trace_cap > 0 ? 1 : 0;
   return a;
 }
 
@@ -381,7 +393,7 @@ struct Enq {
   void gather_partials() {
     if (c->mode != 2) return;  // single / loopback: every slab already wrote into c->partials
     Slab& sl = c->sl[0];
-    nk(nccl_api()->allGather(sl.partials, c->partials, sl.nparts, ncclDouble, c->comm, s));
+    nk(nccl_api()->allGather(sl.partials, c->partials, (size_t)sl.nparts * kNPart, ncclDouble, c->comm, s));
   }
   void llg_step(double dt) {
     for (int st = 1; st <= 4; ++st) stage(st, dt, MODE_LLG, MCQ_TERM_ALL);
@@ -544,7 +556,7 @@ void free_all(mcq_ctx* c) {
     if (c->mode == 2 && s.partials) cudaFree(s.partials);
   }
   c->sl.clear();
-  void* ptrs[] = {c->tw, c->khat, c->cav, c->partials, c->maxbits, c->bad, c->io};
+  void* ptrs[] = {c->tw, c->khat, c->cav, c->partials, c->maxbits, c->bad, c->io, c->trace};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->comm) nccl_api()->commDestroy(c->comm);
@@ -660,12 +672,14 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
   g.zg0 = 0;
   g.zoff = 0;
   g.cs = g.N;
+  c->n_magnetic = g.N;
   g.NS = 1;
   g.KXS = g.P;
   g.kx0 = 0;
   g.kxw = g.NKX;
   g.KG = 16;
   g.KB = g.NKX / 16;
+  g.pdl = 0;
   auto bail = [&](int code) {
     free_all(c);
     delete c;
@@ -725,12 +739,13 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
     s.d.KB = split.KB;
     s.d.kx0 = kx_first(split, r);
     s.d.kxw = kx_first(split, r + 1) - s.d.kx0;
+    s.d.pdl = (c->mode == 0 && g.N <= kPdlMaxCells) ? 1 : 0;  // see common.cuh
     s.nparts = update_grid_blocks(s.d);
     if (alloc_slab(c, s) != MCQ_OK) return bail(MCQ_ENOMEM);
   }
   bool ok = cudaMalloc(&c->khat, 6ULL * (g.Lz / 2 + 1) * (g.Ly / 2 + 1) * g.P * 4) == cudaSuccess &&
             cudaMalloc(&c->tw, kTwMax * 8) == cudaSuccess && cudaMalloc(&c->cav, sizeof(CavState)) == cudaSuccess &&
-            cudaMalloc(&c->partials, (size_t)c->nparts * 8) == cudaSuccess &&
+            cudaMalloc(&c->partials, (size_t)c->nparts * kNPart * 8) == cudaSuccess &&
             cudaMalloc(&c->maxbits, 4) == cudaSuccess && cudaMalloc(&c->bad, 4) == cudaSuccess &&
             cudaMalloc(&c->io, 3ULL * c->cells_here() * 4) == cudaSuccess;
   if (!ok) {
@@ -740,13 +755,13 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
   for (int i = 0; i < count; ++i) {
     Slab& s = c->sl[i];
     if (c->mode == 2) {
-      if (cudaMalloc(&s.partials, (size_t)s.nparts * 8) != cudaSuccess) return bail(MCQ_ENOMEM);
+      if (cudaMalloc(&s.partials, (size_t)s.nparts * kNPart * 8) != cudaSuccess) return bail(MCQ_ENOMEM);
     } else {
-      s.partials = c->partials + (size_t)i * s.nparts;  // global z order = slab order
+      s.partials = c->partials + (size_t)i * s.nparts * kNPart;  // global z order = slab order
     }
   }
   if (cudaMemsetAsync(c->khat, 0, 6ULL * (g.Lz / 2 + 1) * (g.Ly / 2 + 1) * g.P * 4, c->stream) != cudaSuccess ||
-      cudaMemsetAsync(c->partials, 0, (size_t)c->nparts * 8, c->stream) != cudaSuccess ||
+      cudaMemsetAsync(c->partials, 0, (size_t)c->nparts * kNPart * 8, c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->maxbits, 0, 4, c->stream) != cudaSuccess)
     return bail(MCQ_ECUDA);
   // twiddles w_1024^m = exp(-2 pi i m / 1024), generated in fp64
@@ -769,7 +784,8 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
       q.alltoall(true);
       q.alltoall(false);
     }
-    q.nk(nccl_api()->allGather(c->sl[0].partials, c->partials, c->sl[0].nparts, ncclDouble, c->comm, c->stream));
+    q.nk(nccl_api()->allGather(c->sl[0].partials, c->partials, (size_t)c->sl[0].nparts * kNPart, ncclDouble, c->comm,
+                               c->stream));
     q.nk(nccl_api()->allReduce(c->maxbits, c->maxbits, 1, ncclFloat, ncclMax, c->comm, c->stream));
     if (q.rc != MCQ_OK || cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(MCQ_ENCCL);
   }
@@ -790,13 +806,20 @@ static long long slab_cell0(const mcq_ctx* c, int i) { return (long long)c->sl[i
 
 int mcq_set_geometry(mcq_ctx* c, const unsigned char* mask) {
   if (!c) return MCQ_EINVAL;
+  invalidate_graphs(c);  // the trace's mean uses the magnetic cell count
   if (!mask) {
     for (auto& s : c->sl) {
       if (s.mask) cudaFree(s.mask);
       s.mask = nullptr;
     }
     c->have_mask = false;
+    c->n_magnetic = c->dg.N;
     return MCQ_OK;
+  }
+  {
+    long long nm = 0;
+    for (long long i = 0; i < c->dg.N; ++i) nm += mask[i] != 0;
+    c->n_magnetic = nm;
   }
   for (int i = 0; i < (int)c->sl.size(); ++i) {
     Slab& s = c->sl[i];
@@ -1074,6 +1097,42 @@ int mcq_set_cavity_state(mcq_ctx* c, const mcq_cavity_state* in) {
 int mcq_cavity_status(const mcq_ctx* c) {
   if (!c) return MCQ_EINVAL;
   return c->cav_on ? 1 : 0;
+}
+
+int mcq_set_trace(mcq_ctx* c, long long capacity, int every) {
+  if (!c) return MCQ_EINVAL;
+  if (capacity < 0 || capacity > (1LL << 28) || every < 1) return fail(c, MCQ_EINVAL, "trace: 0 <= capacity <= 2^28, every >= 1");
+  CK(c, cudaStreamSynchronize(c->stream));
+  if (c->trace) cudaFree(c->trace);
+  c->trace = nullptr;
+  c->trace_cap = 0;
+  if (capacity > 0) {
+    CK(c, cudaMalloc(&c->trace, (size_t)capacity * kTraceCols * 8));
+    CK(c, cudaMemsetAsync(c->trace, 0, (size_t)capacity * kTraceCols * 8, c->stream));
+  }
+  c->trace_cap = capacity;
+  c->trace_every = every;
+  const long long zero = 0;
+  CK(c, cudaMemcpyAsync(reinterpret_cast<char*>(c->cav) + offsetof(CavState, trace_rows), &zero, sizeof(zero),
+                        cudaMemcpyHostToDevice, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  invalidate_graphs(c);
+  return MCQ_OK;
+}
+
+int mcq_get_trace(mcq_ctx* c, double* out, long long max_rows, long long* rows) {
+  if (!c || (!out && max_rows > 0) || max_rows < 0) return MCQ_EINVAL;
+  CavState h{};
+  CK(c, cudaMemcpyAsync(&h, c->cav, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  const long long stored = std::min(h.trace_rows, c->trace_cap);
+  const long long n = std::min(stored, max_rows);
+  if (n > 0) {
+    CK(c, cudaMemcpyAsync(out, c->trace, (size_t)n * kTraceCols * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+  }
+  if (rows) *rows = stored;
+  return MCQ_OK;
 }
 
 long long mcq_kernel_launches(const mcq_ctx* c) { return c ? c->launches : -1; }

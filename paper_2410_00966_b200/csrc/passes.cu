@@ -84,8 +84,10 @@ __global__ void __launch_bounds__(PassCfg<L, CW>::NT) k_ypass(const float2* __re
   constexpr int E = Cf::E, TL = Cf::TL, C = Cf::C;
   extern __shared__ __align__(128) float2 sm[];
   float2* tw = sm;  // plan twiddles
+  pdl_trigger();
   pass_tw<L, E, Cf::NT>(tw, gtw);
   __syncthreads();
+  pdl_wait();
   const int c = threadIdx.x % C, t = threadIdx.x / C;
   // the first nlone CTAs are "lone column" CTAs whose C lanes take C planes of the last column
   // (NKX = C * nfull + 1), so that column costs nz / C CTAs instead of nz mostly idle ones
@@ -160,8 +162,10 @@ __global__ void __launch_bounds__(ZCfg<L>::NT) k_conv(float2* __restrict__ Y, co
   constexpr int E = Cf::E, TL = Cf::TL, C = Cf::C;
   extern __shared__ __align__(128) float2 sm[];
   float2* tw = sm;
+  pdl_trigger();
   pass_tw<L, E, Cf::NT>(tw, gtw);
   __syncthreads();
+  pdl_wait();
   const int c = threadIdx.x % C, t = threadIdx.x / C;
   const int kx = blockIdx.x * C + c, ky = Y2D ? 0 : blockIdx.y;
   const bool ok = kx < d.NKX;
@@ -234,12 +238,14 @@ __global__ void __launch_bounds__(ZSCfg<L, CW>::NT) k_zconv_seq(float2* __restri
   extern __shared__ __align__(128) float2 sm[];
   float2* tw = sm;
   float2* xch = sm + Cf::TWN;  // [3][L][C]
+  pdl_trigger();
   if constexpr (Cf::TWS == 0) {
     reg_tw_build<L, E, Cf::NT>(tw, gtw);
   } else {
     for (int m = threadIdx.x; m < L; m += Cf::NT) tw[m] = gtw[m * (kTwMax / L)];
   }
   __syncthreads();
+  pdl_wait();
   const int c = threadIdx.x % C, t = threadIdx.x / C;
   // columns kxl of this rank's kx slab (global kx = kx0 + kxl); z runs over all nzg planes,
   // held as [source rank r][c][zl][ky][KXS] with z = r * nz + zl (NS == 1: Y[c][z][ky][P])
@@ -374,8 +380,10 @@ __global__ void __launch_bounds__(ZTCfg<L>::NT, MINB) k_zconv_tma(const __grid_c
     mbar_init(&bar[1], 1);
     fence_mbar_init();
   }
+  pdl_trigger();
   pass_tw<L, E, Cf::NT>(tw, gtw);
   __syncthreads();
+  pdl_wait();
   auto issue = [&](int tile, int b) {
     const int kx0 = (tile % nkt) * C, ky = tile / nkt;
     mbar_arrive_expect_tx(&bar[b], box_bytes);
@@ -447,7 +455,7 @@ int launch_yfwd(const Dims& d, const float2* X, float2* Y, const float2* tw, cud
     using Cf = PassCfg<L>;
     // (lone-column CTAs as in K-Z measured slower here: 38.9 / 37.8 vs 37.8 / 35.6 us)
     const int nfull = (d.NKX + Cf::C - 1) / Cf::C;
-    k_ypass<L, false><<<dim3(nfull * d.nz, 3), Cf::NT, Cf::SMEM, st>>>(X, Y, d, tw, nfull), ++n;
+    launch_pdl(d.pdl, k_ypass<L, false>, dim3(nfull * d.nz, 3), dim3(Cf::NT), Cf::SMEM, st, X, Y, d, tw, nfull), ++n;
   })
   return n;
 }
@@ -458,7 +466,7 @@ int launch_yinv(const Dims& d, const float2* Y, float2* X, const float2* tw, cud
     using Cf = PassCfg<L>;
     // (lone-column CTAs as in K-Z measured slower here: 38.9 / 37.8 vs 37.8 / 35.6 us)
     const int nfull = (d.NKX + Cf::C - 1) / Cf::C;
-    k_ypass<L, true><<<dim3(nfull * d.nz, 3), Cf::NT, Cf::SMEM, st>>>(Y, X, d, tw, nfull), ++n;
+    launch_pdl(d.pdl, k_ypass<L, true>, dim3(nfull * d.nz, 3), dim3(Cf::NT), Cf::SMEM, st, Y, X, d, tw, nfull), ++n;
   })
   return n;
 }
@@ -468,7 +476,7 @@ int launch_zconv(const Dims& d, float2* Y, const float* khat, const float2* tw, 
   MCQ_DISPATCH_L(d.Lz, {
     using Cf = ZCfg<L>;
     dim3 grid((d.NKX + Cf::C - 1) / Cf::C, d.Ly);
-    k_conv<L, false><<<grid, Cf::NT, Cf::SMEM, st>>>(Y, khat, d, tw), ++n;
+    launch_pdl(d.pdl, k_conv<L, false>, grid, dim3(Cf::NT), Cf::SMEM, st, Y, khat, d, tw), ++n;
   })
   return n;
 }
@@ -479,7 +487,7 @@ static int zconv_seq_cols(const Dims& d, float2* Y, const float* khat, const flo
   const bool lone = cols % Cf::C == 1 && cols > Cf::C;
   const int nfull = lone ? cols / Cf::C : (cols + Cf::C - 1) / Cf::C;
   const int nb = nfull * d.Ly + (lone ? (d.Ly + Cf::C - 1) / Cf::C : 0);
-  k_zconv_seq<L, SPLIT><<<nb, Cf::NT, Cf::SMEM, st>>>(Y, khat, d, tw, nfull);
+  launch_pdl(d.pdl, k_zconv_seq<L, SPLIT>, dim3(nb), dim3(Cf::NT), Cf::SMEM, st, Y, khat, d, tw, nfull);
   return 1;
 }
 
@@ -521,9 +529,9 @@ int launch_zconv_tma(const Dims& d, const void* tmap, float2* Y, const float* kh
     const int grid = ntiles < cap ? ntiles : cap;
     const CUtensorMap& tmr = *reinterpret_cast<const CUtensorMap*>(tmap);
     if (v)
-      k_zconv_tma<L, 3><<<grid, Cf::NT, Cf::SMEM, st>>>(tmr, Y, khat, d, tw, ntiles);
+      launch_pdl(d.pdl, k_zconv_tma<L, 3>, dim3(grid), dim3(Cf::NT), Cf::SMEM, st, tmr, Y, khat, d, tw, ntiles);
     else
-      k_zconv_tma<L, 1><<<grid, Cf::NT, Cf::SMEM, st>>>(tmr, Y, khat, d, tw, ntiles);
+      launch_pdl(d.pdl, k_zconv_tma<L, 1>, dim3(grid), dim3(Cf::NT), Cf::SMEM, st, tmr, Y, khat, d, tw, ntiles);
     n = 1;
   })
   return n;
@@ -534,7 +542,7 @@ int launch_y2d(const Dims& d, float2* X, const float* khat, const float2* tw, cu
   MCQ_DISPATCH_L(d.Ly, {
     using Cf = ZCfg<L>;
     dim3 grid((d.NKX + Cf::C - 1) / Cf::C);
-    k_conv<L, true><<<grid, Cf::NT, Cf::SMEM, st>>>(X, khat, d, tw), ++n;
+    launch_pdl(d.pdl, k_conv<L, true>, grid, dim3(Cf::NT), Cf::SMEM, st, X, khat, d, tw), ++n;
   })
   return n;
 }

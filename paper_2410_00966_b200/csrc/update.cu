@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
   float* tap = tmn + Cf::TILE_Z;
   float* tbr = tap + Cf::TILE_Z;
   __shared__ __align__(8) uint64_t bars[2];
-  __shared__ double red[32];
+  __shared__ double red[32 * kNPart];
   __shared__ float redf[32];
 
   const Dims& d = a.d;
@@ -219,10 +219,12 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
   // thread 0 initialises the barriers and issues every copy at once, so the copies' latency
   // overlaps the twiddle-table load below; the other threads see the initialised barriers
   // after the __syncthreads and only then wait on them
+  pdl_trigger();
   if (tma && threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     fence_mbar_init();
+    pdl_wait();  // the copies read the previous kernels' output
     if (use_demag) {
       const uint32_t bx = (uint32_t)(N2 + 2) * 8;  // N2+1 columns rounded to 16 bytes (<= PITCH)
       mbar_arrive_expect_tx(&bars[0], 3u * nrow * bx);
@@ -247,6 +249,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
     }
   }
   for (int m = threadIdx.x; m < LX; m += NT) tw[m] = gtw[m * (kTwMax / LX)];
+  pdl_wait();
   __syncthreads();
   if (!tma) {  // fallback (unaligned rows): cooperative coalesced loads into the same layout
     for (int c = 0; c < 3; ++c) {
@@ -313,6 +316,8 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
   const float gsum = gc + ge;
   double wacc = 0.0;
   float tmax = 0.f;
+  float3 msum = make_float3(0.f, 0.f, 0.f);  // stage 4 with the trace on: sum of m_{n+1}
+  const bool tr = a.trace && a.mode == MODE_LLG && a.stage == 4;
   const unsigned rowbase = (unsigned)nx * (y + (unsigned)ny * zs);  // 32-bit indices (< 2^32 elements)
   const unsigned Nu = (unsigned)N;
   const float* trow = tc + (yl + 1) * nxp;  // this row inside the z tile
@@ -373,6 +378,11 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
 #undef MCQ_PICK
         float3 accn = make_float3(0.f, 0.f, 0.f), Bf = make_float3(0.f, 0.f, 0.f);
         const float3 out = cell_core(a, m, nb, ok, mn, ap, br, Bd, gsum, wacc, tmax, accn, Bf);
+        if (tr) {
+          msum.x += out.x;
+          msum.y += out.y;
+          msum.z += out.z;
+        }
         if (h) {
           o[0].y = out.x; o[1].y = out.y; o[2].y = out.z;
           acc2[0].y = accn.x; acc2[1].y = accn.y; acc2[2].y = accn.z;
@@ -407,14 +417,20 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
   // ---------------- reductions ----------------
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (NT + 31) / 32;
   if (a.mode == MODE_LLG && a.stage == 4) {
+    double q[kNPart] = {wacc, (double)msum.x, (double)msum.y, (double)msum.z};
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wacc += __shfl_down_sync(0xffffffffu, wacc, o);
-    if (lane == 0) red[warp] = wacc;
+    for (int k = 0; k < kNPart; ++k) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) q[k] += __shfl_down_sync(0xffffffffu, q[k], o);
+    }
+    if (lane == 0)
+#pragma unroll
+      for (int k = 0; k < kNPart; ++k) red[warp * kNPart + k] = q[k];
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < kNPart) {  // fixed order over the warps: deterministic
       double s = 0.0;
-      for (int w = 0; w < nw; ++w) s += red[w];
-      a.partials[blockIdx.y * gridDim.x + blockIdx.x] = s;
+      for (int w = 0; w < nw; ++w) s += red[w * kNPart + threadIdx.x];
+      a.partials[(blockIdx.y * gridDim.x + blockIdx.x) * kNPart + threadIdx.x] = s;
     }
   }
   if (a.mode == MODE_MAXTORQUE) {
@@ -490,7 +506,7 @@ void launch_update(const UpdateArgs& a, const float2* tw, cudaStream_t st) {
   MCQ_DISPATCH_N2(a.d.N2, {
     using Cf = UCfg<N2>;
     dim3 grid((a.d.ny + Cf::RY - 1) / Cf::RY, a.d.nz);
-    k_update<N2><<<grid, Cf::NT, Cf::SMEM, st>>>(a, tw);
+    launch_pdl(a.d.pdl, k_update<N2>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
   })
 }
 
@@ -526,17 +542,27 @@ __global__ void k_cav_prepare(CavParams p, CavState* st) {
 // alpha_{n+1} = e^{-(kappa + i w) dt} alpha_n + i (V_c/hbar) W_{n+1} dt, t += dt (a13).
 __global__ void __launch_bounds__(1024) k_cavity(CavParams p, CavState* st, const double* __restrict__ partials,
                                                  int n) {
-  __shared__ double red[1024];
-  double s = 0.0;
-  for (int i = threadIdx.x; i < n; i += 1024) s += partials[i];
-  red[threadIdx.x] = s;
+  __shared__ double red[kNPart][1024];
+  pdl_trigger();
+  pdl_wait();
+  const int nq = p.trace ? kNPart : 1;  // the spatial sums only when the trace records
+  double s[kNPart] = {0.0, 0.0, 0.0, 0.0};
+  for (int i = threadIdx.x; i < n; i += 1024)
+#pragma unroll
+    for (int k = 0; k < kNPart; ++k)
+      if (k < nq) s[k] += partials[i * kNPart + k];
+#pragma unroll
+  for (int k = 0; k < kNPart; ++k) red[k][threadIdx.x] = s[k];
   __syncthreads();
   for (int w = 512; w > 0; w >>= 1) {
-    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    if (threadIdx.x < w)
+#pragma unroll
+      for (int k = 0; k < kNPart; ++k)
+        if (k < nq) red[k][threadIdx.x] += red[k][threadIdx.x + w];
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    const double W = p.cav_on ? p.Ms * red[0] : 0.0;
+    const double W = p.cav_on ? p.Ms * red[0][0] : 0.0;
     const double er = p.ec_re[2], ei = p.ec_im[2];
     const double re = er * st->re - ei * st->im;
     const double im = er * st->im + ei * st->re + p.vc_over_hbar * W * p.dt;
@@ -545,12 +571,27 @@ __global__ void __launch_bounds__(1024) k_cavity(CavParams p, CavState* st, cons
     st->t += p.dt;
     st->W = W;
     st->step += 1;
+    if (p.trace && st->step % p.trace_every == 0) {  // NEXT-3: the per-step observables
+      const long long r = st->trace_rows;
+      if (r < p.trace_cap) {
+        double* row = p.trace + r * kTraceCols;
+        row[0] = st->t;
+        row[1] = red[1][0] * p.inv_nmag;
+        row[2] = red[2][0] * p.inv_nmag;
+        row[3] = red[3][0] * p.inv_nmag;
+        row[4] = re;
+        row[5] = im;
+        row[6] = p.Ms * red[0][0];
+        row[7] = (double)st->step;
+      }
+      st->trace_rows = r + 1;
+    }
     cav_prepare(p, st);
   }
 }
 
 void launch_cavity(const CavParams& p, CavState* st, const double* partials, int n, cudaStream_t s) {
-  k_cavity<<<1, 1024, 0, s>>>(p, st, partials, n);
+  launch_pdl(p.pdl, k_cavity, dim3(1), dim3(1024), 0, s, p, st, partials, n);
 }
 
 void launch_cav_prepare(const CavParams& p, CavState* st, cudaStream_t s) {

@@ -55,6 +55,7 @@ def test_binding_covers_header_and_constants(built):
     from oracle import sim as S
     assert (S.ZEEMAN, S.EXCHANGE, S.ANIS, S.DEMAG, S.CAVITY, S.EXCITATION) == (1, 2, 4, 8, 16, 32)
     assert d["MCQ_NKCLASS"] == mcq.NKCLASS
+    assert d["MCQ_TRACE_COLS"] == len(mcq.TRACE_COLS) == 8
     assert (d["MCQ_OK"], d["MCQ_EINVAL"], d["MCQ_ESTATE"]) == (0, -1, -2)
 
 

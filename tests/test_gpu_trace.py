@@ -1,0 +1,141 @@
+"""On-device trace of the per-step observables and the GPU physics checks
+it enables (north_star: "polariton spectrum peak frequencies and g must agree within 0.5%").
+
+* parity: the trace rows (t, <m>, alpha, W) equal the oracle's step-by-step values;
+* bookkeeping: every / capacity / reset semantics;
+* physics on the GPU path at grid scale: the Kittel frequency of a discretised sphere and the
+  vacuum Rabi splitting of the same sphere at resonance against the two-oscillator model with
+  g from the coupling law g = gamma B_rms sqrt(S/2), S = Ms V_magnet / (hbar gamma)."""
+import math
+
+import numpy as np
+import pytest
+
+from helpers import oracle_from
+from synth import small_config, sphere_mask, tilted_uniform
+from oracle import analytic as A
+from oracle.constants import GAMMA
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2410_00966_b200 as mcq  # noqa: E402
+
+
+def test_trace_rows_match_oracle():
+    cfg = small_config("sphere", (16, 12, 8), seed=5, state="phys")
+    s = mcq.Solver.from_config(cfg)
+    s.trace(200, every=1)
+    ref = oracle_from(cfg)
+    rows = []
+    for _ in range(60):
+        ref.step(cfg.dt)
+        a = ref.mem.alpha()
+        rows.append([ref.mem.t, *ref.mean_m(), a.real, a.imag, ref.mem.W])
+    s.run(cfg.dt, 60)
+    tr = s.trace()
+    rows = np.array(rows)
+    assert tr.shape == (60, 8)
+    assert np.array_equal(tr[:, 7], np.arange(1, 61))
+    assert np.allclose(tr[:, 0], rows[:, 0], rtol=1e-14, atol=0)
+    assert np.abs(tr[:, 1:4] - rows[:, 1:4]).max() < 1e-5      # spatial mean of unit vectors
+    amax = np.abs(rows[:, 4] + 1j * rows[:, 5]).max()
+    assert np.abs((tr[:, 4] + 1j * tr[:, 5]) - (rows[:, 4] + 1j * rows[:, 5])).max() < 1e-4 * amax
+    assert np.allclose(tr[:, 6], rows[:, 6], rtol=1e-4, atol=1e-6 * np.abs(rows[:, 6]).max())
+    # the last row is the cavity state the getter reports
+    cav = s.cavity()
+    assert (cav["re_alpha"], cav["im_alpha"], cav["W"]) == (tr[-1, 4], tr[-1, 5], tr[-1, 6])
+    s.close()
+
+
+def test_trace_every_capacity_reset():
+    cfg = small_config("film", (16, 16, 1), seed=6, state="phys")
+    s = mcq.Solver.from_config(cfg)
+    s.trace(5, every=3)
+    s.run(cfg.dt, 30)
+    n = mcq.TRACE_COLS
+    assert len(n) == 8
+    tr = s.trace()
+    assert tr.shape == (5, 8) and list(tr[:, 7]) == [3, 6, 9, 12, 15]
+    assert tr[:, 0] == pytest.approx(np.array([3, 6, 9, 12, 15]) * cfg.dt, rel=1e-13)
+    mcq.mcq_reset_memory(s.ctx)          # the cavity clock and the trace restart
+    s.run(cfg.dt, 6)
+    tr = s.trace()
+    assert list(tr[:, 7]) == [3, 6] and tr[0, 0] == pytest.approx(3 * cfg.dt, rel=1e-13)
+    s.trace(0)                            # off
+    s.run(cfg.dt, 3)
+    assert s.trace().shape == (0, 8)
+    s.close()
+
+
+# ---------------------------------------------------------------- physics on the GPU path
+
+YIG_MS, YIG_A = 1.4e5, 3.7e-12
+CELL = (7.8125e-9,) * 3
+
+
+def _sphere(grid=(16, 16, 16), B=0.4):
+    mask = sphere_mask(grid, CELL, 0.45 * grid[0] * CELL[0])
+    rng = np.random.default_rng(3)
+    m0 = tilted_uniform(int(np.prod(grid)), rng, (0.0, 0.03, 1.0), 0.0, mask)
+    s = mcq.Solver(grid, CELL, YIG_MS, YIG_A, 0.0)
+    mcq.mcq_set_geometry(s.ctx, mask)
+    mcq.mcq_set_bext(s.ctx, (0.0, 0.0, B))
+    return s, mask, m0
+
+
+def _zero_cross_freq(x, dt):
+    x = np.asarray(x) - np.mean(x)
+    idx = np.nonzero((x[:-1] < 0) & (x[1:] >= 0))[0]
+    tc = (idx + (-x[idx]) / (x[idx + 1] - x[idx])) * dt
+    return (len(tc) - 1) / (tc[-1] - tc[0])
+
+
+def test_gpu_kittel_sphere():
+    """Uniform mode of a discretised YIG sphere (16^3 cells, exchange + full demag on the GPU):
+    omega = gamma B (N = 1/3 each way) within 0.5%."""
+    B = 0.4
+    s, mask, m0 = _sphere(B=B)
+    s.set_m(m0)
+    dt = 2 * math.pi / (GAMMA * B) / 80          # exchange-limited RK4 step (~1.5 ps)
+    s.trace(10000)
+    s.run(dt, 8000)
+    tr = s.trace()
+    f = _zero_cross_freq(tr[:, 2], dt)            # <m_y>
+    assert f == pytest.approx(GAMMA * B / (2 * math.pi), rel=5e-3)
+    s.close()
+
+
+def test_gpu_vacuum_rabi_splitting_sphere():
+    """The same sphere with a uniform B_rms along x and f_c = its measured Kittel frequency:
+    the two peaks of <m_y>(t) sit at the two-oscillator Omega_-+ with g from the coupling law
+     within 0.5% (BJ north_star), exercising W, the alpha recursion and the feedback."""
+    B = 0.4
+    s, mask, m0 = _sphere(B=B)
+    s.set_m(m0)
+    dt0 = 2 * math.pi / (GAMMA * B) / 80
+    s.trace(10000)
+    s.run(dt0, 8000)
+    fz = _zero_cross_freq(s.trace()[:, 2], dt0)
+    wz = 2 * math.pi * fz
+    nmag = int(mask.sum())
+    V = nmag * np.prod(CELL)
+    g = 0.04 * wz
+    Bperp = g / (GAMMA * math.sqrt(YIG_MS * V / (A.HBAR * GAMMA) / 2))
+    assert A.coupling_g(Bperp, YIG_MS, V) == pytest.approx(g, rel=1e-12)
+    mcq.mcq_set_brms(s.ctx, None, (Bperp, 0.0, 0.0))
+    mcq.mcq_set_cavity(s.ctx, fz, 0.0, 0.0, 0.0)
+    s.set_m(m0)
+    dt = 2 * math.pi / wz / 80
+    s.trace(20000)
+    s.run(dt, 16000)
+    tr = s.trace()
+    lo, hi = A.peaks(tr[:, 2], dt, 2, window="hann", pad=8)
+    om, op = A.two_oscillator(wz, wz, g)
+    assert lo == pytest.approx(om / (2 * math.pi), rel=5e-3)
+    assert hi == pytest.approx(op / (2 * math.pi), rel=5e-3)
+    assert 2 * math.pi * (hi - lo) == pytest.approx(op - om, rel=1e-2)
+    s.close()

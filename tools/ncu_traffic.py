@@ -1,0 +1,50 @@
+"""Extract per-launch DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) of the hot-path
+kernels from an `ncu --set full` report and store it for bench.py's roofline "traffic" field.
+
+    python tools/ncu_traffic.py report.ncu-rep profiles/ncu_traffic.json config1
+
+The JSON maps a workload key to {kernel class: bytes per launch, "_source": report name}; kernel
+classes follow bench.py (yfwd, zconv, yinv, y2d, update, cavity)."""
+import csv
+import json
+import os
+import subprocess
+import sys
+
+CLASS = [("k_ypass<", ", 0>", "yfwd"), ("k_ypass<", ", 1>", "yinv"), ("k_zconv", "", "zconv"),
+         ("k_conv<", ", 1>", "y2d"), ("k_conv<", ", 0>", "zconv"), ("k_update", "", "update"),
+         ("k_cavity", "", "cavity")]
+
+
+def classify(name):
+    for pre, post, k in CLASS:
+        if name.startswith("void " + pre) or name.startswith(pre):
+            if not post or post in name.split("(")[0]:
+                return k
+    return None
+
+
+def main(rep, out, key):
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(txt.splitlines()))
+    hdr, data = rows[0], rows[2:]
+    iname = hdr.index("Kernel Name")
+    ir, iw = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+    iu = rows[1]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    acc = {}
+    for d in data:
+        k = classify(d[iname])
+        if not k:
+            continue
+        b = float(d[ir]) * scale.get(iu[ir], 1) + float(d[iw]) * scale.get(iu[iw], 1)
+        acc.setdefault(k, []).append(b)
+    res = json.load(open(out)) if os.path.exists(out) else {}
+    res[key] = {k: sum(v) / len(v) for k, v in acc.items()}
+    res[key]["_source"] = os.path.basename(rep)
+    json.dump(res, open(out, "w"), indent=1, sort_keys=True)
+    print(json.dumps(res[key]))
+
+
+if __name__ == "__main__":
+    main(*sys.argv[1:4])
