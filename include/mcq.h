@@ -2,7 +2,7 @@
  * mcq.h — C ABI of the B200-native Mumax3-cQED hot path (arXiv 2410.00966).
  *
  * One context = one ferromagnet on an nx*ny*nz finite-difference grid coupled to one damped
- * cavity mode.  Each mcq_run step integrates the LLG equation with the cavity field
+ * cavity mode (or up to MCQ_MAX_MODES independent modes, see mcq_set_modes).  Each mcq_run step integrates the LLG equation with the cavity field
  *     dm_i/dt = -gamma/(1+alpha^2) [m_i x B'_i + alpha m_i x (m_i x B'_i)]            (eq:llg)
  *     B'_i = B_ext + B_exch + B_anis + B_demag + a sinc(w_cut t) B_rms,i + B_rms,i Gamma(t)
  *                                                     (eq:bcav P:239, excitation P:165)
@@ -149,8 +149,25 @@ MCQ_API int mcq_set_cavity(mcq_ctx *, double f_c, double kappa, double x0, doubl
 /* Excitation a * sinc(w_cut t) * B_rms, unnormalised sinc, t = cavity clock (C13). */
 MCQ_API int mcq_set_excitation(mcq_ctx *, double amplitude, double omega_cut);
 
-/* ResetMemoryTerm(): alpha <- alpha_0, t <- 0, step <- 0. */
+/* ResetMemoryTerm(): alpha_k <- alpha_0,k for every mode, t <- 0, step <- 0. */
 MCQ_API int mcq_reset_memory(mcq_ctx *);
+
+/* Multimode cavity (P:24 runs modes separately, calls a native multimode
+ * cavity "straightforward").  Reading C-MM: mode k is its own damped oscillator with its own
+ * B_rms,k, f_k, kappa_k, alpha_0,k and excitation, driven by its own overlap
+ * W_k = sum_i M_s m_i . B_rms,k(r_i) through the same recursion; B' gains
+ * sum_k B_rms,k (Gamma_k(t) + a_k sinc(w_k t)).  The single-mode calls above act on mode 0.
+ * mcq_set_modes(n), 1 <= n <= MCQ_MAX_MODES: modes >= n return to their defaults (B_rms = 0,
+ * f = 1 GHz, kappa = x0 = p0 = a = 0); resets the memory.  The *_mode calls take k < n
+ * (EINVAL otherwise) and behave like their single-mode counterparts for mode k.  The clock t and
+ * the step counter are shared; mcq_set_cavity_state_mode sets them together with alpha_k. */
+#define MCQ_MAX_MODES 4
+MCQ_API int mcq_set_modes(mcq_ctx *, int nmodes);
+MCQ_API int mcq_set_brms_mode(mcq_ctx *, int k, const float *map, const double uniform[3]);
+MCQ_API int mcq_set_cavity_mode(mcq_ctx *, int k, double f_c, double kappa, double x0, double p0);
+MCQ_API int mcq_set_excitation_mode(mcq_ctx *, int k, double amplitude, double omega_cut);
+MCQ_API int mcq_get_cavity_mode(mcq_ctx *, int k, mcq_cavity_state *out);
+MCQ_API int mcq_set_cavity_state_mode(mcq_ctx *, int k, const mcq_cavity_state *in);
 
 /* Relax (reading C15): RK4 with step dt (s) on dm/dt = -gamma m x (m x B'), cavity and
  * excitation off, t frozen; every 50 steps stop if max_i |m_i x B'_i| < torque_tol (T); at
@@ -176,7 +193,7 @@ MCQ_API int mcq_get_cavity(mcq_ctx *, mcq_cavity_state *out);
 /* Resume: sets t, alpha (re/im) and step from `in` (other fields ignored). */
 MCQ_API int mcq_set_cavity_state(mcq_ctx *, const mcq_cavity_state *in);
 
-/* CavityFeatureStatus: 1 iff B_rms is set and nonzero, else 0; <0 on error. */
+/* CavityFeatureStatus: 1 iff some active mode's B_rms is nonzero, else 0; <0 on error. */
 MCQ_API int mcq_cavity_status(const mcq_ctx *);
 
 /* Number of library kernels launched so far (graph replays count every kernel node). */

@@ -120,6 +120,42 @@ def mcq_reset_memory(ctx):
     _check(ctx, lib.mcq_reset_memory(ctx))
 
 
+MAX_MODES = 4
+
+
+def mcq_set_modes(ctx, nmodes):
+    """Number of cavity modes (include/mcq.h, NEXT-2); mode 0 is the single-mode API's."""
+    _check(ctx, lib.mcq_set_modes(ctx, int(nmodes)))
+
+
+def mcq_set_brms_mode(ctx, k, map=None, uniform=(0.0, 0.0, 0.0)):
+    a = _vec(map) if map is not None else None
+    _check(ctx, lib.mcq_set_brms_mode(ctx, int(k), a.ctypes.data if a is not None else None, _d3(uniform)))
+
+
+def mcq_set_cavity_mode(ctx, k, f_c, kappa, x0=0.0, p0=0.0):
+    _check(ctx, lib.mcq_set_cavity_mode(ctx, int(k), float(f_c), float(kappa), float(x0), float(p0)))
+
+
+def mcq_set_excitation_mode(ctx, k, amplitude, omega_cut):
+    _check(ctx, lib.mcq_set_excitation_mode(ctx, int(k), float(amplitude), float(omega_cut)))
+
+
+def mcq_get_cavity_mode(ctx, k):
+    s = mcq_cavity_state()
+    _check(ctx, lib.mcq_get_cavity_mode(ctx, int(k), C.byref(s)))
+    return s.as_dict()
+
+
+def mcq_set_cavity_state_mode(ctx, k, state):
+    s = mcq_cavity_state()
+    s.t = float(state["t"])
+    s.re_alpha = float(state["re_alpha"])
+    s.im_alpha = float(state["im_alpha"])
+    s.step = int(state.get("step", 0))
+    _check(ctx, lib.mcq_set_cavity_state_mode(ctx, int(k), C.byref(s)))
+
+
 def mcq_relax(ctx, dt, torque_tol, max_steps):
     n = C.c_longlong(0)
     _check(ctx, lib.mcq_relax(ctx, float(dt), float(torque_tol), int(max_steps), C.byref(n)))

@@ -63,6 +63,12 @@ _sig = {
     "mcq_set_cavity": (C.c_int, [_P, C.c_double, C.c_double, C.c_double, C.c_double]),
     "mcq_set_excitation": (C.c_int, [_P, C.c_double, C.c_double]),
     "mcq_reset_memory": (C.c_int, [_P]),
+    "mcq_set_modes": (C.c_int, [_P, C.c_int]),
+    "mcq_set_brms_mode": (C.c_int, [_P, C.c_int, _P, C.POINTER(C.c_double)]),
+    "mcq_set_cavity_mode": (C.c_int, [_P, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double]),
+    "mcq_set_excitation_mode": (C.c_int, [_P, C.c_int, C.c_double, C.c_double]),
+    "mcq_get_cavity_mode": (C.c_int, [_P, C.c_int, C.POINTER(mcq_cavity_state)]),
+    "mcq_set_cavity_state_mode": (C.c_int, [_P, C.c_int, C.POINTER(mcq_cavity_state)]),
     "mcq_relax": (C.c_int, [_P, C.c_double, C.c_double, C.c_longlong, C.POINTER(C.c_longlong)]),
     "mcq_run": (C.c_int, [_P, C.c_double, C.c_longlong]),
     "mcq_synchronize": (C.c_int, [_P]),

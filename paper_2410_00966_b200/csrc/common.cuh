@@ -91,30 +91,36 @@ __host__ __device__ __forceinline__ int kx_owner(const Dims& d, int kx) {
   return q < d.NS - 1 ? q : d.NS - 1;
 }
 
+// Cavity modes (reading C-MM): mode 0 is the paper's single mode; extra
+// modes are independent oscillators driven by their own overlaps, their fields add.
+constexpr int kMaxModes = 4;
+
 // Cavity state on the device (fp64), advanced once per step by k_cavity (a13).
 struct CavState {
-  double re, im;      // alpha_n
-  double t;           // cavity clock t_n
-  double W;           // overlap of the last completed step
+  double re[kMaxModes], im[kMaxModes];  // alpha_n per mode
+  double t;                             // cavity clock t_n (shared)
+  double W[kMaxModes];                  // overlaps of the last completed step
   long long step;
-  float gc[4];        // Gamma(t_n + c_s dt) = 2 Re(e^{-(kappa+iw) c_s dt} alpha_n), s = 0..3
-  float ge[4];        // a sinc(w_cut (t_n + c_s dt))
-  long long trace_rows;  // trace rows recorded since the last reset (may exceed the capacity)
+  float gc[kMaxModes][4];  // Gamma_k(t_n + c_s dt) = 2 Re(e^{-(kappa_k+iw_k) c_s dt} alpha_k,n), s = 0..3
+  float ge[kMaxModes][4];  // a_k sinc(w_cut,k (t_n + c_s dt))
+  long long trace_rows;    // trace rows recorded since the last reset (may exceed the capacity)
 };
 
-// Per-CTA fp64 partials of the stage-4 update, interleaved [CTA][kNPart]:
-// W = sum B_rms . m, and sum m_x, m_y, m_z (the trace's spatial mean, NEXT-3)
-constexpr int kNPart = 4;
+// Per-CTA fp64 partials of the stage-4 update, per slab [kNPart][CTA]: W_k = sum B_rms,k . m
+// for k < kMaxModes, then sum m_x, m_y, m_z (the trace's spatial mean, NEXT-3)
+constexpr int kNPart = kMaxModes + 3;
+constexpr int kPartM = kMaxModes;  // index of sum m_x
 constexpr int kTraceCols = 8;  // t, <mx>, <my>, <mz>, Re alpha, Im alpha, W, step
 
 // Scalars the cavity kernels need (host precomputed in fp64 for a given dt).
 struct CavParams {
-  double ec_re[3], ec_im[3];  // e^{-(kappa + i w) c dt} for c = 0, 1/2, 1
+  double ec_re[kMaxModes][3], ec_im[kMaxModes][3];  // e^{-(kappa_k + i w_k) c dt}, c = 0, 1/2, 1
   double vc_over_hbar;        // V_c / hbar
   double Ms;
   double dt;
-  double exc_amp, exc_omega;
-  int cav_on;                 // B_rms nonzero (C14)
+  double exc_amp[kMaxModes], exc_omega[kMaxModes];
+  int cav_on[kMaxModes];      // B_rms,k nonzero (C14)
+  int nmodes;
   int pdl;                    // launch K-CAV with programmatic dependent launch
   double* trace;              // [trace_cap][kTraceCols] or nullptr
   long long trace_cap;
@@ -135,8 +141,9 @@ struct UpdateArgs {
   float* mOut;        // m_{s+1} (stages 1-3) or m_{n+1} (stage 4, may alias mN)
   float* acc;         // RK4 accumulator k1 + 2k2 + 2k3 (SoA)
   float2* X;          // x-spectrum rows [3][nz][ny][P]: demag in, FFT(m_{s+1}) out
-  const float* brms;  // SoA map or nullptr
-  float brms_u[3];
+  const float* brms[kMaxModes];  // SoA map per mode or nullptr (then the uniform value)
+  float brms_u[kMaxModes][3];
+  int nmodes;
   float bext[3];
   float ex[3];        // 2A / (Ms d_axis^2)
   float ku, u[3];     // 2 K_u1 / Ms, axis
@@ -171,7 +178,7 @@ int launch_y2d(const Dims& d, float2* X, const float* khat, const float2* tw, cu
 void configure_update_kernels();
 void launch_update(const UpdateArgs& a, const float2* tw, cudaStream_t s);
 int update_grid_blocks(const Dims& d);
-void launch_cavity(const CavParams& p, CavState* st, const double* partials, int n, cudaStream_t s);
+void launch_cavity(const CavParams& p, CavState* st, const double* partials, int n, int nps, cudaStream_t s);
 void launch_cav_prepare(const CavParams& p, CavState* st, cudaStream_t s);
 void launch_aos_to_soa(const float* in, float* out, const uint8_t* mask, long long N, long long cs, long long off,
                        int* bad, cudaStream_t s);

@@ -83,7 +83,8 @@ struct Slab {
   Dims d{};
   float *mN = nullptr, *mA = nullptr, *mB = nullptr, *acc = nullptr;  // [3][cs]
   float2 *X = nullptr, *Y = nullptr, *R = nullptr;  // X [3][nz][ny][P]; Y, R [NS][3][nz][Ly][KXS]
-  float *brms = nullptr, *field = nullptr;          // [3][cs]
+  float* brms[kMaxModes] = {nullptr, nullptr, nullptr, nullptr};  // [3][cs] per mode (maps)
+  float* field = nullptr;                           // [3][cs]
   uint8_t* mask = nullptr;                          // [nz][ny][nx]
   double* partials = nullptr;                       // into ctx partials (loopback) or own (NCCL)
   int nparts = 0;
@@ -106,12 +107,14 @@ struct mcq_ctx {
   std::vector<Slab> sl;
   float2* tw = nullptr;
   float* khat = nullptr;
-  double brms_u[3] = {0, 0, 0};
-  bool brms_map = false;
-  bool cav_on = false;
+  int nmodes = 1;  // cavity modes (mode 0 = the paper's single mode; NEXT-2, reading C-MM)
+  double brms_u[kMaxModes][3] = {};
+  bool brms_map[kMaxModes] = {};
+  bool cav_on[kMaxModes] = {};
   bool have_mask = false;
   double bext[3] = {0, 0, 0};
-  double fc = 1e9, kappa = 0, x0 = 0, p0 = 0, exc_amp = 0, exc_omega = 0;
+  double fc[kMaxModes] = {1e9, 1e9, 1e9, 1e9}, kappa[kMaxModes] = {}, x0[kMaxModes] = {}, p0[kMaxModes] = {};
+  double exc_amp[kMaxModes] = {}, exc_omega[kMaxModes] = {};
   CavState* cav = nullptr;
   double* partials = nullptr;  // all slabs' per-CTA partials [CTA][kNPart] in global z order
   int nparts = 0;              // CTAs of one stage-4 update (all slabs)
@@ -176,20 +179,23 @@ void invalidate_graphs(mcq_ctx* c) {
 
 CavParams cav_params(const mcq_ctx* c, double dt) {
   CavParams p{};
-  const double w = 2.0 * M_PI * c->fc;
   const double cs[3] = {0.0, 0.5, 1.0};
-  for (int i = 0; i < 3; ++i) {
-    const double a = cs[i] * dt;
-    const double dec = std::exp(-c->kappa * a);
-    p.ec_re[i] = dec * std::cos(w * a);
-    p.ec_im[i] = -dec * std::sin(w * a);
+  for (int k = 0; k < kMaxModes; ++k) {
+    const double w = 2.0 * M_PI * c->fc[k];
+    for (int i = 0; i < 3; ++i) {
+      const double a = cs[i] * dt;
+      const double dec = std::exp(-c->kappa[k] * a);
+      p.ec_re[k][i] = dec * std::cos(w * a);
+      p.ec_im[k][i] = -dec * std::sin(w * a);
+    }
+    p.exc_amp[k] = c->exc_amp[k];
+    p.exc_omega[k] = c->exc_omega[k];
+    p.cav_on[k] = (k < c->nmodes && c->cav_on[k]) ? 1 : 0;
   }
+  p.nmodes = c->nmodes;
   p.vc_over_hbar = c->dx * c->dy * c->dz / kHbar;
   p.Ms = c->Ms;
   p.dt = dt;
-  p.exc_amp = c->exc_amp;
-  p.exc_omega = c->exc_omega;
-  p.cav_on = c->cav_on ? 1 : 0;
   p.trace = c->trace_cap > 0 ? c->trace : nullptr;
   p.trace_cap = c->trace_cap;
   p.trace_every = c->trace_every;
@@ -202,11 +208,13 @@ UpdateArgs base_args(const mcq_ctx* c, const Slab& s) {
   UpdateArgs a{};
   a.d = s.d;
   a.terms = MCQ_TERM_ALL;
-  a.brms = c->brms_map ? s.brms : nullptr;
-  for (int i = 0; i < 3; ++i) {
-    a.brms_u[i] = (float)c->brms_u[i];
-    a.bext[i] = (float)c->bext[i];
+  a.nmodes = c->nmodes;
+  for (int k = 0; k < kMaxModes; ++k) {
+    const bool on = k < c->nmodes;
+    a.brms[k] = (on && c->brms_map[k]) ? s.brms[k] : nullptr;
+    for (int i = 0; i < 3; ++i) a.brms_u[k][i] = on ? (float)c->brms_u[k][i] : 0.f;
   }
+  for (int i = 0; i < 3; ++i) a.bext[i] = (float)c->bext[i];
   a.ex[0] = (float)(2.0 * c->Aex / (c->Ms * c->dx * c->dx));
   a.ex[1] = (float)(2.0 * c->Aex / (c->Ms * c->dy * c->dy));
   a.ex[2] = (float)(2.0 * c->Aex / (c->Ms * c->dz * c->dz));
@@ -400,7 +408,7 @@ struct Enq {
     gather_partials();
     const CavParams p = cav_params(c, dt);
     pre(MCQ_K_CAVITY);
-    launch_cavity(p, c->cav, c->partials, c->nparts, s);
+    launch_cavity(p, c->cav, c->partials, c->nparts, c->sl[0].nparts, s);
     post(MCQ_K_CAVITY);
   }
   void relax_step(double dt) {
@@ -467,12 +475,7 @@ int capture(mcq_ctx* c, int which, double dt, int steps) {
   return MCQ_OK;
 }
 
-int set_cav_state(mcq_ctx* c, double re, double im, double t, long long step) {
-  CavState h{};
-  h.re = re;
-  h.im = im;
-  h.t = t;
-  h.step = step;
+int write_cav_state(mcq_ctx* c, const CavState& h) {
   CK(c, cudaMemcpyAsync(c->cav, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
   const CavParams p = cav_params(c, 1e-12);
   launch_cav_prepare(p, c->cav, c->stream);
@@ -481,7 +484,21 @@ int set_cav_state(mcq_ctx* c, double re, double im, double t, long long step) {
   return MCQ_OK;
 }
 
-int reset_memory(mcq_ctx* c) { return set_cav_state(c, 0.5 * c->x0, -0.5 * c->p0, 0.0, 0); }
+int read_cav_state(mcq_ctx* c, CavState& h) {
+  CK(c, cudaMemcpyAsync(&h, c->cav, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  return MCQ_OK;
+}
+
+// every mode back to alpha_0 = (x0 - i p0)/2 at t = 0 (ResetMemoryTerm; C6)
+int reset_memory(mcq_ctx* c) {
+  CavState h{};
+  for (int k = 0; k < kMaxModes; ++k) {
+    h.re[k] = 0.5 * c->x0[k];
+    h.im[k] = -0.5 * c->p0[k];
+  }
+  return write_cav_state(c, h);
+}
 
 // cos / sin transform matrices of one axis: T[k][o], k, o in [0, L/2]
 void axis_matrices(int L, std::vector<double>& Tc, std::vector<double>& Ts) {
@@ -550,7 +567,7 @@ int build_khat(mcq_ctx* c, double* oct_out /* optional host copy of the octant *
 void free_all(mcq_ctx* c) {
   invalidate_graphs(c);
   for (auto& s : c->sl) {
-    void* ptrs[] = {s.mN, s.mA, s.mB, s.acc, s.X, s.Y, s.R, s.brms, s.field, s.mask};
+    void* ptrs[] = {s.mN, s.mA, s.mB, s.acc, s.X, s.Y, s.R, s.brms[0], s.brms[1], s.brms[2], s.brms[3], s.field, s.mask};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (c->mode == 2 && s.partials) cudaFree(s.partials);
@@ -890,8 +907,30 @@ int mcq_set_bext(mcq_ctx* c, const double B[3]) {
   return MCQ_OK;
 }
 
-int mcq_set_brms(mcq_ctx* c, const float* map, const double uniform[3]) {
+static int valid_mode(mcq_ctx* c, int k) { return k >= 0 && k < c->nmodes; }
+
+int mcq_set_modes(mcq_ctx* c, int nmodes) {
+  if (!c) return MCQ_EINVAL;
+  if (nmodes < 1 || nmodes > kMaxModes) return fail(c, MCQ_EINVAL, "1 <= nmodes <= MCQ_MAX_MODES");
+  CK(c, cudaStreamSynchronize(c->stream));
+  for (int k = nmodes; k < kMaxModes; ++k) {  // dropped modes return to their defaults
+    for (auto& s : c->sl) {
+      if (s.brms[k]) cudaFree(s.brms[k]);
+      s.brms[k] = nullptr;
+    }
+    c->brms_map[k] = c->cav_on[k] = false;
+    c->brms_u[k][0] = c->brms_u[k][1] = c->brms_u[k][2] = 0.0;
+    c->fc[k] = 1e9;
+    c->kappa[k] = c->x0[k] = c->p0[k] = c->exc_amp[k] = c->exc_omega[k] = 0.0;
+  }
+  c->nmodes = nmodes;
+  invalidate_graphs(c);
+  return reset_memory(c);
+}
+
+int mcq_set_brms_mode(mcq_ctx* c, int k, const float* map, const double uniform[3]) {
   if (!c || (!map && !uniform)) return MCQ_EINVAL;
+  if (!valid_mode(c, k)) return fail(c, MCQ_EINVAL, "mode index out of range (mcq_set_modes)");
   const long long Nall = c->dg.N;
   if (map) {
     bool nz = false;
@@ -903,51 +942,65 @@ int mcq_set_brms(mcq_ctx* c, const float* map, const double uniform[3]) {
                           c->stream));
     for (int i = 0; i < (int)c->sl.size(); ++i) {
       Slab& s = c->sl[i];
-      if (!s.brms) {
-        CK(c, cudaMalloc(&s.brms, 3ULL * s.d.cs * 4));
-        CK(c, cudaMemsetAsync(s.brms, 0, 3ULL * s.d.cs * 4, c->stream));
+      if (!s.brms[k]) {
+        CK(c, cudaMalloc(&s.brms[k], 3ULL * s.d.cs * 4));
+        CK(c, cudaMemsetAsync(s.brms[k], 0, 3ULL * s.d.cs * 4, c->stream));
       }
-      launch_deinterleave(c->io + 3 * i * s.d.N, s.brms, s.d.N, s.d.cs, (long long)s.d.zoff * s.d.nx * s.d.ny,
+      launch_deinterleave(c->io + 3 * i * s.d.N, s.brms[k], s.d.N, s.d.cs, (long long)s.d.zoff * s.d.nx * s.d.ny,
                           c->stream);
       c->launches += 1;
     }
     CK(c, cudaStreamSynchronize(c->stream));
-    c->brms_u[0] = c->brms_u[1] = c->brms_u[2] = 0.0;
-    c->brms_map = true;
-    c->cav_on = nz;
+    c->brms_u[k][0] = c->brms_u[k][1] = c->brms_u[k][2] = 0.0;
+    c->brms_map[k] = true;
+    c->cav_on[k] = nz;
   } else {
     for (int i = 0; i < 3; ++i)
       if (!std::isfinite(uniform[i])) return fail(c, MCQ_EINVAL, "B_rms not finite");
     for (auto& s : c->sl) {
-      if (s.brms) cudaFree(s.brms);
-      s.brms = nullptr;
+      if (s.brms[k]) cudaFree(s.brms[k]);
+      s.brms[k] = nullptr;
     }
-    c->brms_map = false;
-    for (int i = 0; i < 3; ++i) c->brms_u[i] = uniform[i];
-    c->cav_on = uniform[0] != 0 || uniform[1] != 0 || uniform[2] != 0;
+    c->brms_map[k] = false;
+    for (int i = 0; i < 3; ++i) c->brms_u[k][i] = uniform[i];
+    c->cav_on[k] = uniform[0] != 0 || uniform[1] != 0 || uniform[2] != 0;
   }
   invalidate_graphs(c);
   return reset_memory(c) == MCQ_OK ? MCQ_OK : MCQ_ECUDA;
 }
 
-int mcq_set_cavity(mcq_ctx* c, double f_c, double kappa, double x0, double p0) {
+int mcq_set_brms(mcq_ctx* c, const float* map, const double uniform[3]) {
+  return c ? mcq_set_brms_mode(c, 0, map, uniform) : MCQ_EINVAL;
+}
+
+int mcq_set_cavity_mode(mcq_ctx* c, int k, double f_c, double kappa, double x0, double p0) {
   if (!c) return MCQ_EINVAL;
+  if (!valid_mode(c, k)) return fail(c, MCQ_EINVAL, "mode index out of range (mcq_set_modes)");
   if (!(f_c > 0) || !(kappa >= 0) || !std::isfinite(x0) || !std::isfinite(p0))
     return fail(c, MCQ_EINVAL, "f_c must be > 0, kappa >= 0");
-  c->fc = f_c;
-  c->kappa = kappa;
-  c->x0 = x0;
-  c->p0 = p0;
+  c->fc[k] = f_c;
+  c->kappa[k] = kappa;
+  c->x0[k] = x0;
+  c->p0[k] = p0;
   invalidate_graphs(c);
   return reset_memory(c);
 }
 
-int mcq_set_excitation(mcq_ctx* c, double amplitude, double omega_cut) {
+int mcq_set_cavity(mcq_ctx* c, double f_c, double kappa, double x0, double p0) {
+  return c ? mcq_set_cavity_mode(c, 0, f_c, kappa, x0, p0) : MCQ_EINVAL;
+}
+
+int mcq_set_excitation_mode(mcq_ctx* c, int k, double amplitude, double omega_cut) {
   if (!c || !std::isfinite(amplitude) || !std::isfinite(omega_cut)) return MCQ_EINVAL;
-  c->exc_amp = amplitude;
-  c->exc_omega = omega_cut;
+  if (!valid_mode(c, k)) return fail(c, MCQ_EINVAL, "mode index out of range (mcq_set_modes)");
+  c->exc_amp[k] = amplitude;
+  c->exc_omega[k] = omega_cut;
   invalidate_graphs(c);
   return MCQ_OK;
+}
+
+int mcq_set_excitation(mcq_ctx* c, double amplitude, double omega_cut) {
+  return c ? mcq_set_excitation_mode(c, 0, amplitude, omega_cut) : MCQ_EINVAL;
 }
 
 int mcq_reset_memory(mcq_ctx* c) {
@@ -1064,39 +1117,58 @@ int mcq_get_field(mcq_ctx* c, float* b_out, unsigned terms) {
   return MCQ_OK;
 }
 
-int mcq_get_cavity(mcq_ctx* c, mcq_cavity_state* out) {
+int mcq_get_cavity_mode(mcq_ctx* c, int k, mcq_cavity_state* out) {
   if (!c || !out) return MCQ_EINVAL;
+  if (!valid_mode(c, k)) return fail(c, MCQ_EINVAL, "mode index out of range (mcq_set_modes)");
   CavState h{};
-  CK(c, cudaMemcpyAsync(&h, c->cav, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
-  CK(c, cudaStreamSynchronize(c->stream));
+  int rc = read_cav_state(c, h);
+  if (rc != MCQ_OK) return rc;
+  const double re = h.re[k], im = h.im[k];
   out->t = h.t;
-  out->re_alpha = h.re;
-  out->im_alpha = h.im;
-  out->gamma = 2.0 * h.re;
-  out->W = h.W;
-  out->n_photon = h.re * h.re + h.im * h.im;
+  out->re_alpha = re;
+  out->im_alpha = im;
+  out->gamma = 2.0 * re;
+  out->W = h.W[k];
+  out->n_photon = re * re + im * im;
   out->step = h.step;
   // S - i C = (hbar / V_c)(alpha_0 - e^{(kappa + i w) t} alpha)
-  const double w = 2.0 * M_PI * c->fc, vc = c->dx * c->dy * c->dz;
-  const double g = std::exp(c->kappa * h.t);
+  const double w = 2.0 * M_PI * c->fc[k], vc = c->dx * c->dy * c->dz;
+  const double g = std::exp(c->kappa[k] * h.t);
   const double er = g * std::cos(w * h.t), ei = g * std::sin(w * h.t);
-  const double ar = er * h.re - ei * h.im, ai = er * h.im + ei * h.re;
-  const double dr = 0.5 * c->x0 - ar, di = -0.5 * c->p0 - ai;
+  const double ar = er * re - ei * im, ai = er * im + ei * re;
+  const double dr = 0.5 * c->x0[k] - ar, di = -0.5 * c->p0[k] - ai;
   out->S = kHbar / vc * dr;
   out->C = -kHbar / vc * di;
   return MCQ_OK;
 }
 
-int mcq_set_cavity_state(mcq_ctx* c, const mcq_cavity_state* in) {
+int mcq_get_cavity(mcq_ctx* c, mcq_cavity_state* out) { return c ? mcq_get_cavity_mode(c, 0, out) : MCQ_EINVAL; }
+
+int mcq_set_cavity_state_mode(mcq_ctx* c, int k, const mcq_cavity_state* in) {
   if (!c || !in) return MCQ_EINVAL;
+  if (!valid_mode(c, k)) return fail(c, MCQ_EINVAL, "mode index out of range (mcq_set_modes)");
   if (!std::isfinite(in->t) || !std::isfinite(in->re_alpha) || !std::isfinite(in->im_alpha))
     return fail(c, MCQ_EINVAL, "non-finite cavity state");
-  return set_cav_state(c, in->re_alpha, in->im_alpha, in->t, in->step);
+  CavState h{};
+  int rc = read_cav_state(c, h);
+  if (rc != MCQ_OK) return rc;
+  h.re[k] = in->re_alpha;
+  h.im[k] = in->im_alpha;
+  h.t = in->t;  // the clock and the step counter are shared by the modes
+  h.step = in->step;
+  h.trace_rows = 0;
+  return write_cav_state(c, h);
+}
+
+int mcq_set_cavity_state(mcq_ctx* c, const mcq_cavity_state* in) {
+  return c ? mcq_set_cavity_state_mode(c, 0, in) : MCQ_EINVAL;
 }
 
 int mcq_cavity_status(const mcq_ctx* c) {
   if (!c) return MCQ_EINVAL;
-  return c->cav_on ? 1 : 0;
+  for (int k = 0; k < c->nmodes; ++k)
+    if (c->cav_on[k]) return 1;
+  return 0;
 }
 
 int mcq_set_trace(mcq_ctx* c, long long capacity, int every) {

@@ -75,11 +75,12 @@ struct RowAddr {  // shared-memory address of element pos of component-line l of
 };
 
 // One cell from register inputs: state m, in-mesh neighbours nb[k] (valid where ok[k]), m_n,
-// the RK4 accumulator so far, B_rms and the demag field.  Computes B' and, by mode, the field
-// (Bout), the max torque, or the RK4 stage update (returns m_{s+1}, writes the new accumulator
-// to acc_out).  All memory traffic stays in the caller (paired 8-byte accesses).
+// the RK4 accumulator so far, the cavity + excitation field bcav = sum_k B_rms,k (Gamma_k +
+// a_k sinc) (added iff has_cav) and the demag field.  Computes B' and, by mode, the field (Bout),
+// the max torque, or the RK4 stage update (returns m_{s+1}, writes the new accumulator to
+// acc_out).  All memory traffic (and the overlap sums) stays in the caller.
 __device__ __forceinline__ float3 cell_core(const UpdateArgs& a, float3 m, const float3 (&nb)[6], const bool (&ok)[6],
-                                            float3 mn, float3 ap, float3 br, float3 Bd, float gsum, double& wacc,
+                                            float3 mn, float3 ap, float3 bcav, bool has_cav, float3 Bd,
                                             float& tmax, float3& acc_out, float3& Bout) {
   if (a.mode == MODE_X0) return m;
   float3 B = make_float3(0.f, 0.f, 0.f);
@@ -124,10 +125,10 @@ __device__ __forceinline__ float3 cell_core(const UpdateArgs& a, float3 m, const
         B.z += f1 * a.c1[2] + f2 * a.c2[2] + f3 * a.c3[2];
       }
     }
-    if (gsum != 0.f) {
-      B.x += br.x * gsum;
-      B.y += br.y * gsum;
-      B.z += br.z * gsum;
+    if (has_cav) {
+      B.x += bcav.x;
+      B.y += bcav.y;
+      B.z += bcav.z;
     }
   }
   if (a.mode == MODE_FIELD) {
@@ -155,7 +156,6 @@ __device__ __forceinline__ float3 cell_core(const UpdateArgs& a, float3 m, const
     out = nrm3(make_float3(mn.x + a.h * k.x, mn.y + a.h * k.y, mn.z + a.h * k.z));
   } else {
     out = nrm3(make_float3(mn.x + a.dt6 * (ap.x + k.x), mn.y + a.dt6 * (ap.y + k.y), mn.z + a.dt6 * (ap.z + k.z)));
-    if (a.mode == MODE_LLG) wacc += (double)(br.x * out.x) + (double)(br.y * out.y) + (double)(br.z * out.z);
   }
   return out;
 }
@@ -176,10 +176,11 @@ __device__ __forceinline__ void st_pair(float* __restrict__ p, unsigned i, float
 }
 __device__ __forceinline__ float2 sm_pair(const float* p) { return *reinterpret_cast<const float2*>(p); }
 
-template <int N2>
 #ifndef MCQ_UMINB
 #define MCQ_UMINB 5  // min resident CTAs per SM requested from ptxas (96-register cap: 84.8 vs 86.8 us on configs[1])
 #endif
+// MM: cavity modes compiled in (1, or kMaxModes with a.nmodes <= MM at run time)
+template <int N2, int MM>
 __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a, const float2* __restrict__ gtw) {
   using Cf = UCfg<N2>;
   constexpr int E = Cf::E, TL = Cf::TL, RY = Cf::RY, NT = Cf::NT, LX = 2 * N2, PITCH = Cf::PITCH;
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
   const bool trows = tma && MCQ_UROWS;
   const bool st_mode = a.mode == MODE_LLG || a.mode == MODE_RELAX;
   const bool ld_mn = trows && st_mode && a.stage > 1;  // m_n and the accumulator: stages 2-4
-  const bool ld_br = trows && a.brms && (a.mode == MODE_LLG || a.mode == MODE_FIELD);
+  const bool ld_br = trows && a.brms[0] && (a.mode == MODE_LLG || a.mode == MODE_FIELD);
 
   // ---------------- 0: TMA staging (bars[0]: X rows, bars[1]: m_s tile) ----------------
   // thread 0 initialises the barriers and issues every copy at once, so the copies' latency
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
         tma_load_1d(tmn + c * csz, a.mN + c * N + rows, bz, &bars[1]);
         tma_load_1d(tap + c * csz, a.acc + c * N + rows, bz, &bars[1]);
       }
-      if (ld_br) tma_load_1d(tbr + c * csz, a.brms + c * N + rows, bz, &bars[1]);
+      if (ld_br) tma_load_1d(tbr + c * csz, a.brms[0] + c * N + rows, bz, &bars[1]);
     }
   }
   for (int m = threadIdx.x; m < LX; m += NT) tw[m] = gtw[m * (kTwMax / LX)];
@@ -307,14 +308,26 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
 
   // ---------------- B: per-cell fields, torque, RK4 ----------------
   if (tma) mbar_wait(&bars[1], 0);
-  float gc = 0.f, ge = 0.f;
-  if (a.mode == MODE_LLG || a.mode == MODE_FIELD) {
-    const int si = (a.mode == MODE_FIELD) ? 0 : a.stage - 1;
-    gc = (a.terms & MCQ_TERM_CAVITY) ? a.cav->gc[si] : 0.f;
-    ge = (a.terms & MCQ_TERM_EXCITATION) ? a.cav->ge[si] : 0.f;
+  // per mode k: gsum_k = Gamma_k(t_s) + a_k sinc(w_k t_s) (stage time t_s, C3)
+  const int nm = MM > 1 ? a.nmodes : 1;
+  float gs[MM];
+  bool any_cav = false;
+#pragma unroll
+  for (int k = 0; k < MM; ++k) {
+    float gc = 0.f, ge = 0.f;
+    if (k < nm && (a.mode == MODE_LLG || a.mode == MODE_FIELD)) {
+      const int si = (a.mode == MODE_FIELD) ? 0 : a.stage - 1;
+      gc = (a.terms & MCQ_TERM_CAVITY) ? a.cav->gc[k][si] : 0.f;
+      ge = (a.terms & MCQ_TERM_EXCITATION) ? a.cav->ge[k][si] : 0.f;
+    }
+    gs[k] = gc + ge;
+    any_cav = any_cav || gs[k] != 0.f;
   }
-  const float gsum = gc + ge;
-  double wacc = 0.0;
+  const float gsum = gs[0];
+  double wacc[MM];
+#pragma unroll
+  for (int k = 0; k < MM; ++k) wacc[k] = 0.0;
+  const bool wsum = a.mode == MODE_LLG && a.stage == 4;  // overlaps of m_{n+1}
   float tmax = 0.f;
   float3 msum = make_float3(0.f, 0.f, 0.f);  // stage 4 with the trace on: sum of m_{n+1}
   const bool tr = a.trace && a.mode == MODE_LLG && a.stage == 4;
@@ -324,7 +337,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
   const bool vec = (nx & 1) == 0;           // global pairs are 8-byte aligned
   const bool st = a.mode == MODE_LLG || a.mode == MODE_RELAX;
   const bool need_mn = st && a.stage > 1, need_acc = st && a.stage > 1;
-  const bool need_br = a.brms && (gsum != 0.f || (a.mode == MODE_LLG && a.stage == 4));
+  const bool need_br = a.brms[0] && (gsum != 0.f || wsum);
 #pragma unroll
   for (int i = 0; i < E; ++i) {
     const int x0 = 2 * (t + TL * i);
@@ -353,9 +366,17 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
         const int so = c * csz + yl * nxp + x0;  // staged rows (TMA path)
         mn2[c] = need_mn ? (trows ? sm_pair(tmn + so) : ld_pair(a.mN, c * Nu + idx, vec, two)) : make_float2(0.f, 0.f);
         ap2[c] = need_acc ? (trows ? sm_pair(tap + so) : ld_pair(a.acc, c * Nu + idx, vec, two)) : make_float2(0.f, 0.f);
-        br2[c] = need_br ? (trows ? sm_pair(tbr + so) : ld_pair(a.brms, c * Nu + idx, vec, two))
-                         : make_float2(a.brms_u[c], a.brms_u[c]);
+        br2[c] = need_br ? (trows ? sm_pair(tbr + so) : ld_pair(a.brms[0], c * Nu + idx, vec, two))
+                         : make_float2(a.brms_u[0][c], a.brms_u[0][c]);
       }
+      float2 bk2[MM > 1 ? MM - 1 : 1][3];  // extra modes' B_rms (maps or uniform values)
+#pragma unroll
+      for (int k = 1; k < MM; ++k)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          bk2[k - 1][c] = (k < nm && a.brms[k] && (gs[k] != 0.f || wsum))
+                              ? ld_pair(a.brms[k], c * Nu + idx, vec, two)
+                              : make_float2(a.brms_u[k][c], a.brms_u[k][c]);
       float2 acc2[3], bf2[3];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -375,9 +396,26 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
         const float3 ap = make_float3(MCQ_PICK(ap2[0]), MCQ_PICK(ap2[1]), MCQ_PICK(ap2[2]));
         const float3 br = make_float3(MCQ_PICK(br2[0]), MCQ_PICK(br2[1]), MCQ_PICK(br2[2]));
         const float3 Bd = make_float3(MCQ_PICK(v[0][i]), MCQ_PICK(v[1][i]), MCQ_PICK(v[2][i]));
-#undef MCQ_PICK
         float3 accn = make_float3(0.f, 0.f, 0.f), Bf = make_float3(0.f, 0.f, 0.f);
-        const float3 out = cell_core(a, m, nb, ok, mn, ap, br, Bd, gsum, wacc, tmax, accn, Bf);
+        float3 bcav = make_float3(br.x * gsum, br.y * gsum, br.z * gsum);
+#pragma unroll
+        for (int k = 1; k < MM; ++k) {
+          if (k < nm) {
+            bcav.x += MCQ_PICK(bk2[k - 1][0]) * gs[k];
+            bcav.y += MCQ_PICK(bk2[k - 1][1]) * gs[k];
+            bcav.z += MCQ_PICK(bk2[k - 1][2]) * gs[k];
+          }
+        }
+        const float3 out = cell_core(a, m, nb, ok, mn, ap, bcav, MM > 1 ? any_cav : gsum != 0.f, Bd, tmax, accn, Bf);
+        if (wsum) {
+          wacc[0] += (double)(br.x * out.x) + (double)(br.y * out.y) + (double)(br.z * out.z);
+#pragma unroll
+          for (int k = 1; k < MM; ++k)
+            if (k < nm)
+              wacc[k] += (double)(MCQ_PICK(bk2[k - 1][0]) * out.x) + (double)(MCQ_PICK(bk2[k - 1][1]) * out.y) +
+                         (double)(MCQ_PICK(bk2[k - 1][2]) * out.z);
+        }
+#undef MCQ_PICK
         if (tr) {
           msum.x += out.x;
           msum.y += out.y;
@@ -417,20 +455,31 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
   // ---------------- reductions ----------------
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (NT + 31) / 32;
   if (a.mode == MODE_LLG && a.stage == 4) {
-    double q[kNPart] = {wacc, (double)msum.x, (double)msum.y, (double)msum.z};
+    // one quantity at a time (few live registers): W_k of the compiled modes, then sum m
+    auto warp_sum = [&](double q, int k) {
 #pragma unroll
-    for (int k = 0; k < kNPart; ++k) {
+      for (int o = 16; o > 0; o >>= 1) q += __shfl_down_sync(0xffffffffu, q, o);
+      if (lane == 0) red[warp * kNPart + k] = q;
+    };
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) q[k] += __shfl_down_sync(0xffffffffu, q[k], o);
+    for (int k = 0; k < kMaxModes; ++k) {
+      if (k < MM)
+        warp_sum(wacc[k < MM ? k : 0], k);
+      else if (lane == 0)
+        red[warp * kNPart + k] = 0.0;
     }
-    if (lane == 0)
-#pragma unroll
-      for (int k = 0; k < kNPart; ++k) red[warp * kNPart + k] = q[k];
+    if (tr) {
+      warp_sum((double)msum.x, kPartM);
+      warp_sum((double)msum.y, kPartM + 1);
+      warp_sum((double)msum.z, kPartM + 2);
+    }
     __syncthreads();
-    if (threadIdx.x < kNPart) {  // fixed order over the warps: deterministic
+    if (threadIdx.x < kNPart) {  // fixed order over the warps: deterministic; [q][CTA] layout
       double s = 0.0;
-      for (int w = 0; w < nw; ++w) s += red[w * kNPart + threadIdx.x];
-      a.partials[(blockIdx.y * gridDim.x + blockIdx.x) * kNPart + threadIdx.x] = s;
+      if (threadIdx.x < kPartM || tr)
+        for (int w = 0; w < nw; ++w) s += red[w * kNPart + threadIdx.x];
+      const int nps = gridDim.x * gridDim.y;
+      a.partials[threadIdx.x * nps + blockIdx.y * gridDim.x + blockIdx.x] = s;
     }
   }
   if (a.mode == MODE_MAXTORQUE) {
@@ -506,82 +555,105 @@ void launch_update(const UpdateArgs& a, const float2* tw, cudaStream_t st) {
   MCQ_DISPATCH_N2(a.d.N2, {
     using Cf = UCfg<N2>;
     dim3 grid((a.d.ny + Cf::RY - 1) / Cf::RY, a.d.nz);
-    launch_pdl(a.d.pdl, k_update<N2>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
+    if (a.nmodes > 1)
+      launch_pdl(a.d.pdl, k_update<N2, kMaxModes>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
+    else
+      launch_pdl(a.d.pdl, k_update<N2, 1>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
   })
 }
 
 void configure_update_kernels() {
   for (int n = 2; n <= 512; n *= 2) {
     MCQ_DISPATCH_N2(n, {
-      cudaFuncSetAttribute(k_update<N2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UCfg<N2>::SMEM);
+      cudaFuncSetAttribute(k_update<N2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UCfg<N2>::SMEM);
+      cudaFuncSetAttribute(k_update<N2, kMaxModes>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UCfg<N2>::SMEM);
     })
   }
 }
 
 // ---------------------------------------------------------------- K-CAV
-// Stage factors for the step that starts at (alpha, t): Gamma(t + c dt) = 2 Re(e_c alpha)
-// (P:343 with S_n, C_n frozen, reading C3/C5), excitation a sinc(w_cut (t + c dt)) (C13).
+// Stage factors for the step that starts at (alpha_k, t): Gamma_k(t + c dt) = 2 Re(e_{k,c} alpha_k)
+// (P:343 with S_n, C_n frozen, reading C3/C5), excitation a_k sinc(w_k (t + c dt)) (C13), per mode.
 __device__ void cav_prepare(const CavParams& p, CavState* st) {
   const double c[4] = {0.0, 0.5, 0.5, 1.0};
   const int ci[4] = {0, 1, 1, 2};
-  for (int s = 0; s < 4; ++s) {
-    const double er = p.ec_re[ci[s]], ei = p.ec_im[ci[s]];
-    const double g = 2.0 * (er * st->re - ei * st->im);
-    const double x = p.exc_omega * (st->t + c[s] * p.dt);
-    const double sc = (x == 0.0) ? 1.0 : sin(x) / x;
-    st->gc[s] = (float)(p.cav_on ? g : 0.0);
-    st->ge[s] = (float)(p.exc_amp * sc);
-  }
+  for (int k = 0; k < p.nmodes; ++k)
+    for (int s = 0; s < 4; ++s) {
+      const double er = p.ec_re[k][ci[s]], ei = p.ec_im[k][ci[s]];
+      const double g = 2.0 * (er * st->re[k] - ei * st->im[k]);
+      const double x = p.exc_omega[k] * (st->t + c[s] * p.dt);
+      const double sc = (x == 0.0) ? 1.0 : sin(x) / x;
+      st->gc[k][s] = (float)(p.cav_on[k] ? g : 0.0);
+      st->ge[k][s] = (float)(p.exc_amp[k] * sc);
+    }
 }
 
 __global__ void k_cav_prepare(CavParams p, CavState* st) {
   if (threadIdx.x == 0 && blockIdx.x == 0) cav_prepare(p, st);
 }
 
-// Fixed-order reduction of the per-CTA partials (deterministic), then
-// alpha_{n+1} = e^{-(kappa + i w) dt} alpha_n + i (V_c/hbar) W_{n+1} dt, t += dt (a13).
-__global__ void __launch_bounds__(1024) k_cavity(CavParams p, CavState* st, const double* __restrict__ partials,
-                                                 int n) {
-  __shared__ double red[kNPart][1024];
+// Fixed-order reduction of the per-CTA partials (deterministic), then per mode
+// alpha_{n+1} = e^{-(kappa + i w) dt} alpha_n + i (V_c/hbar) W_{n+1} dt; t += dt (a13).
+// partials: per slab [kNPart][nps] (slab-major, global CTA order i = slab * nps + b).
+constexpr int kCavThreads = 1024;
+__global__ void __launch_bounds__(kCavThreads) k_cavity(CavParams p, CavState* st, const double* __restrict__ partials,
+                                                        int n, int nps) {
+  __shared__ double red[kNPart][kCavThreads / 32];
   pdl_trigger();
   pdl_wait();
-  const int nq = p.trace ? kNPart : 1;  // the spatial sums only when the trace records
-  double s[kNPart] = {0.0, 0.0, 0.0, 0.0};
-  for (int i = threadIdx.x; i < n; i += 1024)
+  bool use[kNPart];  // the overlaps of the active modes; the spatial sums when the trace records
+#pragma unroll
+  for (int k = 0; k < kNPart; ++k) use[k] = k < kMaxModes ? k < p.nmodes : p.trace != nullptr;
+  double s[kNPart];
+#pragma unroll
+  for (int k = 0; k < kNPart; ++k) s[k] = 0.0;
+  for (int i = threadIdx.x; i < n; i += kCavThreads) {
+    const int r = i / nps, b = i - r * nps;
+    const double* pr = partials + (size_t)r * kNPart * nps + b;
 #pragma unroll
     for (int k = 0; k < kNPart; ++k)
-      if (k < nq) s[k] += partials[i * kNPart + k];
-#pragma unroll
-  for (int k = 0; k < kNPart; ++k) red[k][threadIdx.x] = s[k];
-  __syncthreads();
-  for (int w = 512; w > 0; w >>= 1) {
-    if (threadIdx.x < w)
-#pragma unroll
-      for (int k = 0; k < kNPart; ++k)
-        if (k < nq) red[k][threadIdx.x] += red[k][threadIdx.x + w];
-    __syncthreads();
+      if (use[k]) s[k] += pr[(size_t)k * nps];
   }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < kNPart; ++k) {
+    if (use[k]) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s[k] += __shfl_down_sync(0xffffffffu, s[k], o);
+      if (lane == 0) red[k][warp] = s[k];
+    }
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    const double W = p.cav_on ? p.Ms * red[0][0] : 0.0;
-    const double er = p.ec_re[2], ei = p.ec_im[2];
-    const double re = er * st->re - ei * st->im;
-    const double im = er * st->im + ei * st->re + p.vc_over_hbar * W * p.dt;
-    st->re = re;
-    st->im = im;
+    double tot[kNPart];
+#pragma unroll
+    for (int k = 0; k < kNPart; ++k) {
+      tot[k] = 0.0;
+      if (use[k])
+        for (int w = 0; w < kCavThreads / 32; ++w) tot[k] += red[k][w];
+    }
+    for (int k = 0; k < p.nmodes; ++k) {
+      const double W = p.cav_on[k] ? p.Ms * tot[k] : 0.0;
+      const double er = p.ec_re[k][2], ei = p.ec_im[k][2];
+      const double re = er * st->re[k] - ei * st->im[k];
+      const double im = er * st->im[k] + ei * st->re[k] + p.vc_over_hbar * W * p.dt;
+      st->re[k] = re;
+      st->im[k] = im;
+      st->W[k] = W;
+    }
     st->t += p.dt;
-    st->W = W;
     st->step += 1;
     if (p.trace && st->step % p.trace_every == 0) {  // NEXT-3: the per-step observables
       const long long r = st->trace_rows;
       if (r < p.trace_cap) {
         double* row = p.trace + r * kTraceCols;
         row[0] = st->t;
-        row[1] = red[1][0] * p.inv_nmag;
-        row[2] = red[2][0] * p.inv_nmag;
-        row[3] = red[3][0] * p.inv_nmag;
-        row[4] = re;
-        row[5] = im;
-        row[6] = p.Ms * red[0][0];
+        row[1] = tot[kPartM] * p.inv_nmag;
+        row[2] = tot[kPartM + 1] * p.inv_nmag;
+        row[3] = tot[kPartM + 2] * p.inv_nmag;
+        row[4] = st->re[0];
+        row[5] = st->im[0];
+        row[6] = p.Ms * tot[0];
         row[7] = (double)st->step;
       }
       st->trace_rows = r + 1;
@@ -590,8 +662,8 @@ __global__ void __launch_bounds__(1024) k_cavity(CavParams p, CavState* st, cons
   }
 }
 
-void launch_cavity(const CavParams& p, CavState* st, const double* partials, int n, cudaStream_t s) {
-  launch_pdl(p.pdl, k_cavity, dim3(1), dim3(1024), 0, s, p, st, partials, n);
+void launch_cavity(const CavParams& p, CavState* st, const double* partials, int n, int nps, cudaStream_t s) {
+  launch_pdl(p.pdl, k_cavity, dim3(1), dim3(kCavThreads), 0, s, p, st, partials, n, nps);
 }
 
 void launch_cav_prepare(const CavParams& p, CavState* st, cudaStream_t s) {
