@@ -47,11 +47,17 @@ __device__ __forceinline__ void pass_tw(float2* tw, const float2* __restrict__ g
 // CW > 0: a configuration with CW columns per CTA (a separate narrow launch for the last kx
 // column beyond the final 16-column tile was measured slower: the extra kernel boundary costs
 // more than the mostly idle tile it replaces)
+#ifndef MCQ_YE
+#define MCQ_YE 16   // points per thread per line in K-Y / K-YI
+#endif
+#ifndef MCQ_YNT
+#define MCQ_YNT 256  // target threads per CTA in K-Y / K-YI
+#endif
 template <int L, int CW = 0>
 struct PassCfg {  // single-component passes (K-Y, K-YI)
-  static constexpr int E = L < 16 ? L : 16;
+  static constexpr int E = L < MCQ_YE ? L : MCQ_YE;
   static constexpr int TL = L / E;
-  static constexpr int C0 = 256 / TL;
+  static constexpr int C0 = MCQ_YNT / TL;
   static constexpr int C = CW > 0 ? CW : (C0 < 8 ? 8 : (C0 > 64 ? 64 : C0));
   static constexpr int NT = C * TL;
   static constexpr int TWN = pass_twn<L, E>();  // twiddle table (complex)
@@ -218,11 +224,14 @@ __global__ void __launch_bounds__(ZCfg<L>::NT) k_conv(float2* __restrict__ Y, co
 #ifndef MCQ_ZPF
 #define MCQ_ZPF 1   // load component g+1 before transforming g (with ZTAB: 123.3 vs 127.3 us)
 #endif
+#ifndef MCQ_ZNT
+#define MCQ_ZNT 256  // target threads per CTA in K-Z
+#endif
 template <int L, int CW = 0>
 struct ZSCfg {
   static constexpr int E = L <= MCQ_ZSE ? L : MCQ_ZSE;
   static constexpr int TL = L / E;
-  static constexpr int C0 = 256 / TL;
+  static constexpr int C0 = MCQ_ZNT / TL;
   static constexpr int C = CW > 0 ? CW : (C0 < 4 ? 4 : (C0 > 64 ? 64 : C0));
   static constexpr int NT = C * TL;
   static constexpr int TWS = MCQ_ZTAB ? 0 : 1;

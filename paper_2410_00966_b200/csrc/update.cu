@@ -75,12 +75,13 @@ struct RowAddr {  // shared-memory address of element pos of component-line l of
 };
 
 // One cell from register inputs: state m, in-mesh neighbours nb[k] (valid where ok[k]), m_n,
-// the RK4 accumulator so far, the cavity + excitation field bcav = sum_k B_rms,k (Gamma_k +
-// a_k sinc) (added iff has_cav) and the demag field.  Computes B' and, by mode, the field (Bout),
+// the RK4 accumulator so far, the cavity + excitation field bcav * gmul (added iff gmul != 0:
+// B_rms * (Gamma + a sinc) for one mode, or the summed field of all modes with gmul = 1) and
+// the demag field.  Computes B' and, by mode, the field (Bout),
 // the max torque, or the RK4 stage update (returns m_{s+1}, writes the new accumulator to
 // acc_out).  All memory traffic (and the overlap sums) stays in the caller.
 __device__ __forceinline__ float3 cell_core(const UpdateArgs& a, float3 m, const float3 (&nb)[6], const bool (&ok)[6],
-                                            float3 mn, float3 ap, float3 bcav, bool has_cav, float3 Bd,
+                                            float3 mn, float3 ap, float3 bcav, float gmul, float3 Bd,
                                             float& tmax, float3& acc_out, float3& Bout) {
   if (a.mode == MODE_X0) return m;
   float3 B = make_float3(0.f, 0.f, 0.f);
@@ -125,10 +126,10 @@ __device__ __forceinline__ float3 cell_core(const UpdateArgs& a, float3 m, const
         B.z += f1 * a.c1[2] + f2 * a.c2[2] + f3 * a.c3[2];
       }
     }
-    if (has_cav) {
-      B.x += bcav.x;
-      B.y += bcav.y;
-      B.z += bcav.z;
+    if (gmul != 0.f) {
+      B.x += bcav.x * gmul;
+      B.y += bcav.y * gmul;
+      B.z += bcav.z * gmul;
     }
   }
   if (a.mode == MODE_FIELD) {
@@ -329,8 +330,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
   for (int k = 0; k < MM; ++k) wacc[k] = 0.0;
   const bool wsum = a.mode == MODE_LLG && a.stage == 4;  // overlaps of m_{n+1}
   float tmax = 0.f;
-  float3 msum = make_float3(0.f, 0.f, 0.f);  // stage 4 with the trace on: sum of m_{n+1}
-  const bool tr = a.trace && a.mode == MODE_LLG && a.stage == 4;
+  const bool tr = a.trace && a.mode == MODE_LLG && a.stage == 4;  // sum m_{n+1} for the trace
   const unsigned rowbase = (unsigned)nx * (y + (unsigned)ny * zs);  // 32-bit indices (< 2^32 elements)
   const unsigned Nu = (unsigned)N;
   const float* trow = tc + (yl + 1) * nxp;  // this row inside the z tile
@@ -397,16 +397,21 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
         const float3 br = make_float3(MCQ_PICK(br2[0]), MCQ_PICK(br2[1]), MCQ_PICK(br2[2]));
         const float3 Bd = make_float3(MCQ_PICK(v[0][i]), MCQ_PICK(v[1][i]), MCQ_PICK(v[2][i]));
         float3 accn = make_float3(0.f, 0.f, 0.f), Bf = make_float3(0.f, 0.f, 0.f);
-        float3 bcav = make_float3(br.x * gsum, br.y * gsum, br.z * gsum);
+        float3 out;
+        if constexpr (MM == 1) {
+          out = cell_core(a, m, nb, ok, mn, ap, br, gsum, Bd, tmax, accn, Bf);
+        } else {
+          float3 bcav = make_float3(br.x * gsum, br.y * gsum, br.z * gsum);
 #pragma unroll
-        for (int k = 1; k < MM; ++k) {
-          if (k < nm) {
-            bcav.x += MCQ_PICK(bk2[k - 1][0]) * gs[k];
-            bcav.y += MCQ_PICK(bk2[k - 1][1]) * gs[k];
-            bcav.z += MCQ_PICK(bk2[k - 1][2]) * gs[k];
+          for (int k = 1; k < MM; ++k) {
+            if (k < nm) {
+              bcav.x += MCQ_PICK(bk2[k - 1][0]) * gs[k];
+              bcav.y += MCQ_PICK(bk2[k - 1][1]) * gs[k];
+              bcav.z += MCQ_PICK(bk2[k - 1][2]) * gs[k];
+            }
           }
+          out = cell_core(a, m, nb, ok, mn, ap, bcav, any_cav ? 1.f : 0.f, Bd, tmax, accn, Bf);
         }
-        const float3 out = cell_core(a, m, nb, ok, mn, ap, bcav, MM > 1 ? any_cav : gsum != 0.f, Bd, tmax, accn, Bf);
         if (wsum) {
           wacc[0] += (double)(br.x * out.x) + (double)(br.y * out.y) + (double)(br.z * out.z);
 #pragma unroll
@@ -416,11 +421,6 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
                          (double)(MCQ_PICK(bk2[k - 1][2]) * out.z);
         }
 #undef MCQ_PICK
-        if (tr) {
-          msum.x += out.x;
-          msum.y += out.y;
-          msum.z += out.z;
-        }
         if (h) {
           o[0].y = out.x; o[1].y = out.y; o[2].y = out.z;
           acc2[0].y = accn.x; acc2[1].y = accn.y; acc2[2].y = accn.z;
@@ -454,6 +454,15 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
 
   // ---------------- reductions ----------------
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (NT + 31) / 32;
+  float3 msum = make_float3(0.f, 0.f, 0.f);  // from the packed new state in v (0 outside the mesh)
+  if (tr) {
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      msum.x += v[0][i].x + v[0][i].y;
+      msum.y += v[1][i].x + v[1][i].y;
+      msum.z += v[2][i].x + v[2][i].y;
+    }
+  }
   if (a.mode == MODE_LLG && a.stage == 4) {
     // one quantity at a time (few live registers): W_k of the compiled modes, then sum m
     auto warp_sum = [&](double q, int k) {
@@ -608,7 +617,7 @@ __global__ void __launch_bounds__(kCavThreads) k_cavity(CavParams p, CavState* s
 #pragma unroll
   for (int k = 0; k < kNPart; ++k) s[k] = 0.0;
   for (int i = threadIdx.x; i < n; i += kCavThreads) {
-    const int r = i / nps, b = i - r * nps;
+    const int r = n == nps ? 0 : i / nps, b = i - r * nps;
     const double* pr = partials + (size_t)r * kNPart * nps + b;
 #pragma unroll
     for (int k = 0; k < kNPart; ++k)
