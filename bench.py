@@ -262,7 +262,7 @@ def main():
 
     # per-kernel timing (CUDA events around each launch, same stream) -> roofline of the top kernel
     prof = mcq.mcq_profile_run(solver.ctx, cfg.dt, args.profile_steps)
-    ns = world if slab else 1
+    ns = world if slab else (args.loopback if args.loopback > 1 else 1)  # slabs per launch
     ab = alg_bytes(L, cfg.grid, cfg.brms_map is not None, ns)
     share = {k: v[0] * v[1] for k, v in prof.items() if v[1] > 0}
     top = max(share, key=share.get)

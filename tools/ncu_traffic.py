@@ -11,17 +11,17 @@ import os
 import subprocess
 import sys
 
-CLASS = [("k_ypass<", ", 0>", "yfwd"), ("k_ypass<", ", 1>", "yinv"), ("k_zconv", "", "zconv"),
-         ("k_conv<", ", 1>", "y2d"), ("k_conv<", ", 0>", "zconv"), ("k_update", "", "update"),
-         ("k_cavity", "", "cavity")]
-
-
 def classify(name):
-    for pre, post, k in CLASS:
-        if name.startswith("void " + pre) or name.startswith(pre):
-            if not post or post in name.split("(")[0]:
-                return k
-    return None
+    """Kernel class of an ncu kernel name (template arguments: k_ypass<L, INV, ...>,
+    k_conv<L, Y2D>)."""
+    n = name.split("(")[0].replace("void ", "").replace("mcq::", "").strip()
+    base = n.split("<")[0]
+    targs = [x.strip(" >") for x in n.split("<", 1)[1].split(",")] if "<" in n else []
+    if base == "k_ypass":
+        return "yinv" if len(targs) > 1 and targs[1] in ("1", "true") else "yfwd"
+    if base == "k_conv":
+        return "y2d" if len(targs) > 1 and targs[1] in ("1", "true") else "zconv"
+    return {"k_zconv_seq": "zconv", "k_zconv_tma": "zconv", "k_update": "update", "k_cavity": "cavity"}.get(base)
 
 
 def main(rep, out, key):
