@@ -192,10 +192,14 @@ def main():
                     help="N > 1: z-slab decomposition of one grid (strong) or independent replicas (weak)")
     ap.add_argument("--loopback", type=int, default=0,
                     help="N == 1: run the decomposed schedule with this many z slabs on the one GPU")
+    ap.add_argument("--batch", type=int, default=1,
+                    help="independent replicas per GPU (one bias point each, own stream; latency-bound grids)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
         return run_reference(args)
+    if args.batch > 1:  # more hardware work queues than the default 8 for concurrent replica streams
+        os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
     import torch
     import torch.distributed as dist
@@ -213,37 +217,59 @@ def main():
     from paper_2410_00966_b200.slabs import slab_dist
     cfg = make_config(args.config)
     slab = world > 1 and args.decomp == "slab"
-    if world > 1 and not slab:
-        cfg.bext = replica_bias(cfg.bext, world, rank)  # replica r: its bias-field sweep point
-    stream = torch.cuda.Stream()          # a real stream: the library's kernels and our events share it
+    R = max(1, args.batch) if not slab and args.loopback <= 1 else 1
+    # replica (rank, j): its own bias point of the sweep (replicas for small grids)
+    bext0 = cfg.bext
+    streams, solvers = [], []
+    for j in range(R):
+        if (world > 1 and not slab) or R > 1:
+            cfg.bext = replica_bias(bext0, world * R, rank * R + j)
+        s_j = torch.cuda.Stream()         # a real stream: the library's kernels and our events share it
+        dd = slab_dist(rank, world, local) if slab else None
+        if world == 1 and args.loopback > 1:
+            dd = {"rank": -1, "world": args.loopback}
+        sv = mcq.Solver.from_config(cfg, stream=s_j.cuda_stream, dist=dd)
+        if cfg.relax_first:
+            sv.relax(cfg.dt * 0.5, 1e-3, 2000)
+            mcq.mcq_reset_memory(sv.ctx)
+        streams.append(s_j)
+        solvers.append(sv)
+    stream, solver = streams[0], solvers[0]
     torch.cuda.set_stream(stream)
-    dd = slab_dist(rank, world, local) if slab else None
-    if world == 1 and args.loopback > 1:
-        dd = {"rank": -1, "world": args.loopback}
-    solver = mcq.Solver.from_config(cfg, stream=stream.cuda_stream, dist=dd)
-    jobs = 1 if slab else world           # grids the job advances per step
-    if cfg.relax_first:
-        solver.relax(cfg.dt * 0.5, 1e-3, 2000)
-        mcq.mcq_reset_memory(solver.ctx)
+    jobs = (1 if slab else world) * R     # grids the job advances per step
     L = mcq.mcq_debug_layout(solver.ctx)
 
     def barrier():
+        # drain this rank's work (incl. libmcq's own NCCL calls) before torch's collective, so
+        # the two communicators never have kernels in flight at the same time
+        torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
+    def run_all(steps):  # every replica on its own stream, fork / join through events
+        fork = torch.cuda.Event()
+        fork.record(stream)
+        for s_j, sv in zip(streams, solvers):
+            s_j.wait_event(fork)
+            sv.run(cfg.dt, steps)
+        for s_j in streams[1:]:
+            join = torch.cuda.Event()
+            join.record(s_j)
+            stream.wait_event(join)
+
     # warm-up (captures the graphs)
-    solver.run(cfg.dt, args.warmup)
+    run_all(args.warmup)
     barrier()
-    launches0 = mcq.mcq_kernel_launches(solver.ctx)
+    launches0 = sum(mcq.mcq_kernel_launches(sv.ctx) for sv in solvers)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
         ev0.record(stream)
-        solver.run(cfg.dt, args.steps)
+        run_all(args.steps)
         ev1.record(stream)
         barrier()
-    launches = mcq.mcq_kernel_launches(solver.ctx) - launches0
+    launches = sum(mcq.mcq_kernel_launches(sv.ctx) for sv in solvers) - launches0
     ms_max = max_over_ranks(ev0.elapsed_time(ev1), device="cuda")
     value = cfg.n * args.steps * jobs / (ms_max * 1e-3)
 
@@ -253,9 +279,12 @@ def main():
     e2e_steps = args.steps
     barrier()
     t0 = time.perf_counter()
-    mcq.mcq_set_m(solver.ctx, m_host.numpy())
-    solver.run(cfg.dt, e2e_steps)
-    mcq.mcq_get_m(solver.ctx, cfg.n, out_host.numpy().reshape(-1))
+    for sv in solvers:
+        mcq.mcq_set_m(sv.ctx, m_host.numpy())
+    for sv in solvers:
+        sv.run(cfg.dt, e2e_steps)
+    for sv in solvers:
+        mcq.mcq_get_m(sv.ctx, cfg.n, out_host.numpy().reshape(-1))
     torch.cuda.synchronize()
     e2e_s = max_over_ranks(time.perf_counter() - t0, device="cuda")
     e2e_val = cfg.n * e2e_steps * jobs / e2e_s
@@ -282,6 +311,7 @@ def main():
                        "parallelism": (f"z-slab x{world} (NCCL)" if slab else f"replicas x{world}")
                        if world > 1 else (f"single GPU, loopback z-slab x{args.loopback}"
                                           if args.loopback > 1 else "single GPU"),
+                       "replicas_per_gpu": R,
                        "l2": "working set > 126 MB L2 every step (no flush needed)",
                        "padded_fft": [L["Lx"], L["Ly"], L["Lz"]]},
             "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": pk["hbm_gbs"],
@@ -304,7 +334,8 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             res["cpu_baseline"] = cpu_baseline(cfg)
         print(json.dumps(res), flush=True)
-    solver.close()
+    for sv in solvers:
+        sv.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -1,16 +1,6 @@
-mkdir -p gpurun_out/final
-cd $GRAFT_REPO_ROOT
-nvidia-smi --query-gpu=name,clocks.max.sm,clocks.sm,power.limit --format=csv > gpurun_out/final/gpu.txt 2>&1
-timeout 900 python bench.py > gpurun_out/final/bench_c1.json 2> gpurun_out/final/bench_c1.err
-timeout 600 python bench.py --config 3 --steps 300 --warmup 10 --no-cpu-baseline > gpurun_out/final/bench_c3.json 2>&1
-timeout 600 python bench.py --config 0 --steps 2000 --warmup 20 --no-cpu-baseline > gpurun_out/final/bench_c0.json 2>&1
-timeout 600 python bench.py --config 2 --steps 500 --warmup 10 --no-cpu-baseline > gpurun_out/final/bench_c2.json 2>&1
-timeout 900 python bench.py --config 4 --steps 20 --warmup 3 --no-cpu-baseline --profile-steps 2 > gpurun_out/final/bench_c4.json 2>&1
-timeout 600 python bench.py --loopback 4 --steps 300 --warmup 10 --no-cpu-baseline > gpurun_out/final/bench_c1_loop4.json 2>&1
-timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/final/bench_ref.json 2>&1
-python bench.py --steps 4 --warmup 3 --no-cpu-baseline --profile-steps 1 > gpurun_out/final/pre_launches.log 2>&1 && \
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/final/launches.csv python bench.py --steps 4 --warmup 3 --no-cpu-baseline --profile-steps 1 > gpurun_out/final/ncu_launches.log 2>&1
-python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/final/pre_full.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_zconv_seq|k_update|k_ypass|k_cavity" --launch-skip 40 -c 5 -o gpurun_out/final/r1_final_full python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/final/ncu_full.log 2>&1
-ls -la gpurun_out/final
-tail -c 400 gpurun_out/final/bench_c1.json
+mkdir -p gpurun_out
+for b in 1 8 32 64; do timeout 300 python bench.py --config 0 --steps 1000 --warmup 10 --no-cpu-baseline --batch $b > gpurun_out/bench48_b$b.log 2>&1; done
+timeout 300 python bench.py --steps 500 --warmup 10 --no-cpu-baseline > gpurun_out/bench48_c1.log 2>&1
+timeout 300 python bench.py --steps 300 --warmup 10 --no-cpu-baseline --loopback 4 > gpurun_out/bench48_l4.log 2>&1
+for f in b1 b8 b32 b64 c1 l4; do python -c "
+import json;d=json.loads(open('gpurun_out/bench48_$f.log').read().strip().splitlines()[-1]);print('$f',round(d['value']/1e9,4),round(d['ms_per_step'],4),d['gpu_launches'],d['roofline']['frac'],d['e2e']['value'])"; done
