@@ -20,7 +20,7 @@ from .constants import GAMMA, HBAR
 from . import fields as F
 from . import tensor as T
 from .cavity import CavityMemory
-from .llg import torque, relax_torque, normalize, rk4_step
+from .llg import torque, relax_torque, normalize, rk4_step, dp45_step, dp_controller
 
 ZEEMAN, EXCHANGE, ANIS, DEMAG, CAVITY, EXCITATION = 1, 2, 4, 8, 16, 32
 ALL = ZEEMAN | EXCHANGE | ANIS | DEMAG | CAVITY | EXCITATION
@@ -137,6 +137,41 @@ class Simulation:
         for _ in range(int(steps)):
             self.step(dt)
         return self.m
+
+    # ---------------------------------------------------------------- Dormand-Prince (NEXT-1)
+    def _advance_memory(self, dt):
+        W = self.W(self.m) if self.cavity_enabled else 0.0
+        self.mem.update(W, dt)
+        for b, mem, _, _ in self.extra:
+            Wk = float(np.sum(self.Ms * np.sum(self.m * b, axis=-1) * self.mag)) if np.any(b != 0) else 0.0
+            mem.update(Wk, dt)
+
+    def step_dp(self, dt):
+        """One fixed Dormand-Prince step (reading C-DP), memory advanced with this dt (C3-C5).
+        Returns the error estimate."""
+        self.m, err = dp45_step(self.rhs, self.m, self.mem.t, dt)
+        self._advance_memory(dt)
+        return err
+
+    def run_adaptive(self, duration, dt0, tol, max_attempts=10**6):
+        """Adaptive Dormand-Prince over `duration`: an attempt with err <= tol is accepted (state
+        and memory advance by its dt, the step variable of eq:Sdiscrete/eq:Cdiscrete), a rejected
+        one leaves both untouched; the next dt follows dp_controller, clipped to the end time.
+        Returns (accepted, rejected, dt_next, accepted dts)."""
+        t_end = self.mem.t + duration
+        dt, acc, rej, dts = dt0, 0, 0, []
+        while t_end - self.mem.t > 1e-12 * max(duration, 1e-30) and acc + rej < max_attempts:
+            h = min(dt, t_end - self.mem.t)
+            m_new, err = dp45_step(self.rhs, self.m, self.mem.t, h)
+            if err <= tol:
+                self.m = m_new
+                self._advance_memory(h)
+                acc += 1
+                dts.append(h)
+            else:
+                rej += 1
+            dt = dp_controller(h, err, tol)
+        return acc, rej, dt, dts
 
     # ---------------------------------------------------------------- relax (step 7)
     def max_torque(self, m=None):
