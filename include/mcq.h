@@ -178,6 +178,23 @@ MCQ_API int mcq_relax(mcq_ctx *, double dt, double torque_tol, long long max_ste
  * the context stream; returns without synchronising.  ESTATE before the first set_m. */
 MCQ_API int mcq_run(mcq_ctx *, double dt, long long steps);
 
+/* Dormand-Prince 5(4) (Mumax3 integrates with its own adaptive solvers,
+ * P:324).  Reading C-DP: standard DP tableau, every stage state renormalised (as C2), the
+ * 5th-order solution propagated, error estimate err = max_i |dt sum_j (b5_j - b4_j) k_j| (max
+ * over cells, fp32); the cavity memory is frozen inside a step at the stage nodes c_s (C3) and
+ * advanced by the accepted step's dt (eq:Sdiscrete with the step variable).  No FSAL reuse.
+ * mcq_run_dp: `steps` fixed steps of size dt (every step accepted; no graph, no host sync).
+ * mcq_run_adaptive: advances the cavity clock by `duration` (s) from its current value: an
+ * attempt with err <= tol (dimensionless, |m| = 1) is accepted, else m_n and the memory are
+ * left untouched; the next step is h * min(5, max(0.2, 0.9 (tol/err)^(1/5))), clipped to the
+ * end time; one 4-byte device-to-host read per attempt.  Stops after max_attempts attempts.
+ * *accepted, *rejected, *dt_next (each may be NULL) receive the counts and the proposed next
+ * step.  EINVAL on non-positive dt0 / tol; ESTATE before set_m.  Under NCCL the error is
+ * reduced with a max over ranks, so every rank takes the same decisions. */
+MCQ_API int mcq_run_dp(mcq_ctx *, double dt, long long steps);
+MCQ_API int mcq_run_adaptive(mcq_ctx *, double duration, double dt0, double tol, long long max_attempts,
+                             long long *accepted, long long *rejected, double *dt_next);
+
 /* Block until all enqueued work is done; reports asynchronous kernel errors (ECUDA). */
 MCQ_API int mcq_synchronize(mcq_ctx *);
 

@@ -166,6 +166,19 @@ def mcq_run(ctx, dt, steps):
     _check(ctx, lib.mcq_run(ctx, float(dt), int(steps)))
 
 
+def mcq_run_dp(ctx, dt, steps):
+    """Fixed-step Dormand-Prince 5(4) (include/mcq.h, NEXT-1)."""
+    _check(ctx, lib.mcq_run_dp(ctx, float(dt), int(steps)))
+
+
+def mcq_run_adaptive(ctx, duration, dt0, tol, max_attempts=10**7):
+    """Adaptive Dormand-Prince over `duration` s; returns (accepted, rejected, dt_next)."""
+    a, r, d = C.c_longlong(), C.c_longlong(), C.c_double()
+    _check(ctx, lib.mcq_run_adaptive(ctx, float(duration), float(dt0), float(tol), int(max_attempts),
+                                     C.byref(a), C.byref(r), C.byref(d)))
+    return a.value, r.value, d.value
+
+
 def mcq_synchronize(ctx):
     _check(ctx, lib.mcq_synchronize(ctx))
 

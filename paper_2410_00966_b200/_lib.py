@@ -71,6 +71,9 @@ _sig = {
     "mcq_set_cavity_state_mode": (C.c_int, [_P, C.c_int, C.POINTER(mcq_cavity_state)]),
     "mcq_relax": (C.c_int, [_P, C.c_double, C.c_double, C.c_longlong, C.POINTER(C.c_longlong)]),
     "mcq_run": (C.c_int, [_P, C.c_double, C.c_longlong]),
+    "mcq_run_dp": (C.c_int, [_P, C.c_double, C.c_longlong]),
+    "mcq_run_adaptive": (C.c_int, [_P, C.c_double, C.c_double, C.c_double, C.c_longlong, C.POINTER(C.c_longlong),
+                                   C.POINTER(C.c_longlong), C.POINTER(C.c_double)]),
     "mcq_synchronize": (C.c_int, [_P]),
     "mcq_get_m": (C.c_int, [_P, _P]),
     "mcq_get_m_device": (C.c_int, [_P, _P]),

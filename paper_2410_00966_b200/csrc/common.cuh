@@ -101,8 +101,8 @@ struct CavState {
   double t;                             // cavity clock t_n (shared)
   double W[kMaxModes];                  // overlaps of the last completed step
   long long step;
-  float gc[kMaxModes][4];  // Gamma_k(t_n + c_s dt) = 2 Re(e^{-(kappa_k+iw_k) c_s dt} alpha_k,n), s = 0..3
-  float ge[kMaxModes][4];  // a_k sinc(w_cut,k (t_n + c_s dt))
+  float gc[kMaxModes][8];  // Gamma_k(t_n + c_s dt) = 2 Re(e^{-(kappa_k+iw_k) c_s dt} alpha_k,n) per stage s
+  float ge[kMaxModes][8];  // a_k sinc(w_cut,k (t_n + c_s dt))
   long long trace_rows;    // trace rows recorded since the last reset (may exceed the capacity)
 };
 
@@ -114,7 +114,10 @@ constexpr int kTraceCols = 8;  // t, <mx>, <my>, <mz>, Re alpha, Im alpha, W, st
 
 // Scalars the cavity kernels need (host precomputed in fp64 for a given dt).
 struct CavParams {
-  double ec_re[kMaxModes][3], ec_im[kMaxModes][3];  // e^{-(kappa_k + i w_k) c dt}, c = 0, 1/2, 1
+  int nst;                                          // integrator stages (4: RK4, 7: Dormand-Prince)
+  double cst[8];                                    // stage nodes c_s
+  double ec_re[kMaxModes][8], ec_im[kMaxModes][8];  // e^{-(kappa_k + i w_k) c_s dt} per stage
+  double ecn_re[kMaxModes], ecn_im[kMaxModes];      // e^{-(kappa_k + i w_k) dt}: the step advance
   double vc_over_hbar;        // V_c / hbar
   double Ms;
   double dt;
@@ -128,7 +131,7 @@ struct CavParams {
   double inv_nmag;            // 1 / number of magnetic cells (spatial mean)
 };
 
-enum UpdateMode : int { MODE_LLG = 0, MODE_RELAX = 1, MODE_FIELD = 2, MODE_MAXTORQUE = 3, MODE_X0 = 4 };
+enum UpdateMode : int { MODE_LLG = 0, MODE_RELAX = 1, MODE_FIELD = 2, MODE_MAXTORQUE = 3, MODE_X0 = 4, MODE_DP = 5 };
 
 // Arguments of the fused update kernel K-U.
 struct UpdateArgs {
@@ -159,6 +162,12 @@ struct UpdateArgs {
   unsigned* maxbits;  // MODE_MAXTORQUE output (float bits, >= 0)
   int demag;          // run the x-C2R demag phase
   int trace;          // stage 4: also accumulate sum m for the trace
+  // MODE_DP (Dormand-Prince, reading C-DP), stage s = 1..7 with h = dt: K[j] = k_{j+1} ([3][cs]
+  // each), comb[j] (j < s) the weights of k_1..k_s: stages 1-6 write
+  // m_{s+1} = norm(m_n + h sum_j comb[j] k_{j+1}) and K[s-1] = k_s; stage 7 reduces
+  // max |h sum_j comb[j] k_{j+1}| (comb = b5 - b4) into maxbits and takes W of its own state
+  float* K;
+  float comb[8];
 };
 
 // ---------------------------------------------------------------- launchers

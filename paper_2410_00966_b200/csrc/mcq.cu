@@ -83,6 +83,7 @@ struct Slab {
   Dims d{};
   float *mN = nullptr, *mA = nullptr, *mB = nullptr, *acc = nullptr;  // [3][cs]
   float2 *X = nullptr, *Y = nullptr, *R = nullptr;  // X [3][nz][ny][P]; Y, R [NS][3][nz][Ly][KXS]
+  float* K = nullptr;  // Dormand-Prince slopes k_1..k_6, [6][3][cs] (allocated on first use)
   float* brms[kMaxModes] = {nullptr, nullptr, nullptr, nullptr};  // [3][cs] per mode (maps)
   float* field = nullptr;                           // [3][cs]
   uint8_t* mask = nullptr;                          // [nz][ny][nx]
@@ -177,17 +178,23 @@ void invalidate_graphs(mcq_ctx* c) {
   }
 }
 
-CavParams cav_params(const mcq_ctx* c, double dt) {
+// stage nodes c_s: classical RK4 (C1) and Dormand-Prince (C-DP)
+constexpr double kRK4Nodes[4] = {0.0, 0.5, 0.5, 1.0};
+constexpr double kDPNodes[7] = {0.0, 1.0 / 5, 3.0 / 10, 4.0 / 5, 8.0 / 9, 1.0, 1.0};
+
+CavParams cav_params(const mcq_ctx* c, double dt, bool dp = false) {
   CavParams p{};
-  const double cs[3] = {0.0, 0.5, 1.0};
+  p.nst = dp ? 7 : 4;
+  for (int s = 0; s < p.nst; ++s) p.cst[s] = dp ? kDPNodes[s] : kRK4Nodes[s];
   for (int k = 0; k < kMaxModes; ++k) {
     const double w = 2.0 * M_PI * c->fc[k];
-    for (int i = 0; i < 3; ++i) {
-      const double a = cs[i] * dt;
+    auto factor = [&](double a, double& re, double& im) {  // e^{-(kappa + i w) a}
       const double dec = std::exp(-c->kappa[k] * a);
-      p.ec_re[k][i] = dec * std::cos(w * a);
-      p.ec_im[k][i] = -dec * std::sin(w * a);
-    }
+      re = dec * std::cos(w * a);
+      im = -dec * std::sin(w * a);
+    };
+    for (int s = 0; s < p.nst; ++s) factor(p.cst[s] * dt, p.ec_re[k][s], p.ec_im[k][s]);
+    factor(dt, p.ecn_re[k], p.ecn_im[k]);
     p.exc_amp[k] = c->exc_amp[k];
     p.exc_omega[k] = c->exc_omega[k];
     p.cav_on[k] = (k < c->nmodes && c->cav_on[k]) ? 1 : 0;
@@ -415,6 +422,50 @@ struct Enq {
     for (int st = 1; st <= 4; ++st)
       stage(st, dt, MODE_RELAX, MCQ_TERM_ALL & ~(MCQ_TERM_CAVITY | MCQ_TERM_EXCITATION));
   }
+  // ---------------- Dormand-Prince (reading C-DP): 7 stages, state buffers mN -> mA -> mB -> ...
+  // stage s reads the state s-1 wrote (stage 1: m_n) and writes m_{s+1} to mA (s odd) / mB (s
+  // even); stage 6 writes the step result y5 to mB, stage 7 evaluates k7 on it for the error
+  void dp_stage(int st, double dt) {
+    static const double A[7][7] = {
+        {1.0 / 5},
+        {3.0 / 40, 9.0 / 40},
+        {44.0 / 45, -56.0 / 15, 32.0 / 9},
+        {19372.0 / 6561, -25360.0 / 2187, 64448.0 / 6561, -212.0 / 729},
+        {9017.0 / 3168, -355.0 / 33, 46732.0 / 5247, 49.0 / 176, -5103.0 / 18656},
+        {35.0 / 384, 0.0, 500.0 / 1113, 125.0 / 192, -2187.0 / 6784, 11.0 / 84},
+        {35.0 / 384 - 5179.0 / 57600, 0.0, 500.0 / 1113 - 7571.0 / 16695, 125.0 / 192 - 393.0 / 640,
+         -2187.0 / 6784 + 92097.0 / 339200, 11.0 / 84 - 187.0 / 2100, -1.0 / 40}};  // b5 - b4
+    const int in = st == 1 ? 0 : ((st - 1) % 2 == 1 ? 1 : 2);
+    halo(in);
+    demag();
+    for (auto& sl : c->sl) {
+      UpdateArgs a = base_args(c, sl);
+      a.mode = MODE_DP;
+      a.stage = st;
+      a.mN = sl.mN;
+      a.mS = in == 0 ? sl.mN : (in == 1 ? sl.mA : sl.mB);
+      a.mOut = st % 2 == 1 ? sl.mA : sl.mB;
+      a.h = (float)dt;
+      a.K = sl.K;
+      for (int j = 0; j < st; ++j) a.comb[j] = (float)A[st - 1][j];
+      update(a);
+    }
+  }
+  void dp_attempt(double dt) {
+    for (int st = 1; st <= 6; ++st) dp_stage(st, dt);
+    if (cudaMemsetAsync(c->maxbits, 0, 4, s) != cudaSuccess && rc == MCQ_OK) rc = fail(c, MCQ_ECUDA, "memset");
+    dp_stage(7, dt);
+    if (c->mode == 2)  // max over ranks (non-negative floats: the float order is the bit order)
+      nk(nccl_api()->allReduce(c->maxbits, c->maxbits, 1, ncclFloat, ncclMax, c->comm, s));
+  }
+  void dp_commit(double dt) {  // m_n <- y5; every mode's alpha advances by dt on W(y5)
+    for (auto& sl : c->sl) copy(sl.mN, sl.mB, 3ULL * sl.d.cs * sizeof(float));
+    gather_partials();
+    const CavParams p = cav_params(c, dt, true);
+    pre(MCQ_K_CAVITY);
+    launch_cavity(p, c->cav, c->partials, c->nparts, c->sl[0].nparts, s);
+    post(MCQ_K_CAVITY);
+  }
   void x0() {  // X <- R2C(m_n) in every slab
     for (auto& sl : c->sl) {
       UpdateArgs a = base_args(c, sl);
@@ -567,7 +618,8 @@ int build_khat(mcq_ctx* c, double* oct_out /* optional host copy of the octant *
 void free_all(mcq_ctx* c) {
   invalidate_graphs(c);
   for (auto& s : c->sl) {
-    void* ptrs[] = {s.mN, s.mA, s.mB, s.acc, s.X, s.Y, s.R, s.brms[0], s.brms[1], s.brms[2], s.brms[3], s.field, s.mask};
+    void* ptrs[] = {s.mN, s.mA, s.mB, s.acc, s.X, s.Y, s.R, s.K, s.brms[0], s.brms[1], s.brms[2], s.brms[3],
+                    s.field, s.mask};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (c->mode == 2 && s.partials) cudaFree(s.partials);
@@ -1058,6 +1110,78 @@ int mcq_relax(mcq_ctx* c, double dt, double tol, long long max_steps, long long*
   }
   if (taken) *taken = done;
   return reset_memory(c);
+}
+
+static int ensure_dp(mcq_ctx* c) {
+  for (auto& s : c->sl)
+    if (!s.K) {
+      CK(c, cudaMalloc(&s.K, 6ULL * 3 * s.d.cs * sizeof(float)));
+      CK(c, cudaMemsetAsync(s.K, 0, 6ULL * 3 * s.d.cs * sizeof(float), c->stream));
+    }
+  return MCQ_OK;
+}
+
+int mcq_run_dp(mcq_ctx* c, double dt, long long steps) {
+  if (!c) return MCQ_EINVAL;
+  if (!(dt > 0) || steps < 0) return fail(c, MCQ_EINVAL, "dt must be > 0 and steps >= 0");
+  if (!c->m_set) return fail(c, MCQ_ESTATE, "mcq_run_dp before mcq_set_m");
+  int rc = ensure_dp(c);
+  if (rc != MCQ_OK) return rc;
+  Enq q{c, c->stream};
+  for (long long i = 0; i < steps; ++i) {
+    launch_cav_prepare(cav_params(c, dt, true), c->cav, c->stream);
+    q.dp_attempt(dt);
+    q.dp_commit(dt);
+    if (q.rc != MCQ_OK) return q.rc;
+  }
+  c->launches += q.count + steps;
+  CK(c, cudaGetLastError());
+  return MCQ_OK;
+}
+
+int mcq_run_adaptive(mcq_ctx* c, double duration, double dt0, double tol, long long max_attempts,
+                     long long* accepted, long long* rejected, double* dt_next) {
+  if (!c) return MCQ_EINVAL;
+  if (!(duration >= 0) || !(dt0 > 0) || !(tol > 0) || max_attempts < 0)
+    return fail(c, MCQ_EINVAL, "adaptive: duration >= 0, dt0 > 0, tol > 0, max_attempts >= 0");
+  if (!c->m_set) return fail(c, MCQ_ESTATE, "mcq_run_adaptive before mcq_set_m");
+  int rc = ensure_dp(c);
+  if (rc != MCQ_OK) return rc;
+  CavState h{};
+  if ((rc = read_cav_state(c, h)) != MCQ_OK) return rc;
+  const double t_end = h.t + duration;
+  double t = h.t, dt = dt0;
+  long long acc = 0, rej = 0;
+  Enq q{c, c->stream};
+  while (t_end - t > 1e-12 * std::max(duration, 1e-30) && acc + rej < max_attempts) {
+    const double step = std::min(dt, t_end - t);
+    launch_cav_prepare(cav_params(c, step, true), c->cav, c->stream);
+    q.dp_attempt(step);
+    if (q.rc != MCQ_OK) return q.rc;
+    unsigned bits = 0;
+    CK(c, cudaMemcpyAsync(&bits, c->maxbits, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    float err;
+    std::memcpy(&err, &bits, 4);
+    if (!std::isfinite(err)) return fail(c, MCQ_ECUDA, "non-finite error estimate");
+    if ((double)err <= tol) {  // accept: state and memory advance by this step
+      q.dp_commit(step);
+      t += step;
+      ++acc;
+    } else {  // reject: m_n untouched; restore its spectrum
+      q.x0();
+      ++rej;
+    }
+    if (q.rc != MCQ_OK) return q.rc;
+    // controller (reading C-DP): safety 0.9, growth in [0.2, 5]
+    dt = err > 0 ? step * std::min(5.0, std::max(0.2, 0.9 * std::pow(tol / (double)err, 0.2))) : step * 5.0;
+  }
+  c->launches += q.count + acc + rej;
+  if (accepted) *accepted = acc;
+  if (rejected) *rejected = rej;
+  if (dt_next) *dt_next = dt;
+  CK(c, cudaGetLastError());
+  return MCQ_OK;
 }
 
 int mcq_synchronize(mcq_ctx* c) {

@@ -80,6 +80,7 @@ struct RowAddr {  // shared-memory address of element pos of component-line l of
 // the demag field.  Computes B' and, by mode, the field (Bout),
 // the max torque, or the RK4 stage update (returns m_{s+1}, writes the new accumulator to
 // acc_out).  All memory traffic (and the overlap sums) stays in the caller.
+template <bool DPM>
 __device__ __forceinline__ float3 cell_core(const UpdateArgs& a, float3 m, const float3 (&nb)[6], const bool (&ok)[6],
                                             float3 mn, float3 ap, float3 bcav, float gmul, float3 Bd,
                                             float& tmax, float3& acc_out, float3& Bout) {
@@ -143,7 +144,7 @@ __device__ __forceinline__ float3 cell_core(const UpdateArgs& a, float3 m, const
   }
   const float3 mmxB = cross3(m, mxB);
   float3 k;
-  if (a.mode == MODE_LLG) {
+  if (a.mode == MODE_LLG || (DPM && a.mode == MODE_DP)) {
     k = make_float3(-a.gl * (mxB.x + a.alpha * mmxB.x), -a.gl * (mxB.y + a.alpha * mmxB.y),
                     -a.gl * (mxB.z + a.alpha * mmxB.z));
   } else {  // MODE_RELAX: -gamma m x (m x B)
@@ -151,6 +152,17 @@ __device__ __forceinline__ float3 cell_core(const UpdateArgs& a, float3 m, const
   }
   const int stage = a.stage;
   if (stage == 1) mn = m;
+  if (DPM && a.mode == MODE_DP) {  // ap = sum_{j < s} comb[j-1] k_j from the caller (reading C-DP)
+    const float cs = a.comb[stage - 1];
+    const float3 inc = make_float3(ap.x + cs * k.x, ap.y + cs * k.y, ap.z + cs * k.z);
+    acc_out = k;
+    if (stage == 7) {  // error estimate of this cell; the state is the step result itself
+      const float3 e = make_float3(a.h * inc.x, a.h * inc.y, a.h * inc.z);
+      tmax = fmaxf(tmax, sqrtf(dot3(e, e)));
+      return m;
+    }
+    return nrm3(make_float3(mn.x + a.h * inc.x, mn.y + a.h * inc.y, mn.z + a.h * inc.z));
+  }
   float3 out;
   if (stage < 4) {
     acc_out = (stage == 1) ? k : make_float3(ap.x + 2.f * k.x, ap.y + 2.f * k.y, ap.z + 2.f * k.z);
@@ -180,8 +192,9 @@ __device__ __forceinline__ float2 sm_pair(const float* p) { return *reinterpret_
 #ifndef MCQ_UMINB
 #define MCQ_UMINB 5  // min resident CTAs per SM requested from ptxas (96-register cap: 84.8 vs 86.8 us on configs[1])
 #endif
-// MM: cavity modes compiled in (1, or kMaxModes with a.nmodes <= MM at run time)
-template <int N2, int MM>
+// MM: cavity modes compiled in (1, or kMaxModes with a.nmodes <= MM at run time); DPM: the
+// Dormand-Prince stage mode compiled in (kept out of the RK4 instances)
+template <int N2, int MM, bool DPM>
 __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a, const float2* __restrict__ gtw) {
   using Cf = UCfg<N2>;
   constexpr int E = Cf::E, TL = Cf::TL, RY = Cf::RY, NT = Cf::NT, LX = 2 * N2, PITCH = Cf::PITCH;
@@ -316,7 +329,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
 #pragma unroll
   for (int k = 0; k < MM; ++k) {
     float gc = 0.f, ge = 0.f;
-    if (k < nm && (a.mode == MODE_LLG || a.mode == MODE_FIELD)) {
+    if (k < nm && (a.mode == MODE_LLG || a.mode == MODE_FIELD || a.mode == MODE_DP)) {
       const int si = (a.mode == MODE_FIELD) ? 0 : a.stage - 1;
       gc = (a.terms & MCQ_TERM_CAVITY) ? a.cav->gc[k][si] : 0.f;
       ge = (a.terms & MCQ_TERM_EXCITATION) ? a.cav->ge[k][si] : 0.f;
@@ -328,15 +341,17 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
   double wacc[MM];
 #pragma unroll
   for (int k = 0; k < MM; ++k) wacc[k] = 0.0;
-  const bool wsum = a.mode == MODE_LLG && a.stage == 4;  // overlaps of m_{n+1}
+  const bool dp = DPM && a.mode == MODE_DP;
+  // overlaps (and the trace's sum m) of the step result: RK4 stage 4's output, DP stage 7's input
+  const bool wsum = (a.mode == MODE_LLG && a.stage == 4) || (dp && a.stage == 7);
   float tmax = 0.f;
-  const bool tr = a.trace && a.mode == MODE_LLG && a.stage == 4;  // sum m_{n+1} for the trace
+  const bool tr = a.trace && wsum;
   const unsigned rowbase = (unsigned)nx * (y + (unsigned)ny * zs);  // 32-bit indices (< 2^32 elements)
   const unsigned Nu = (unsigned)N;
   const float* trow = tc + (yl + 1) * nxp;  // this row inside the z tile
   const bool vec = (nx & 1) == 0;           // global pairs are 8-byte aligned
-  const bool st = a.mode == MODE_LLG || a.mode == MODE_RELAX;
-  const bool need_mn = st && a.stage > 1, need_acc = st && a.stage > 1;
+  const bool st = a.mode == MODE_LLG || a.mode == MODE_RELAX || (dp && a.stage < 7);  // writes a state
+  const bool need_mn = st && a.stage > 1, need_acc = !dp && st && a.stage > 1;
   const bool need_br = a.brms[0] && (gsum != 0.f || wsum);
 #pragma unroll
   for (int i = 0; i < E; ++i) {
@@ -369,6 +384,19 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
         br2[c] = need_br ? (trows ? sm_pair(tbr + so) : ld_pair(a.brms[0], c * Nu + idx, vec, two))
                          : make_float2(a.brms_u[0][c], a.brms_u[0][c]);
       }
+      if (dp) {  // ap = sum_{j < s} comb[j-1] k_j (the earlier stages' slopes, from HBM)
+#pragma unroll 1
+        for (int j = 1; j < a.stage; ++j) {
+          const float w = a.comb[j - 1];
+          const float* Kj = a.K + (size_t)(j - 1) * 3 * Nu;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const float2 kk = ld_pair(Kj, c * Nu + idx, vec, two);
+            ap2[c].x += w * kk.x;
+            ap2[c].y += w * kk.y;
+          }
+        }
+      }
       float2 bk2[MM > 1 ? MM - 1 : 1][3];  // extra modes' B_rms (maps or uniform values)
 #pragma unroll
       for (int k = 1; k < MM; ++k)
@@ -399,7 +427,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
         float3 accn = make_float3(0.f, 0.f, 0.f), Bf = make_float3(0.f, 0.f, 0.f);
         float3 out;
         if constexpr (MM == 1) {
-          out = cell_core(a, m, nb, ok, mn, ap, br, gsum, Bd, tmax, accn, Bf);
+          out = cell_core<DPM>(a, m, nb, ok, mn, ap, br, gsum, Bd, tmax, accn, Bf);
         } else {
           float3 bcav = make_float3(br.x * gsum, br.y * gsum, br.z * gsum);
 #pragma unroll
@@ -410,7 +438,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
               bcav.z += MCQ_PICK(bk2[k - 1][2]) * gs[k];
             }
           }
-          out = cell_core(a, m, nb, ok, mn, ap, bcav, any_cav ? 1.f : 0.f, Bd, tmax, accn, Bf);
+          out = cell_core<DPM>(a, m, nb, ok, mn, ap, bcav, any_cav ? 1.f : 0.f, Bd, tmax, accn, Bf);
         }
         if (wsum) {
           wacc[0] += (double)(br.x * out.x) + (double)(br.y * out.y) + (double)(br.z * out.z);
@@ -444,7 +472,10 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
         if (a.mode == MODE_FIELD) st_pair(a.bout, c * Nu + idx, bf2[c], vec, two);
         if (st) {
           st_pair(a.mOut, c * Nu + idx, o[c], vec, two);
-          if (a.stage < 4) st_pair(a.acc, c * Nu + idx, acc2[c], vec, two);
+          if (dp)
+            st_pair(a.K + (size_t)(a.stage - 1) * 3 * Nu, c * Nu + idx, acc2[c], vec, two);  // k_s
+          else if (a.stage < 4)
+            st_pair(a.acc, c * Nu + idx, acc2[c], vec, two);
         }
       }
     }
@@ -463,7 +494,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
       msum.z += v[2][i].x + v[2][i].y;
     }
   }
-  if (a.mode == MODE_LLG && a.stage == 4) {
+  if (wsum) {  // RK4 stage 4 / Dormand-Prince stage 7: the step result's partials
     // one quantity at a time (few live registers): W_k of the compiled modes, then sum m
     auto warp_sum = [&](double q, int k) {
 #pragma unroll
@@ -489,6 +520,17 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
         for (int w = 0; w < nw; ++w) s += red[w * kNPart + threadIdx.x];
       const int nps = gridDim.x * gridDim.y;
       a.partials[threadIdx.x * nps + blockIdx.y * gridDim.x + blockIdx.x] = s;
+    }
+  }
+  if (dp && a.stage == 7) {  // the step's error estimate: max over cells (fp32 bits, >= 0)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_down_sync(0xffffffffu, tmax, o));
+    if (lane == 0) redf[warp] = tmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float s = 0.f;
+      for (int w = 0; w < nw; ++w) s = fmaxf(s, redf[w]);
+      atomicMax(a.maxbits, __float_as_uint(s));
     }
   }
   if (a.mode == MODE_MAXTORQUE) {
@@ -564,18 +606,23 @@ void launch_update(const UpdateArgs& a, const float2* tw, cudaStream_t st) {
   MCQ_DISPATCH_N2(a.d.N2, {
     using Cf = UCfg<N2>;
     dim3 grid((a.d.ny + Cf::RY - 1) / Cf::RY, a.d.nz);
-    if (a.nmodes > 1)
-      launch_pdl(a.d.pdl, k_update<N2, kMaxModes>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
+    if (a.mode == MODE_DP)
+      launch_pdl(a.d.pdl, k_update<N2, kMaxModes, true>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
+    else if (a.nmodes > 1)
+      launch_pdl(a.d.pdl, k_update<N2, kMaxModes, false>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
     else
-      launch_pdl(a.d.pdl, k_update<N2, 1>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
+      launch_pdl(a.d.pdl, k_update<N2, 1, false>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
   })
 }
 
 void configure_update_kernels() {
   for (int n = 2; n <= 512; n *= 2) {
     MCQ_DISPATCH_N2(n, {
-      cudaFuncSetAttribute(k_update<N2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UCfg<N2>::SMEM);
-      cudaFuncSetAttribute(k_update<N2, kMaxModes>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UCfg<N2>::SMEM);
+      cudaFuncSetAttribute(k_update<N2, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UCfg<N2>::SMEM);
+      cudaFuncSetAttribute(k_update<N2, kMaxModes, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)UCfg<N2>::SMEM);
+      cudaFuncSetAttribute(k_update<N2, kMaxModes, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)UCfg<N2>::SMEM);
     })
   }
 }
@@ -584,13 +631,11 @@ void configure_update_kernels() {
 // Stage factors for the step that starts at (alpha_k, t): Gamma_k(t + c dt) = 2 Re(e_{k,c} alpha_k)
 // (P:343 with S_n, C_n frozen, reading C3/C5), excitation a_k sinc(w_k (t + c dt)) (C13), per mode.
 __device__ void cav_prepare(const CavParams& p, CavState* st) {
-  const double c[4] = {0.0, 0.5, 0.5, 1.0};
-  const int ci[4] = {0, 1, 1, 2};
   for (int k = 0; k < p.nmodes; ++k)
-    for (int s = 0; s < 4; ++s) {
-      const double er = p.ec_re[k][ci[s]], ei = p.ec_im[k][ci[s]];
+    for (int s = 0; s < p.nst; ++s) {  // stage nodes c_s of the integrator (RK4 or Dormand-Prince)
+      const double er = p.ec_re[k][s], ei = p.ec_im[k][s];
       const double g = 2.0 * (er * st->re[k] - ei * st->im[k]);
-      const double x = p.exc_omega[k] * (st->t + c[s] * p.dt);
+      const double x = p.exc_omega[k] * (st->t + p.cst[s] * p.dt);
       const double sc = (x == 0.0) ? 1.0 : sin(x) / x;
       st->gc[k][s] = (float)(p.cav_on[k] ? g : 0.0);
       st->ge[k][s] = (float)(p.exc_amp[k] * sc);
@@ -643,7 +688,7 @@ __global__ void __launch_bounds__(kCavThreads) k_cavity(CavParams p, CavState* s
     }
     for (int k = 0; k < p.nmodes; ++k) {
       const double W = p.cav_on[k] ? p.Ms * tot[k] : 0.0;
-      const double er = p.ec_re[k][2], ei = p.ec_im[k][2];
+      const double er = p.ecn_re[k], ei = p.ecn_im[k];
       const double re = er * st->re[k] - ei * st->im[k];
       const double im = er * st->im[k] + ei * st->re[k] + p.vc_over_hbar * W * p.dt;
       st->re[k] = re;
