@@ -139,3 +139,28 @@ def test_gpu_vacuum_rabi_splitting_sphere():
     assert hi == pytest.approx(op / (2 * math.pi), rel=5e-3)
     assert 2 * math.pi * (hi - lo) == pytest.approx(op - om, rel=1e-2)
     s.close()
+
+
+def test_gpu_bright_mode_vacuum_rabi_configs1_construction():
+    """The BJ configs[1] construction (YIG sphere, two-wire "bright" B_rms map normalised to
+    g/2pi = 1 GHz through the coupling law, f_c = 13.2 GHz = gamma B_ext / 2pi) at 32^3 cells:
+    the spectrum of <m_y> shows the vacuum Rabi doublet of P:22 ("g/2pi ~ 1 GHz") at the
+    two-oscillator frequencies within 1 % (the map's non-uniformity also couples weakly to
+    higher magnetostatic modes)."""
+    from synth import make_config
+    cfg = make_config(1, grid=(32, 32, 32))
+    rng = np.random.default_rng(1)
+    cfg.m0 = tilted_uniform(cfg.n, rng, (0.0, 0.03, 1.0), 0.0, cfg.mask)
+    cfg.exc_amp = 0.0
+    cfg.x0 = cfg.p0 = 0.0
+    s = mcq.Solver.from_config(cfg)
+    s.trace(20000)
+    s.run(cfg.dt, 16000)                     # 8 ns
+    tr = s.trace()
+    lo, hi = A.peaks(tr[:, 2], cfg.dt, 2, window="hann", pad=8)
+    w = 2 * math.pi * cfg.f_c
+    om, op = A.two_oscillator(w, w, 2 * math.pi * 1e9)
+    assert lo == pytest.approx(om / (2 * math.pi), rel=1e-2)
+    assert hi == pytest.approx(op / (2 * math.pi), rel=1e-2)
+    assert (hi - lo) == pytest.approx((op - om) / (2 * math.pi), rel=5e-2)
+    s.close()
