@@ -300,6 +300,13 @@ def main():
     step_bytes = step_alg_bytes(L, cfg.grid, cfg.brms_map is not None, ns)
     traffic, traffic_src = ncu_traffic(args.config, top) if (world == 1 and args.loopback <= 1) else (None, None)
     ms_step = ms_max / args.steps
+    # resident working set of one replica: 4 state arrays, X, Y, Khat (+ map), vs the 126 MB L2
+    ws = (4 * 12 * cfg.n + 3 * cfg.grid[2] * cfg.grid[1] * L["P"] * 8 * (1 + (L["Ly"] if cfg.grid[2] > 1 else 0)
+          / max(cfg.grid[1], 1)) + 6 * (L["Lz"] // 2 + 1) * (L["Ly"] // 2 + 1) * L["P"] * 4
+          + (12 * cfg.n if cfg.brms_map is not None else 0)) * R
+    l2_note = (f"working set {ws / 1e6:.0f} MB > 126 MB L2: streamed from HBM every step (no flush needed)"
+               if ws > 126e6 else
+               f"working set {ws / 1e6:.1f} MB fits in the 126 MB L2 (latency-bound workload; not flushed)")
 
     if rank == 0:
         res = {
@@ -312,7 +319,7 @@ def main():
                        if world > 1 else (f"single GPU, loopback z-slab x{args.loopback}"
                                           if args.loopback > 1 else "single GPU"),
                        "replicas_per_gpu": R,
-                       "l2": "working set > 126 MB L2 every step (no flush needed)",
+                       "l2": l2_note,
                        "padded_fft": [L["Lx"], L["Ly"], L["Lz"]]},
             "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": pk["hbm_gbs"],
                          "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
