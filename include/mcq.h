@@ -195,6 +195,21 @@ MCQ_API int mcq_run_dp(mcq_ctx *, double dt, long long steps);
 MCQ_API int mcq_run_adaptive(mcq_ctx *, double duration, double dt0, double tol, long long max_attempts,
                              long long *accepted, long long *rejected, double *dt_next);
 
+/* OVF 2.0 vector fields (the paper hands B_rms maps to Mumax3 as
+ * brmsfile.ovf; format per SPEC's ovf-io module).  Host-only, no context, no GPU.
+ * mcq_ovf_read: rectangular mesh, valuedim 3, payload "Text" / "Binary 4" / "Binary 8" (check
+ * values 1234567.0f / 123456789012345.0, little-endian); fills grid = (xnodes, ynodes, znodes)
+ * and cell = (x/y/zstepsize, m); with out != NULL also copies the 3 nx ny nz values (x fastest,
+ * float) if capacity (floats) suffices.  EINVAL with a message naming the byte offset for a bad
+ * magic (OVF 1.0 is rejected), a check-value mismatch, a truncated payload or a bad header.
+ * mcq_ovf_write: canonical file (fixed header order, LF, 17 significant digits in text);
+ * representation 0 = text, 4 = binary 4, 8 = binary 8.  mcq_ovf_last_error: this thread's last
+ * OVF error message. */
+MCQ_API int mcq_ovf_read(const char *path, int grid[3], double cell[3], float *out, long long capacity);
+MCQ_API int mcq_ovf_write(const char *path, const int grid[3], const double cell[3], const float *data,
+                          int representation);
+MCQ_API const char *mcq_ovf_last_error(void);
+
 /* Block until all enqueued work is done; reports asynchronous kernel errors (ECUDA). */
 MCQ_API int mcq_synchronize(mcq_ctx *);
 

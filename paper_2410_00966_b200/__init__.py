@@ -179,6 +179,39 @@ def mcq_run_adaptive(ctx, duration, dt0, tol, max_attempts=10**7):
     return a.value, r.value, d.value
 
 
+def mcq_ovf_last_error():
+    return lib.mcq_ovf_last_error().decode()
+
+
+def mcq_ovf_read(path):
+    """OVF 2.0 file -> (values (N, 3) float32 x-fastest, grid (nx, ny, nz), cell (dx, dy, dz))."""
+    g = (C.c_int * 3)()
+    c = (C.c_double * 3)()
+    p = str(path).encode()
+    rc = lib.mcq_ovf_read(p, g, c, None, 0)
+    if rc != 0:
+        raise MCQError(rc, mcq_ovf_last_error())
+    n = g[0] * g[1] * g[2]
+    out = np.empty(3 * n, np.float32)
+    rc = lib.mcq_ovf_read(p, g, c, out.ctypes.data, out.size)
+    if rc != 0:
+        raise MCQError(rc, mcq_ovf_last_error())
+    return out.reshape(n, 3), tuple(g), tuple(c)
+
+
+def mcq_ovf_write(path, values, grid, cell, representation="binary4"):
+    """Write a (N, 3) field as OVF 2.0: representation "text", "binary4" or "binary8"."""
+    rep = {"text": 0, "binary4": 4, "binary8": 8}[representation]
+    a = _vec(values)
+    g = (C.c_int * 3)(*[int(x) for x in grid])
+    c = (C.c_double * 3)(*[float(x) for x in cell])
+    if a.size != 3 * g[0] * g[1] * g[2]:
+        raise ValueError("values do not match the grid")
+    rc = lib.mcq_ovf_write(str(path).encode(), g, c, a.ctypes.data, rep)
+    if rc != 0:
+        raise MCQError(rc, mcq_ovf_last_error())
+
+
 def mcq_synchronize(ctx):
     _check(ctx, lib.mcq_synchronize(ctx))
 
@@ -290,6 +323,7 @@ class Solver:
 
     def __init__(self, grid, cell, Ms, Aex, alpha, aniso=None, stream=None, dist=None):
         self.grid = tuple(int(g) for g in grid)
+        self.cell = tuple(float(c) for c in cell)
         self.n = self.grid[0] * self.grid[1] * self.grid[2]
         d = dict(dist or {})
         if stream:
@@ -326,6 +360,16 @@ class Solver:
 
     def cavity(self):
         return mcq_get_cavity(self.ctx)
+
+    def set_brms_ovf(self, path, mode=0, rtol=1e-9):
+        """B_rms of `mode` from an OVF 2.0 file: the node counts must equal the grid and
+        the step sizes must match the cell within rtol (no resampling)."""
+        vals, g, c = mcq_ovf_read(path)
+        if tuple(g) != self.grid:
+            raise ValueError(f"OVF grid {g} != solver grid {self.grid}")
+        if any(abs(a - b) > rtol * abs(b) for a, b in zip(c, self.cell)):
+            raise ValueError(f"OVF cell {c} != solver cell {self.cell}")
+        mcq_set_brms_mode(self.ctx, mode, vals)
 
     def trace(self, capacity=None, every=1):
         """trace(capacity): start recording; trace(): the rows recorded so far."""

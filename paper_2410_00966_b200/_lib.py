@@ -89,6 +89,9 @@ _sig = {
     "mcq_debug_tensor_octant": (C.c_int, [_P, _P]),
     "mcq_debug_khat": (C.c_int, [_P, _P]),
     "mcq_last_error": (C.c_char_p, [_P]),
+    "mcq_ovf_read": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_double), _P, C.c_longlong]),
+    "mcq_ovf_write": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_double), _P, C.c_int]),
+    "mcq_ovf_last_error": (C.c_char_p, []),
     "mcq_destroy": (None, [_P]),
 }
 for _name, (_res, _args) in _sig.items():

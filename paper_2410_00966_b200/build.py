@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmcq.so")
-SOURCES = ["mcq.cu", "passes.cu", "update.cu", "tensor.cu"]
+SOURCES = ["mcq.cu", "passes.cu", "update.cu", "tensor.cu", "ovf.cpp"]
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
          "-Xptxas", "-O3"]
@@ -31,7 +31,7 @@ def build(force=False, verbose=False, jobs=4):
     objs = []
     procs = []
     for src in SOURCES:
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
+        obj = os.path.join(CSRC, os.path.splitext(src)[0] + ".o")
         cmd = [nvcc, *FLAGS, "-dc" if False else "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)

@@ -113,3 +113,25 @@ def test_mode_api_validation_and_single_mode_fallback():
     assert a.cavity()["re_alpha"] == b.cavity()["re_alpha"]
     a.close()
     b.close()
+
+
+def test_brms_from_ovf_file_equals_direct_map(tmp_path):
+    """the B_rms map handed over as an OVF 2.0 file (binary 4) drives the same run bit
+    for bit; a file on another grid is refused (no resampling)."""
+    cfg = small_config("sphere", (16, 12, 8), seed=5, state="phys")
+    p = tmp_path / "brmsfile.ovf"
+    mcq.mcq_ovf_write(p, cfg.brms_map, cfg.grid, cfg.cell, "binary4")
+    a = mcq.Solver.from_config(cfg)
+    b = mcq.Solver.from_config(cfg, set_state=False)
+    mcq.mcq_set_brms(b.ctx, None, (0.0, 0.0, 0.0))
+    b.set_brms_ovf(p)
+    b.set_m(cfg.m0)
+    a.run(cfg.dt, 20)
+    b.run(cfg.dt, 20)
+    assert np.array_equal(a.m(), b.m()) and a.cavity()["re_alpha"] == b.cavity()["re_alpha"]
+    q = tmp_path / "other.ovf"
+    mcq.mcq_ovf_write(q, np.zeros((8 * 8 * 8, 3), np.float32), (8, 8, 8), cfg.cell, "binary4")
+    with pytest.raises(ValueError):
+        b.set_brms_ovf(q)
+    a.close()
+    b.close()
