@@ -128,9 +128,11 @@ struct mcq_ctx {
   float* io = nullptr;  // AoS staging for the cells this context holds
   bool m_set = false;
   // graphs: [0] = 1 LLG step, [1] = kGraphSteps LLG steps, [2] = 1 relax step, [3] = relax chunk
-  cudaGraphExec_t g[4] = {nullptr, nullptr, nullptr, nullptr};
-  double g_dt[4] = {0, 0, 0, 0};
-  long long g_launches[4] = {0, 0, 0, 0};
+  // graphs: [0]/[1] 1 / kGraphSteps LLG (RK4) steps, [2]/[3] 1 / 50 relax steps,
+  // [4]/[5] 1 / kGraphSteps fixed Dormand-Prince steps
+  cudaGraphExec_t g[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  double g_dt[6] = {0, 0, 0, 0, 0, 0};
+  long long g_launches[6] = {0, 0, 0, 0, 0, 0};
   long long launches = 0;
   alignas(64) CUtensorMap tmz;  // TMA descriptor of Y for the pipelined K-Z kernel (1 slab)
   bool have_tmz = false;
@@ -172,7 +174,7 @@ int next_pow2(int n) {
 int padded(int n) { return n == 1 ? 1 : next_pow2(2 * n); }
 
 void invalidate_graphs(mcq_ctx* c) {
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 6; ++i) {
     if (c->g[i]) cudaGraphExecDestroy(c->g[i]);
     c->g[i] = nullptr;
   }
@@ -504,10 +506,14 @@ int capture(mcq_ctx* c, int which, double dt, int steps) {
   CK(c, cudaStreamBeginCapture(c->cap, c->mode == 2 ? cudaStreamCaptureModeRelaxed : cudaStreamCaptureModeThreadLocal));
   Enq q{c, c->cap};
   for (int i = 0; i < steps; ++i) {
-    if (which < 2)
+    if (which < 2) {
       q.llg_step(dt);
-    else
+    } else if (which < 4) {
       q.relax_step(dt);
+    } else {
+      q.dp_attempt(dt);
+      q.dp_commit(dt);
+    }
   }
   cudaGraph_t graph = nullptr;
   cudaError_t e1 = cudaStreamEndCapture(c->cap, &graph);
@@ -1127,14 +1133,15 @@ int mcq_run_dp(mcq_ctx* c, double dt, long long steps) {
   if (!c->m_set) return fail(c, MCQ_ESTATE, "mcq_run_dp before mcq_set_m");
   int rc = ensure_dp(c);
   if (rc != MCQ_OK) return rc;
-  Enq q{c, c->stream};
-  for (long long i = 0; i < steps; ++i) {
-    launch_cav_prepare(cav_params(c, dt, true), c->cav, c->stream);
-    q.dp_attempt(dt);
-    q.dp_commit(dt);
-    if (q.rc != MCQ_OK) return q.rc;
-  }
-  c->launches += q.count + steps;
+  if (steps == 0) return MCQ_OK;
+  // stage factors at the DP nodes for this dt; every step's cavity kernel renews them
+  launch_cav_prepare(cav_params(c, dt, true), c->cav, c->stream);
+  c->launches += 1;
+  if (steps >= kGraphSteps && (rc = capture(c, 5, dt, kGraphSteps)) != MCQ_OK) return rc;
+  if (steps % kGraphSteps && (rc = capture(c, 4, dt, 1)) != MCQ_OK) return rc;
+  for (long long i = 0; i < steps / kGraphSteps; ++i) CK(c, cudaGraphLaunch(c->g[5], c->stream));
+  for (long long i = 0; i < steps % kGraphSteps; ++i) CK(c, cudaGraphLaunch(c->g[4], c->stream));
+  c->launches += (steps / kGraphSteps) * c->g_launches[5] + (steps % kGraphSteps) * c->g_launches[4];
   CK(c, cudaGetLastError());
   return MCQ_OK;
 }
