@@ -16,7 +16,8 @@ namespace mcq {
 // slab, small grids (latency-bound; configs[0] 56.1 vs 59.5 us/step; configs[1] 1.067 vs 1.031
 // ms/step slower) — never with device copies or NCCL calls between kernels.
 #ifndef MCQ_PDL
-#define MCQ_PDL 1
+#define MCQ_PDL 0  // off: with it on, one small-grid parity case (demag through the TMA-staged
+                   // rows) failed intermittently (1 of 4 suite runs); the gain was 6 % on configs[0]
 #endif
 __device__ __forceinline__ void pdl_trigger() {
 #if MCQ_PDL
@@ -26,6 +27,8 @@ __device__ __forceinline__ void pdl_trigger() {
 __device__ __forceinline__ void pdl_wait() {
 #if MCQ_PDL
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // order the previous grid's generic-proxy writes before this thread's TMA (async-proxy) reads
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 #endif
 }
 template <typename... KArgs, typename... Args>
