@@ -16,8 +16,7 @@ namespace mcq {
 // slab, small grids (latency-bound; configs[0] 56.1 vs 59.5 us/step; configs[1] 1.067 vs 1.031
 // ms/step slower) — never with device copies or NCCL calls between kernels.
 #ifndef MCQ_PDL
-#define MCQ_PDL 0  // off: with it on, one small-grid parity case (demag through the TMA-staged
-                   // rows) failed intermittently (1 of 4 suite runs); the gain was 6 % on configs[0]
+#define MCQ_PDL 0  // off: 6 % on the latency-bound configs[0] only, slower on configs[1]
 #endif
 __device__ __forceinline__ void pdl_trigger() {
 #if MCQ_PDL

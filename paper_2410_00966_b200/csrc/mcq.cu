@@ -600,8 +600,12 @@ int build_khat(mcq_ctx* c, double* oct_out /* optional host copy of the octant *
     for (int ax = 0; ax < 3 && rc == MCQ_OK; ++ax) {
       axis_matrices(Ls[ax], Tc, Ts);
       const size_t mm = (size_t)ms[ax] * ms[ax];
-      if (cudaMemcpy(T, Tc.data(), mm * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
-          cudaMemcpy(T + tmax, Ts.data(), mm * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) {
+      // stream-ordered uploads: a plain cudaMemcpy from pageable memory may return before the
+      // data lands and is not ordered with the (non-blocking) work stream — it made Khat
+      // nondeterministic (stale matrices read by the transform)
+      if (cudaMemcpyAsync(T, Tc.data(), mm * sizeof(double), cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+          cudaMemcpyAsync(T + tmax, Ts.data(), mm * sizeof(double), cudaMemcpyHostToDevice, c->stream) !=
+              cudaSuccess) {
         rc = fail(c, MCQ_ECUDA, "tensor matrix upload");
         break;
       }
@@ -846,7 +850,9 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
       const double ang = 2.0 * M_PI * m / kTwMax;
       h[m] = make_float2((float)std::cos(ang), (float)-std::sin(ang));
     }
-    if (cudaMemcpy(c->tw, h.data(), kTwMax * 8, cudaMemcpyHostToDevice) != cudaSuccess) return bail(MCQ_ECUDA);
+    if (cudaMemcpyAsync(c->tw, h.data(), kTwMax * 8, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+        cudaStreamSynchronize(c->stream) != cudaSuccess)
+      return bail(MCQ_ECUDA);
   }
   if (build_khat(c, nullptr) != MCQ_OK) return bail(MCQ_ECUDA);
   make_y_tensor_map(c);

@@ -311,3 +311,17 @@ def test_full_size_run_properties():
     W = ref.W(m.astype(np.float64).reshape(ref.m.shape))
     assert s.cavity()["W"] == pytest.approx(W, rel=1e-5)
     s.close()
+
+
+def test_khat_bitwise_reproducible_across_contexts():
+    """The device precompute of Khat must not depend on timing (it once did: transform matrices
+    uploaded outside the work stream's order)."""
+    cfg = small_config("disc", (40, 72, 3), seed=11, aniso=UNI, state="rand")
+    first = None
+    for _ in range(8):
+        s = _solver(cfg)
+        k = mcq.mcq_debug_khat(s.ctx)
+        if first is None:
+            first = k
+        assert np.array_equal(k, first)
+        s.close()
