@@ -32,7 +32,11 @@ namespace mcq {
 
 template <int N2>
 struct UCfg {
-  static constexpr int E = N2 < MCQ_UE ? N2 : MCQ_UE;
+#ifndef MCQ_UE_BIG
+#define MCQ_UE_BIG MCQ_UE  // positions per thread for N2 >= 256 (experiment knob)
+#endif
+  static constexpr int EU = N2 >= 256 ? MCQ_UE_BIG : MCQ_UE;
+  static constexpr int E = N2 < EU ? N2 : EU;
   static constexpr int TL = N2 / E;                       // threads per row
   static constexpr int RY0 = 128 / TL;
   static constexpr int RY = RY0 < 1 ? 1 : (RY0 > 16 ? 16 : RY0);
