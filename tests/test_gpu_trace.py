@@ -164,3 +164,38 @@ def test_gpu_bright_mode_vacuum_rabi_configs1_construction():
     assert hi == pytest.approx(op / (2 * math.pi), rel=1e-2)
     assert (hi - lo) == pytest.approx((op - om) / (2 * math.pi), rel=5e-2)
     s.close()
+
+
+def test_gpu_bias_sweep_fits_coupling_law():
+    """NEXT-3 driver: a bias sweep across the anticrossing, run as concurrent replicas (own
+    streams, device traces), fitted with the two-oscillator model: g and f_c come back at the
+    coupling-law g and the set f_c."""
+    from paper_2410_00966_b200 import spectroscopy as SP
+    grid = (12, 12, 12)
+    mask = sphere_mask(grid, CELL, 0.45 * grid[0] * CELL[0])
+    n = int(np.prod(grid))
+    m0 = tilted_uniform(n, np.random.default_rng(3), (0.0, 0.03, 1.0), 0.0, mask)
+    B0 = 0.4
+    wc = GAMMA * B0
+    V = int(mask.sum()) * np.prod(CELL)
+    g = 0.03 * wc
+    Bperp = g / (GAMMA * math.sqrt(YIG_MS * V / (A.HBAR * GAMMA) / 2))
+    points = list(np.linspace(0.94, 1.06, 7) * B0)
+
+    def make(B, stream):
+        s = mcq.Solver(grid, CELL, YIG_MS, YIG_A, 0.0, stream=stream)
+        mcq.mcq_set_geometry(s.ctx, mask)
+        mcq.mcq_set_bext(s.ctx, (0.0, 0.0, B))
+        mcq.mcq_set_brms(s.ctx, None, (Bperp, 0.0, 0.0))
+        mcq.mcq_set_cavity(s.ctx, wc / (2 * math.pi), 0.0)
+        s.set_m(m0)
+        return s
+
+    dt = 2 * math.pi / wc / 80
+    pk = SP.sweep(make, points, dt, 16000)
+    w_mag = GAMMA * np.array(points)             # sphere: uniform-mode frequency gamma B
+    wc_fit, g_fit = SP.fit_anticrossing(w_mag, 2 * math.pi * pk[:, 0], 2 * math.pi * pk[:, 1], wc, 0.02 * wc)
+    assert wc_fit == pytest.approx(wc, rel=5e-3)
+    assert g_fit == pytest.approx(g, rel=2e-2)
+    # the product's normal-mode formula agrees with the oracle's pinned two-oscillator formula
+    assert SP.normal_modes(wc, 1.1 * wc, g)[1] == pytest.approx(A.two_oscillator(wc, 1.1 * wc, g)[1], rel=1e-14)
