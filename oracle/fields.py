@@ -40,6 +40,34 @@ def exchange(m, mag, cell, Aex, Ms):
     return np.where(mag[..., None], out, 0.0)
 
 
+def _neighbour(m, mag, axis, shift):
+    """m at i + shift along `axis`, with the cell's own m where the neighbour is outside the
+    mesh or in vacuum (Neumann ghost, reading C-DMI)."""
+    nb = np.roll(m, -shift, axis=axis)
+    valid = np.roll(mag, -shift, axis=axis).copy()
+    idx = [slice(None)] * 3
+    idx[axis] = m.shape[axis] - 1 if shift == +1 else 0
+    valid[tuple(idx)] = False
+    return np.where(valid[..., None], nb, m)
+
+
+def dmi_interfacial(m, mag, cell, D, Ms):
+    """Interfacial DMI (P:188 lists DMI among Mumax3's field terms; reading C-DMI):
+    energy density D [m_z div m - (m . grad) m_z] (in-plane derivatives), field
+    B = (2D/M_s) (d_x m_z, d_y m_z, -(d_x m_x + d_y m_y)) with central differences
+    d_x f = (f_{x+1} - f_{x-1}) / (2 dx) and Neumann ghosts at mesh / vacuum boundaries (the
+    DMI-tilted boundary condition of Mumax3 is not modelled)."""
+    dxp, dxm = _neighbour(m, mag, 2, +1), _neighbour(m, mag, 2, -1)
+    dyp, dym = _neighbour(m, mag, 1, +1), _neighbour(m, mag, 1, -1)
+    ddx = (dxp - dxm) / (2 * cell[0])
+    ddy = (dyp - dym) / (2 * cell[1])
+    out = np.zeros_like(m)
+    out[..., 0] = ddx[..., 2]
+    out[..., 1] = ddy[..., 2]
+    out[..., 2] = -(ddx[..., 0] + ddy[..., 1])
+    return np.where(mag[..., None], (2 * D / Ms) * out, 0.0)
+
+
 def uniaxial(m, mag, Ku1, u, Ms):
     """First-order uniaxial anisotropy (reading C10): B = (2K_u1/M_s)(m.u)u."""
     u = np.asarray(u, dtype=np.float64)

@@ -22,8 +22,8 @@ from . import tensor as T
 from .cavity import CavityMemory
 from .llg import torque, relax_torque, normalize, rk4_step, dp45_step, dp_controller
 
-ZEEMAN, EXCHANGE, ANIS, DEMAG, CAVITY, EXCITATION = 1, 2, 4, 8, 16, 32
-ALL = ZEEMAN | EXCHANGE | ANIS | DEMAG | CAVITY | EXCITATION
+ZEEMAN, EXCHANGE, ANIS, DEMAG, CAVITY, EXCITATION, DMI = 1, 2, 4, 8, 16, 32, 64
+ALL = ZEEMAN | EXCHANGE | ANIS | DEMAG | CAVITY | EXCITATION | DMI
 RELAX_CHECK_EVERY = 50
 
 
@@ -31,7 +31,7 @@ class Simulation:
     def __init__(self, grid, cell, Ms, Aex, alpha, m0, mask=None, bext=(0.0, 0.0, 0.0),
                  brms_map=None, brms_uniform=(0.0, 0.0, 0.0), f_c=1e9, kappa=0.0, x0=0.0, p0=0.0,
                  exc_amp=0.0, exc_omega=0.0, aniso=None, demag="auto", octant=None, hbar=HBAR,
-                 gamma=GAMMA, terms=ALL, modes=()):
+                 gamma=GAMMA, terms=ALL, modes=(), dmi=0.0):
         self.grid = tuple(int(g) for g in grid)
         nx, ny, nz = self.grid
         self.shape = (nz, ny, nx)
@@ -48,6 +48,7 @@ class Simulation:
         else:
             self.brms = F.zeeman(self.shape, brms_uniform)
         self.aniso = aniso or {}
+        self.dmi = float(dmi)       # interfacial DMI constant D (J/m^2), reading C-DMI
         self.exc_amp, self.exc_omega = float(exc_amp), float(exc_omega)
         self.mem = CavityMemory(2 * math.pi * f_c, kappa, x0, p0, self.vcell, hbar)
         # extra modes k >= 1 (reading C-MM): dicts with brms_map | brms_uniform, f_c, kappa,
@@ -106,6 +107,8 @@ class Simulation:
                 B += F.cubic(m, self.mag, a["kc1"], a["c1"], a["c2"], self.Ms)
         if terms & DEMAG and self.demag_mode != "off":
             B += self.demag(m)
+        if terms & DMI and self.dmi != 0.0:
+            B += F.dmi_interfacial(m, self.mag, self.cell, self.dmi, self.Ms)
         if terms & EXCITATION and self.exc_amp != 0.0:
             B += self.exc_amp * float(F.sinc(self.exc_omega * t)) * self.brms
         if terms & CAVITY and self.cavity_enabled:
