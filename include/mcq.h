@@ -64,7 +64,8 @@ extern "C" {
 #define MCQ_TERM_DEMAG 8u
 #define MCQ_TERM_CAVITY 16u     /* B_rms * Gamma(t) */
 #define MCQ_TERM_EXCITATION 32u /* a sinc(w_cut t) B_rms */
-#define MCQ_TERM_ALL 63u
+#define MCQ_TERM_DMI 64u        /* interfacial Dzyaloshinskii-Moriya (mcq_set_dmi) */
+#define MCQ_TERM_ALL 127u
 
 /* kernel classes reported by mcq_profile_run */
 #define MCQ_K_YFWD 0   /* y-forward FFT pass (3D)                        */
@@ -145,6 +146,11 @@ MCQ_API int mcq_set_brms(mcq_ctx *, const float *map, const double uniform[3]);
 /* Cavity parameters: f_c (Hz, > 0), kappa (rad/s, >= 0), x0 = 2 Re alpha_0, p0 = -2 Im alpha_0
  * (P:362-368).  Resets the memory term (alpha <- alpha_0, t <- 0). */
 MCQ_API int mcq_set_cavity(mcq_ctx *, double f_c, double kappa, double x0, double p0);
+
+/* Interfacial DMI constant D (J/m^2; 0 = off) (P:188 lists DMI among the field terms; SURVEY
+ * NEXT-4).  Reading C-DMI: B = (2D/M_s)(d_x m_z, d_y m_z, -(d_x m_x + d_y m_y)) with central
+ * differences and Neumann ghosts (own m) at mesh and vacuum boundaries. */
+MCQ_API int mcq_set_dmi(mcq_ctx *, double D);
 
 /* Excitation a * sinc(w_cut t) * B_rms, unnormalised sinc, t = cavity clock (C13). */
 MCQ_API int mcq_set_excitation(mcq_ctx *, double amplitude, double omega_cut);

@@ -13,7 +13,8 @@ LIB_PATH = os.environ.get("MCQ_LIB_PATH") or os.path.join(HERE, "libmcq.so")  # 
 
 MCQ_OK, MCQ_EINVAL, MCQ_ESTATE, MCQ_ENOMEM, MCQ_ECUDA, MCQ_ENCCL = 0, -1, -2, -3, -4, -5
 TERM_ZEEMAN, TERM_EXCHANGE, TERM_ANIS, TERM_DEMAG, TERM_CAVITY, TERM_EXCITATION = 1, 2, 4, 8, 16, 32
-TERM_ALL = 63
+TERM_DMI = 64
+TERM_ALL = 127
 K_YFWD, K_ZCONV, K_YINV, K_Y2D, K_UPDATE, K_CAVITY = range(6)
 NKCLASS = 6
 KCLASS_NAMES = ("yfwd", "zconv", "yinv", "y2d", "update", "cavity")
@@ -62,6 +63,7 @@ _sig = {
     "mcq_set_brms": (C.c_int, [_P, _P, C.POINTER(C.c_double)]),
     "mcq_set_cavity": (C.c_int, [_P, C.c_double, C.c_double, C.c_double, C.c_double]),
     "mcq_set_excitation": (C.c_int, [_P, C.c_double, C.c_double]),
+    "mcq_set_dmi": (C.c_int, [_P, C.c_double]),
     "mcq_reset_memory": (C.c_int, [_P]),
     "mcq_set_modes": (C.c_int, [_P, C.c_int]),
     "mcq_set_brms_mode": (C.c_int, [_P, C.c_int, _P, C.POINTER(C.c_double)]),

@@ -153,6 +153,7 @@ struct UpdateArgs {
   float ex[3];        // 2A / (Ms d_axis^2)
   float ku, u[3];     // 2 K_u1 / Ms, axis
   float kc, c1[3], c2[3], c3[3];  // 2 K_c1 / Ms, axes
+  float dmi[2];       // interfacial DMI: D / (Ms dx), D / (Ms dy) (0: off), reading C-DMI
   float gl;           // gamma / (1 + alpha^2)
   float alpha;
   float gamma;

@@ -114,6 +114,7 @@ struct mcq_ctx {
   bool cav_on[kMaxModes] = {};
   bool have_mask = false;
   double bext[3] = {0, 0, 0};
+  double dmi = 0;  // interfacial DMI constant (J/m^2)
   double fc[kMaxModes] = {1e9, 1e9, 1e9, 1e9}, kappa[kMaxModes] = {}, x0[kMaxModes] = {}, p0[kMaxModes] = {};
   double exc_amp[kMaxModes] = {}, exc_omega[kMaxModes] = {};
   CavState* cav = nullptr;
@@ -234,6 +235,8 @@ UpdateArgs base_args(const mcq_ctx* c, const Slab& s) {
   a.ku = (float)(2.0 * c->K.ku1 / c->Ms);
   unit(c->K.u, a.u);
   a.kc = (float)(2.0 * c->K.kc1 / c->Ms);
+  a.dmi[0] = (float)(c->dmi / (c->Ms * c->dx));
+  a.dmi[1] = (float)(c->dmi / (c->Ms * c->dy));
   {
     double c1[3], c2[3], n1, n2;
     n1 = std::sqrt(c->K.c1[0] * c->K.c1[0] + c->K.c1[1] * c->K.c1[1] + c->K.c1[2] * c->K.c1[2]);
@@ -1052,6 +1055,13 @@ int mcq_set_cavity_mode(mcq_ctx* c, int k, double f_c, double kappa, double x0, 
 
 int mcq_set_cavity(mcq_ctx* c, double f_c, double kappa, double x0, double p0) {
   return c ? mcq_set_cavity_mode(c, 0, f_c, kappa, x0, p0) : MCQ_EINVAL;
+}
+
+int mcq_set_dmi(mcq_ctx* c, double D) {
+  if (!c || !std::isfinite(D)) return MCQ_EINVAL;
+  c->dmi = D;
+  invalidate_graphs(c);
+  return MCQ_OK;
 }
 
 int mcq_set_excitation_mode(mcq_ctx* c, int k, double amplitude, double omega_cut) {

@@ -84,7 +84,7 @@ struct RowAddr {  // shared-memory address of element pos of component-line l of
 // the demag field.  Computes B' and, by mode, the field (Bout),
 // the max torque, or the RK4 stage update (returns m_{s+1}, writes the new accumulator to
 // acc_out).  All memory traffic (and the overlap sums) stays in the caller.
-template <bool DPM>
+template <bool GEN>
 __device__ __forceinline__ float3 cell_core(const UpdateArgs& a, float3 m, const float3 (&nb)[6], const bool (&ok)[6],
                                             float3 mn, float3 ap, float3 bcav, float gmul, float3 Bd,
                                             float& tmax, float3& acc_out, float3& Bout) {
@@ -131,6 +131,15 @@ __device__ __forceinline__ float3 cell_core(const UpdateArgs& a, float3 m, const
         B.z += f1 * a.c1[2] + f2 * a.c2[2] + f3 * a.c3[2];
       }
     }
+    if (GEN && (a.terms & MCQ_TERM_DMI) && (a.dmi[0] != 0.f || a.dmi[1] != 0.f)) {
+      // interfacial DMI, central differences, Neumann ghosts (own m) outside the mesh / in vacuum
+      float3 g[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) g[k] = (ok[k] && dot3(nb[k], nb[k]) > 0.f) ? nb[k] : m;
+      B.x += a.dmi[0] * (g[1].z - g[0].z);
+      B.y += a.dmi[1] * (g[3].z - g[2].z);
+      B.z -= a.dmi[0] * (g[1].x - g[0].x) + a.dmi[1] * (g[3].y - g[2].y);
+    }
     if (gmul != 0.f) {
       B.x += bcav.x * gmul;
       B.y += bcav.y * gmul;
@@ -148,7 +157,7 @@ __device__ __forceinline__ float3 cell_core(const UpdateArgs& a, float3 m, const
   }
   const float3 mmxB = cross3(m, mxB);
   float3 k;
-  if (a.mode == MODE_LLG || (DPM && a.mode == MODE_DP)) {
+  if (a.mode == MODE_LLG || (GEN && a.mode == MODE_DP)) {
     k = make_float3(-a.gl * (mxB.x + a.alpha * mmxB.x), -a.gl * (mxB.y + a.alpha * mmxB.y),
                     -a.gl * (mxB.z + a.alpha * mmxB.z));
   } else {  // MODE_RELAX: -gamma m x (m x B)
@@ -156,7 +165,7 @@ __device__ __forceinline__ float3 cell_core(const UpdateArgs& a, float3 m, const
   }
   const int stage = a.stage;
   if (stage == 1) mn = m;
-  if (DPM && a.mode == MODE_DP) {  // ap = sum_{j < s} comb[j-1] k_j from the caller (reading C-DP)
+  if (GEN && a.mode == MODE_DP) {  // ap = sum_{j < s} comb[j-1] k_j from the caller (reading C-DP)
     const float cs = a.comb[stage - 1];
     const float3 inc = make_float3(ap.x + cs * k.x, ap.y + cs * k.y, ap.z + cs * k.z);
     acc_out = k;
@@ -196,9 +205,9 @@ __device__ __forceinline__ float2 sm_pair(const float* p) { return *reinterpret_
 #ifndef MCQ_UMINB
 #define MCQ_UMINB 5  // min resident CTAs per SM requested from ptxas (96-register cap: 84.8 vs 86.8 us on configs[1])
 #endif
-// MM: cavity modes compiled in (1, or kMaxModes with a.nmodes <= MM at run time); DPM: the
-// Dormand-Prince stage mode compiled in (kept out of the RK4 instances)
-template <int N2, int MM, bool DPM>
+// MM: cavity modes compiled in (1, or kMaxModes with a.nmodes <= MM at run time); GEN: the
+// general instance (Dormand-Prince stages, interfacial DMI) — kept out of the plain RK4 ones
+template <int N2, int MM, bool GEN>
 __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a, const float2* __restrict__ gtw) {
   using Cf = UCfg<N2>;
   constexpr int E = Cf::E, TL = Cf::TL, RY = Cf::RY, NT = Cf::NT, LX = 2 * N2, PITCH = Cf::PITCH;
@@ -345,7 +354,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
   double wacc[MM];
 #pragma unroll
   for (int k = 0; k < MM; ++k) wacc[k] = 0.0;
-  const bool dp = DPM && a.mode == MODE_DP;
+  const bool dp = GEN && a.mode == MODE_DP;
   // overlaps (and the trace's sum m) of the step result: RK4 stage 4's output, DP stage 7's input
   const bool wsum = (a.mode == MODE_LLG && a.stage == 4) || (dp && a.stage == 7);
   float tmax = 0.f;
@@ -431,7 +440,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
         float3 accn = make_float3(0.f, 0.f, 0.f), Bf = make_float3(0.f, 0.f, 0.f);
         float3 out;
         if constexpr (MM == 1) {
-          out = cell_core<DPM>(a, m, nb, ok, mn, ap, br, gsum, Bd, tmax, accn, Bf);
+          out = cell_core<GEN>(a, m, nb, ok, mn, ap, br, gsum, Bd, tmax, accn, Bf);
         } else {
           float3 bcav = make_float3(br.x * gsum, br.y * gsum, br.z * gsum);
 #pragma unroll
@@ -442,7 +451,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
               bcav.z += MCQ_PICK(bk2[k - 1][2]) * gs[k];
             }
           }
-          out = cell_core<DPM>(a, m, nb, ok, mn, ap, bcav, any_cav ? 1.f : 0.f, Bd, tmax, accn, Bf);
+          out = cell_core<GEN>(a, m, nb, ok, mn, ap, bcav, any_cav ? 1.f : 0.f, Bd, tmax, accn, Bf);
         }
         if (wsum) {
           wacc[0] += (double)(br.x * out.x) + (double)(br.y * out.y) + (double)(br.z * out.z);
@@ -610,7 +619,7 @@ void launch_update(const UpdateArgs& a, const float2* tw, cudaStream_t st) {
   MCQ_DISPATCH_N2(a.d.N2, {
     using Cf = UCfg<N2>;
     dim3 grid((a.d.ny + Cf::RY - 1) / Cf::RY, a.d.nz);
-    if (a.mode == MODE_DP)
+    if (a.mode == MODE_DP || a.dmi[0] != 0.f || a.dmi[1] != 0.f)
       launch_pdl(a.d.pdl, k_update<N2, kMaxModes, true>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
     else if (a.nmodes > 1)
       launch_pdl(a.d.pdl, k_update<N2, kMaxModes, false>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);

@@ -49,11 +49,12 @@ def test_binding_covers_header_and_constants(built):
     for n in _declared():
         assert callable(getattr(mcq, n))
     d = _defines()
-    assert d["MCQ_TERM_ALL"] == mcq.TERM_ALL == 63
+    assert d["MCQ_TERM_ALL"] == mcq.TERM_ALL == 127 and d["MCQ_TERM_DMI"] == mcq.TERM_DMI == 64
     assert (d["MCQ_TERM_ZEEMAN"], d["MCQ_TERM_EXCHANGE"], d["MCQ_TERM_ANIS"], d["MCQ_TERM_DEMAG"],
             d["MCQ_TERM_CAVITY"], d["MCQ_TERM_EXCITATION"]) == (1, 2, 4, 8, 16, 32)
     from oracle import sim as S
-    assert (S.ZEEMAN, S.EXCHANGE, S.ANIS, S.DEMAG, S.CAVITY, S.EXCITATION) == (1, 2, 4, 8, 16, 32)
+    assert (S.ZEEMAN, S.EXCHANGE, S.ANIS, S.DEMAG, S.CAVITY, S.EXCITATION, S.DMI) == (1, 2, 4, 8, 16, 32, 64)
+    assert S.ALL == 127
     assert d["MCQ_NKCLASS"] == mcq.NKCLASS
     assert d["MCQ_TRACE_COLS"] == len(mcq.TRACE_COLS) == 8
     assert (d["MCQ_OK"], d["MCQ_EINVAL"], d["MCQ_ESTATE"]) == (0, -1, -2)
