@@ -323,7 +323,8 @@ def main():
                        "padded_fft": [L["Lx"], L["Ly"], L["Lz"]]},
             "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": pk["hbm_gbs"],
                          "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
-                         "traffic_source": (f"profiles/{traffic_src} (ncu --set full, dram bytes read+write per launch)"
+                         "traffic_source": (f"profiles/ncu_traffic.json from {traffic_src} (ncu --set full, dram "
+                                            f"bytes read+write per launch; summary profiles/r1_final_ncu_full.txt)"
                                             if traffic_src else None),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("_fallback") else "fallback",
                          "alg_bytes_per_launch": ab[top], "ms_per_launch": prof[top][0]},

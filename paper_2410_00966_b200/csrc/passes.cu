@@ -227,6 +227,9 @@ __global__ void __launch_bounds__(ZCfg<L>::NT) k_conv(float2* __restrict__ Y, co
 #ifndef MCQ_ZNT
 #define MCQ_ZNT 256  // target threads per CTA in K-Z
 #endif
+#ifndef MCQ_ZPAIR
+#define MCQ_ZPAIR 1  // order K-Z rows as (0, Ly/2, 1, Ly-1, 2, ...): shared Khat rows back to back (1.025 vs 1.036 ms/step)
+#endif
 template <int L, int CW = 0>
 struct ZSCfg {
   static constexpr int E = L <= MCQ_ZSE ? L : MCQ_ZSE;
@@ -264,7 +267,14 @@ __global__ void __launch_bounds__(ZSCfg<L, CW>::NT) k_zconv_seq(float2* __restri
   const bool lone = (int)blockIdx.x < nlone;
   const int b = blockIdx.x - nlone;
   const int kxl = lone ? d.kxw - 1 : (b % nfull) * C + c, kx = d.kx0 + kxl;
-  const int ky = lone ? blockIdx.x * C + c : b / nfull;
+#if MCQ_ZPAIR
+  // rows ky and Ly - ky read the same folded Khat rows: schedule them back to back (L2 reuse)
+  const int kyi = b / nfull, kyh = kyi >> 1;
+  const int kyn = kyi == 1 ? d.Ly / 2 : ((kyi & 1) ? d.Ly - kyh : kyh);
+#else
+  const int kyn = b / nfull;
+#endif
+  const int ky = lone ? blockIdx.x * C + c : kyn;
   const bool ok = kxl < d.kxw && ky < d.Ly;
   const int kyc = ky < d.Ly ? ky : d.Ly - 1;  // in-range row for address arithmetic
   const int nz = d.nzg, nzl = d.nz;
