@@ -50,6 +50,9 @@ __device__ __forceinline__ void pass_tw(float2* tw, const float2* __restrict__ g
 #ifndef MCQ_YE
 #define MCQ_YE 16   // points per thread per line in K-Y / K-YI
 #endif
+#ifndef MCQ_YREV
+#define MCQ_YREV 1  // K-Y / K-YI CTA order: z descending, components inner (1.013 vs 1.025 ms/step)
+#endif
 #ifndef MCQ_YNT
 #define MCQ_YNT 256  // target threads per CTA in K-Y / K-YI
 #endif
@@ -99,11 +102,18 @@ __global__ void __launch_bounds__(PassCfg<L, CW>::NT) k_ypass(const float2* __re
   // (NKX = C * nfull + 1), so that column costs nz / C CTAs instead of nz mostly idle ones
   // (scheduled first: as the last wave they would extend the kernel's tail); the others are
   // column tile (b % nfull) at plane b / nfull
+#if MCQ_YREV
+  // z descending with the components inner: the passes meet the planes the previous kernel
+  // (K-U, which runs z ascending) wrote last, while they are still in L2
+  const int b = blockIdx.x, rest = b / nfull;
+  const int comp = rest % 3, kx = (b % nfull) * C + c, z = d.nz - 1 - rest / 3;
+#else
   const int nlone = (gridDim.x - nfull * d.nz), comp = blockIdx.y;
   const bool lone = (int)blockIdx.x < nlone;
   const int b = blockIdx.x - nlone;
   const int kx = lone ? d.NKX - 1 : (b % nfull) * C + c;
   const int z = lone ? blockIdx.x * C + c : b / nfull;
+#endif
   const bool ok = kx < d.NKX && z < d.nz;
   const int nin = INV ? L : d.ny, nout = INV ? d.ny : L;
   // X side: X[c][z][y][P]; Y side: kx-slab-major Y[q][c][z][ky][KXS] (common.cuh)
@@ -474,7 +484,8 @@ int launch_yfwd(const Dims& d, const float2* X, float2* Y, const float2* tw, cud
     using Cf = PassCfg<L>;
     // (lone-column CTAs as in K-Z measured slower here: 38.9 / 37.8 vs 37.8 / 35.6 us)
     const int nfull = (d.NKX + Cf::C - 1) / Cf::C;
-    launch_pdl(d.pdl, k_ypass<L, false>, dim3(nfull * d.nz, 3), dim3(Cf::NT), Cf::SMEM, st, X, Y, d, tw, nfull), ++n;
+    launch_pdl(d.pdl, k_ypass<L, false>, MCQ_YREV ? dim3(nfull * d.nz * 3) : dim3(nfull * d.nz, 3), dim3(Cf::NT),
+               Cf::SMEM, st, X, Y, d, tw, nfull), ++n;
   })
   return n;
 }
@@ -485,7 +496,8 @@ int launch_yinv(const Dims& d, const float2* Y, float2* X, const float2* tw, cud
     using Cf = PassCfg<L>;
     // (lone-column CTAs as in K-Z measured slower here: 38.9 / 37.8 vs 37.8 / 35.6 us)
     const int nfull = (d.NKX + Cf::C - 1) / Cf::C;
-    launch_pdl(d.pdl, k_ypass<L, true>, dim3(nfull * d.nz, 3), dim3(Cf::NT), Cf::SMEM, st, Y, X, d, tw, nfull), ++n;
+    launch_pdl(d.pdl, k_ypass<L, true>, MCQ_YREV ? dim3(nfull * d.nz * 3) : dim3(nfull * d.nz, 3), dim3(Cf::NT),
+               Cf::SMEM, st, Y, X, d, tw, nfull), ++n;
   })
   return n;
 }
