@@ -189,7 +189,8 @@ MCQ_API int mcq_run(mcq_ctx *, double dt, long long steps);
  * 5th-order solution propagated, error estimate err = max_i |dt sum_j (b5_j - b4_j) k_j| (max
  * over cells, fp32); the cavity memory is frozen inside a step at the stage nodes c_s (C3) and
  * advanced by the accepted step's dt (eq:Sdiscrete with the step variable).  No FSAL reuse.
- * mcq_run_dp: `steps` fixed steps of size dt (every step accepted; no graph, no host sync).
+ * mcq_run_dp: `steps` fixed steps of size dt (every step accepted; replayed as CUDA graphs like
+ * mcq_run, no host sync).
  * mcq_run_adaptive: advances the cavity clock by `duration` (s) from its current value: an
  * attempt with err <= tol (dimensionless, |m| = 1) is accepted, else m_n and the memory are
  * left untouched; the next step is h * min(5, max(0.2, 0.9 (tol/err)^(1/5))), clipped to the
@@ -238,7 +239,8 @@ MCQ_API int mcq_cavity_status(const mcq_ctx *);
 MCQ_API long long mcq_kernel_launches(const mcq_ctx *);
 
 /* On-device trace of the per-step observables (the spectra of P:172 are
- * the numerical FT of the spatially averaged m).  After every `every`-th completed LLG step the
+ * the numerical FT of the spatially averaged m).  After every `every`-th completed (accepted)
+ * RK4 or Dormand-Prince step the
  * cavity kernel appends one row of MCQ_TRACE_COLS doubles:
  *     t_{n+1} (s), <m_x>, <m_y>, <m_z> (mean over magnetic cells, from the same fixed-order
  *     per-CTA fp64 partials as W), Re alpha, Im alpha, W (A/m T), n+1
