@@ -65,7 +65,8 @@ extern "C" {
 #define MCQ_TERM_CAVITY 16u     /* B_rms * Gamma(t) */
 #define MCQ_TERM_EXCITATION 32u /* a sinc(w_cut t) B_rms */
 #define MCQ_TERM_DMI 64u        /* interfacial Dzyaloshinskii-Moriya (mcq_set_dmi) */
-#define MCQ_TERM_ALL 127u
+#define MCQ_TERM_ALL 127u       /* the deterministic terms */
+#define MCQ_TERM_THERM 128u     /* thermal field (mcq_set_temperature); stochastic, not in ALL */
 
 /* kernel classes reported by mcq_profile_run */
 #define MCQ_K_YFWD 0   /* y-forward FFT pass (3D)                        */
@@ -152,6 +153,19 @@ MCQ_API int mcq_set_cavity(mcq_ctx *, double f_c, double kappa, double x0, doubl
  * differences and Neumann ghosts (own m) at mesh and vacuum boundaries. */
 MCQ_API int mcq_set_dmi(mcq_ctx *, double D);
 
+/* Temperature T (K, >= 0; 0 = off) and the seed of the thermal stream (P:188 lists the thermal
+ * field among the Mumax3 terms).  Reading C-TH (Mumax3's Brown field):
+ * B_th = eta sqrt(2 alpha k_B T / (gamma M_s V_cell dt)) in magnetic cells, eta a standard normal
+ * 3-vector per cell drawn once per mcq_run step and held for its four RK4 stages.  eta is
+ * counter-based and reproducible: SplitMix64 started at state `seed`, counters
+ * 2 (n N + g) and 2 (n N + g) + 1 for global cell g = (z ny + y) nx + x at step n (the cavity
+ * state's step count), N cells; Box-Muller on u1 = (h >> 40 + 1) 2^-24, u2 = (h & 0xFFFFFF)
+ * 2^-24 gives eta = (r0 cos 2pi u2_0, r0 sin 2pi u2_0, r1 cos 2pi u2_1), r = sqrt(-2 ln u1).
+ * mcq_get_field with MCQ_TERM_THERM returns the draw of the next step scaled for the last
+ * mcq_run's dt (ESTATE before any run).  With T > 0, mcq_run_dp / mcq_run_adaptive return
+ * ESTATE (defined for the fixed-step RK4 path only); mcq_relax ignores the thermal field. */
+MCQ_API int mcq_set_temperature(mcq_ctx *, double T, unsigned long long seed);
+
 /* Excitation a * sinc(w_cut t) * B_rms, unnormalised sinc, t = cavity clock (C13). */
 MCQ_API int mcq_set_excitation(mcq_ctx *, double amplitude, double omega_cut);
 
@@ -217,7 +231,13 @@ MCQ_API int mcq_ovf_write(const char *path, const int grid[3], const double cell
                           int representation);
 MCQ_API const char *mcq_ovf_last_error(void);
 
-/* Block until all enqueued work is done; reports asynchronous kernel errors (ECUDA). */
+/* Block until all enqueued work is done; reports asynchronous kernel errors (ECUDA).  Failure
+ * detection: the last stage of every step (RK4 stage 4 / DP stage 7) flags a non-finite new m
+ * (through its overlap partial W_0, which any NaN / inf component turns NaN); once flagged,
+ * every mcq_synchronize returns ESTATE ("diverged") until mcq_set_m installs a fresh state
+ * (mcq_set_m clears the flag; a diverged run leaves the cavity memory non-finite too, so reset
+ * it with mcq_reset_memory, or it flags the next step again).
+ * The flag covers this process's cells (per rank under a distributed context). */
 MCQ_API int mcq_synchronize(mcq_ctx *);
 
 /* Magnetisation out, 3N floats interleaved (host / device pointer). */

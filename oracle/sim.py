@@ -19,11 +19,13 @@ import numpy as np
 from .constants import GAMMA, HBAR
 from . import fields as F
 from . import tensor as T
+from . import thermal as TH
 from .cavity import CavityMemory
 from .llg import torque, relax_torque, normalize, rk4_step, dp45_step, dp_controller
 
 ZEEMAN, EXCHANGE, ANIS, DEMAG, CAVITY, EXCITATION, DMI = 1, 2, 4, 8, 16, 32, 64
 ALL = ZEEMAN | EXCHANGE | ANIS | DEMAG | CAVITY | EXCITATION | DMI
+THERM = 128    # the thermal field (reading C-TH): stochastic, so not part of ALL
 RELAX_CHECK_EVERY = 50
 
 
@@ -31,7 +33,7 @@ class Simulation:
     def __init__(self, grid, cell, Ms, Aex, alpha, m0, mask=None, bext=(0.0, 0.0, 0.0),
                  brms_map=None, brms_uniform=(0.0, 0.0, 0.0), f_c=1e9, kappa=0.0, x0=0.0, p0=0.0,
                  exc_amp=0.0, exc_omega=0.0, aniso=None, demag="auto", octant=None, hbar=HBAR,
-                 gamma=GAMMA, terms=ALL, modes=(), dmi=0.0):
+                 gamma=GAMMA, terms=ALL, modes=(), dmi=0.0, temperature=0.0, seed=0):
         self.grid = tuple(int(g) for g in grid)
         nx, ny, nz = self.grid
         self.shape = (nz, ny, nx)
@@ -49,6 +51,9 @@ class Simulation:
             self.brms = F.zeeman(self.shape, brms_uniform)
         self.aniso = aniso or {}
         self.dmi = float(dmi)       # interfacial DMI constant D (J/m^2), reading C-DMI
+        self.temperature, self.seed = float(temperature), int(seed)   # reading C-TH
+        self.th_dt = None           # dt of the last run: the thermal field's scale
+        self._bth = None            # B_th of the step in progress
         self.exc_amp, self.exc_omega = float(exc_amp), float(exc_omega)
         self.mem = CavityMemory(2 * math.pi * f_c, kappa, x0, p0, self.vcell, hbar)
         # extra modes k >= 1 (reading C-MM): dicts with brms_map | brms_uniform, f_c, kappa,
@@ -94,6 +99,7 @@ class Simulation:
         """B'(m, t) summed in the fixed order Zeeman, exchange, anisotropy, demag, excitation,
         cavity; vacuum cells get 0.  Gamma uses the S_n, C_n of the last completed step (C3)."""
         B = np.zeros_like(m)
+        therm = terms & THERM
         terms &= self.terms
         if terms & ZEEMAN:
             B += F.zeeman(self.shape, self.bext)
@@ -118,7 +124,16 @@ class Simulation:
                 B += a_k * float(F.sinc(w_k * t)) * b
             if terms & CAVITY and np.any(b != 0):
                 B += b * mem.gamma(t)
+        if therm and self.temperature > 0.0:       # the next step's draw (reading C-TH)
+            if self.th_dt is None:
+                raise RuntimeError("thermal field before any run (its scale needs dt)")
+            B += self.thermal(self.th_dt)
         return np.where(self.mag[..., None], B, 0.0)
+
+    def thermal(self, dt):
+        """B_th of step n = mem.step (steps completed), for time step dt (reading C-TH)."""
+        sig = TH.sigma(self.alpha, self.temperature, self.gamma, self.Ms, self.vcell, dt)
+        return TH.thermal_field(self.shape, self.mag, self.seed, self.mem.step, sig)
 
     def W(self, m):
         """Overlap W = sum_i M_s,i m_i . B_rms(r_i)."""
@@ -126,10 +141,17 @@ class Simulation:
 
     # ---------------------------------------------------------------- stepping (steps 4-6)
     def rhs(self, m, t):
-        return torque(m, self.field(m, t), self.alpha, self.gamma)
+        B = self.field(m, t)
+        if self._bth is not None:                  # held for all stages of the step (C-TH)
+            B = B + self._bth
+        return torque(m, B, self.alpha, self.gamma)
 
     def step(self, dt):
+        if self.temperature > 0.0:
+            self.th_dt = dt
+            self._bth = self.thermal(dt)
         self.m = rk4_step(self.rhs, self.m, self.mem.t, dt)
+        self._bth = None
         W = self.W(self.m) if self.cavity_enabled else 0.0
         self.mem.update(W, dt)
         for b, mem, _, _ in self.extra:              # every mode advances on its own overlap
@@ -152,6 +174,8 @@ class Simulation:
     def step_dp(self, dt):
         """One fixed Dormand-Prince step (reading C-DP), memory advanced with this dt (C3-C5).
         Returns the error estimate."""
+        if self.temperature > 0.0:
+            raise RuntimeError("the thermal field is defined for the fixed-step RK4 path only (C-TH)")
         self.m, err = dp45_step(self.rhs, self.m, self.mem.t, dt)
         self._advance_memory(dt)
         return err
@@ -161,6 +185,8 @@ class Simulation:
         and memory advance by its dt, the step variable of eq:Sdiscrete/eq:Cdiscrete), a rejected
         one leaves both untouched; the next dt follows dp_controller, clipped to the end time.
         Returns (accepted, rejected, dt_next, accepted dts)."""
+        if self.temperature > 0.0:
+            raise RuntimeError("the thermal field is defined for the fixed-step RK4 path only (C-TH)")
         t_end = self.mem.t + duration
         dt, acc, rej, dts = dt0, 0, 0, []
         while t_end - self.mem.t > 1e-12 * max(duration, 1e-30) and acc + rej < max_attempts:

@@ -12,7 +12,7 @@ import numpy as np
 
 from ._lib import (lib, MCQError, mcq_aniso, mcq_dist, mcq_cavity_state, EXPORTED,  # noqa: F401
                    TERM_ZEEMAN, TERM_EXCHANGE, TERM_ANIS, TERM_DEMAG, TERM_CAVITY, TERM_EXCITATION,
-                   TERM_DMI, TERM_ALL, NKCLASS, KCLASS_NAMES, K_YFWD, K_ZCONV, K_YINV, K_Y2D, K_UPDATE, K_CAVITY)
+                   TERM_DMI, TERM_ALL, TERM_THERM, NKCLASS, KCLASS_NAMES, K_YFWD, K_ZCONV, K_YINV, K_Y2D, K_UPDATE, K_CAVITY)
 
 __all__ = [n for n in EXPORTED] + ["Solver", "MCQError"]
 
@@ -119,6 +119,11 @@ def mcq_set_excitation(ctx, amplitude, omega_cut):
 def mcq_set_dmi(ctx, D):
     """Interfacial DMI constant D (J/m^2), reading C-DMI (include/mcq.h)."""
     _check(ctx, lib.mcq_set_dmi(ctx, float(D)))
+
+
+def mcq_set_temperature(ctx, T, seed=0):
+    """Temperature (K) and thermal-stream seed, reading C-TH (include/mcq.h)."""
+    _check(ctx, lib.mcq_set_temperature(ctx, float(T), int(seed) & (2**64 - 1)))
 
 
 def mcq_reset_memory(ctx):

@@ -15,6 +15,7 @@ MCQ_OK, MCQ_EINVAL, MCQ_ESTATE, MCQ_ENOMEM, MCQ_ECUDA, MCQ_ENCCL = 0, -1, -2, -3
 TERM_ZEEMAN, TERM_EXCHANGE, TERM_ANIS, TERM_DEMAG, TERM_CAVITY, TERM_EXCITATION = 1, 2, 4, 8, 16, 32
 TERM_DMI = 64
 TERM_ALL = 127
+TERM_THERM = 128
 K_YFWD, K_ZCONV, K_YINV, K_Y2D, K_UPDATE, K_CAVITY = range(6)
 NKCLASS = 6
 KCLASS_NAMES = ("yfwd", "zconv", "yinv", "y2d", "update", "cavity")
@@ -64,6 +65,7 @@ _sig = {
     "mcq_set_cavity": (C.c_int, [_P, C.c_double, C.c_double, C.c_double, C.c_double]),
     "mcq_set_excitation": (C.c_int, [_P, C.c_double, C.c_double]),
     "mcq_set_dmi": (C.c_int, [_P, C.c_double]),
+    "mcq_set_temperature": (C.c_int, [_P, C.c_double, C.c_ulonglong]),
     "mcq_reset_memory": (C.c_int, [_P]),
     "mcq_set_modes": (C.c_int, [_P, C.c_int]),
     "mcq_set_brms_mode": (C.c_int, [_P, C.c_int, _P, C.POINTER(C.c_double)]),

@@ -49,6 +49,7 @@ inline cudaError_t launch_pdl(bool pdl, void (*k)(KArgs...), dim3 g, dim3 b, siz
 constexpr double kGamma = 1.7595e11;             // rad s^-1 T^-1 (reading C8)
 constexpr double kMu0 = 4e-7 * 3.14159265358979323846;
 constexpr double kHbar = 1.05457182e-34;         // J s
+constexpr double kKB = 1.380649e-23;             // J K^-1, SI exact (thermal field, reading C-TH)
 constexpr int kTwMax = 1024;                     // global twiddle table length (max FFT length)
 
 // Sizes of one context's padded spectral layout.  Row layout, kx fastest:
@@ -163,6 +164,12 @@ struct UpdateArgs {
   double* partials;   // per-CTA overlap partials (stage 4)
   float* bout;        // MODE_FIELD output (SoA)
   unsigned* maxbits;  // MODE_MAXTORQUE output (float bits, >= 0)
+  int* nonfinite;     // set to 1 by the step's last stage when some m_{n+1} is not finite
+  // thermal field (reading C-TH): B_th = th * eta(th_seed, step, global cell), th = sqrt(2 alpha
+  // k_B T / (gamma M_s V dt)) for the run's dt (0: off); eta from SplitMix64 + Box-Muller, drawn
+  // once per step (counter = the cavity state's step count) and held for all its stages
+  float th;
+  unsigned long long th_seed;
   int demag;          // run the x-C2R demag phase
   int trace;          // stage 4: also accumulate sum m for the trace
   // MODE_DP (Dormand-Prince, reading C-DP), stage s = 1..7 with h = dt: K[j] = k_{j+1} ([3][cs]

@@ -115,6 +115,9 @@ struct mcq_ctx {
   bool have_mask = false;
   double bext[3] = {0, 0, 0};
   double dmi = 0;  // interfacial DMI constant (J/m^2)
+  double temperature = 0;           // K (reading C-TH; 0: no thermal field)
+  unsigned long long th_seed = 0;   // SplitMix64 start state of the thermal stream
+  double th_dt = 0;                 // dt of the last mcq_run: the field getter's thermal scale
   double fc[kMaxModes] = {1e9, 1e9, 1e9, 1e9}, kappa[kMaxModes] = {}, x0[kMaxModes] = {}, p0[kMaxModes] = {};
   double exc_amp[kMaxModes] = {}, exc_omega[kMaxModes] = {};
   CavState* cav = nullptr;
@@ -125,6 +128,7 @@ struct mcq_ctx {
   int trace_every = 1;
   long long n_magnetic = 0;
   unsigned* maxbits = nullptr;
+  int* nonfinite = nullptr;  // divergence flag (set by the update kernel, read by mcq_synchronize)
   int* bad = nullptr;
   float* io = nullptr;  // AoS staging for the cells this context holds
   bool m_set = false;
@@ -214,6 +218,11 @@ CavParams cav_params(const mcq_ctx* c, double dt, bool dp = false) {
   return p;
 }
 
+// sigma of each B_th component for time step dt (reading C-TH, Mumax3's Brown field)
+static double th_sigma(const mcq_ctx* c, double dt) {
+  return std::sqrt(2.0 * c->alpha * kKB * c->temperature / (kGamma * c->Ms * c->dx * c->dy * c->dz * dt));
+}
+
 UpdateArgs base_args(const mcq_ctx* c, const Slab& s) {
   UpdateArgs a{};
   a.d = s.d;
@@ -259,6 +268,7 @@ UpdateArgs base_args(const mcq_ctx* c, const Slab& s) {
   a.partials = s.partials;
   a.bout = s.field;
   a.maxbits = c->maxbits;
+  a.nonfinite = c->nonfinite;
   a.X = s.X;
   a.acc = s.acc;
   a.demag = 1;
@@ -407,6 +417,10 @@ struct Enq {
       a.mOut = st == 1 ? sl.mA : (st == 2 ? sl.mB : (st == 3 ? sl.mA : sl.mN));
       a.h = (float)(st == 3 ? dt : 0.5 * dt);
       a.dt6 = (float)(dt / 6.0);
+      if (mode == MODE_LLG && c->temperature > 0) {  // one draw per step, held for its stages
+        a.th = (float)th_sigma(c, dt);
+        a.th_seed = c->th_seed;
+      }
       update(a);
     }
   }
@@ -493,6 +507,10 @@ struct Enq {
       a.mS = sl.mN;
       a.mN = sl.mN;
       a.mOut = sl.mN;
+      if (mode == MODE_FIELD && (terms & MCQ_TERM_THERM) && c->temperature > 0 && c->th_dt > 0) {
+        a.th = (float)th_sigma(c, c->th_dt);  // the draw the next step will use
+        a.th_seed = c->th_seed;
+      }
       update(a);
     }
     x0();
@@ -638,7 +656,7 @@ void free_all(mcq_ctx* c) {
     if (c->mode == 2 && s.partials) cudaFree(s.partials);
   }
   c->sl.clear();
-  void* ptrs[] = {c->tw, c->khat, c->cav, c->partials, c->maxbits, c->bad, c->io, c->trace};
+  void* ptrs[] = {c->tw, c->khat, c->cav, c->partials, c->maxbits, c->bad, c->nonfinite, c->io, c->trace};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->comm) nccl_api()->commDestroy(c->comm);
@@ -829,6 +847,7 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
             cudaMalloc(&c->tw, kTwMax * 8) == cudaSuccess && cudaMalloc(&c->cav, sizeof(CavState)) == cudaSuccess &&
             cudaMalloc(&c->partials, (size_t)c->nparts * kNPart * 8) == cudaSuccess &&
             cudaMalloc(&c->maxbits, 4) == cudaSuccess && cudaMalloc(&c->bad, 4) == cudaSuccess &&
+            cudaMalloc(&c->nonfinite, 4) == cudaSuccess &&
             cudaMalloc(&c->io, 3ULL * c->cells_here() * 4) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
@@ -844,7 +863,8 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
   }
   if (cudaMemsetAsync(c->khat, 0, 6ULL * (g.Lz / 2 + 1) * (g.Ly / 2 + 1) * g.P * 4, c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->partials, 0, (size_t)c->nparts * kNPart * 8, c->stream) != cudaSuccess ||
-      cudaMemsetAsync(c->maxbits, 0, 4, c->stream) != cudaSuccess)
+      cudaMemsetAsync(c->maxbits, 0, 4, c->stream) != cudaSuccess ||
+      cudaMemsetAsync(c->nonfinite, 0, 4, c->stream) != cudaSuccess)
     return bail(MCQ_ECUDA);
   // twiddles w_1024^m = exp(-2 pi i m / 1024), generated in fp64
   {
@@ -946,6 +966,7 @@ static int set_m_from_io(mcq_ctx* c) {
   Enq q{c, c->stream};
   q.x0();
   c->launches += q.count + (long long)c->sl.size();
+  CK(c, cudaMemsetAsync(c->nonfinite, 0, 4, c->stream));  // a fresh state clears a divergence
   CK(c, cudaGetLastError());
   c->m_set = true;
   return MCQ_OK;
@@ -1057,6 +1078,14 @@ int mcq_set_cavity(mcq_ctx* c, double f_c, double kappa, double x0, double p0) {
   return c ? mcq_set_cavity_mode(c, 0, f_c, kappa, x0, p0) : MCQ_EINVAL;
 }
 
+int mcq_set_temperature(mcq_ctx* c, double T, unsigned long long seed) {
+  if (!c || !std::isfinite(T) || T < 0) return MCQ_EINVAL;
+  c->temperature = T;
+  c->th_seed = seed;
+  invalidate_graphs(c);
+  return MCQ_OK;
+}
+
 int mcq_set_dmi(mcq_ctx* c, double D) {
   if (!c || !std::isfinite(D)) return MCQ_EINVAL;
   c->dmi = D;
@@ -1087,6 +1116,7 @@ int mcq_run(mcq_ctx* c, double dt, long long steps) {
   if (!(dt > 0) || steps < 0) return fail(c, MCQ_EINVAL, "dt must be > 0 and steps >= 0");
   if (!c->m_set) return fail(c, MCQ_ESTATE, "mcq_run before mcq_set_m");
   if (steps == 0) return MCQ_OK;
+  c->th_dt = dt;
   const CavParams p = cav_params(c, dt);
   launch_cav_prepare(p, c->cav, c->stream);
   c->launches += 1;
@@ -1147,6 +1177,7 @@ int mcq_run_dp(mcq_ctx* c, double dt, long long steps) {
   if (!c) return MCQ_EINVAL;
   if (!(dt > 0) || steps < 0) return fail(c, MCQ_EINVAL, "dt must be > 0 and steps >= 0");
   if (!c->m_set) return fail(c, MCQ_ESTATE, "mcq_run_dp before mcq_set_m");
+  if (c->temperature > 0) return fail(c, MCQ_ESTATE, "the thermal field is defined for mcq_run (RK4) only");
   int rc = ensure_dp(c);
   if (rc != MCQ_OK) return rc;
   if (steps == 0) return MCQ_OK;
@@ -1167,6 +1198,7 @@ int mcq_run_adaptive(mcq_ctx* c, double duration, double dt0, double tol, long l
   if (!c) return MCQ_EINVAL;
   if (!(duration >= 0) || !(dt0 > 0) || !(tol > 0) || max_attempts < 0)
     return fail(c, MCQ_EINVAL, "adaptive: duration >= 0, dt0 > 0, tol > 0, max_attempts >= 0");
+  if (c->temperature > 0) return fail(c, MCQ_ESTATE, "the thermal field is defined for mcq_run (RK4) only");
   if (!c->m_set) return fail(c, MCQ_ESTATE, "mcq_run_adaptive before mcq_set_m");
   int rc = ensure_dp(c);
   if (rc != MCQ_OK) return rc;
@@ -1211,6 +1243,9 @@ int mcq_synchronize(mcq_ctx* c) {
   if (!c) return MCQ_EINVAL;
   CK(c, cudaStreamSynchronize(c->stream));
   CK(c, cudaGetLastError());
+  int nf = 0;
+  CK(c, cudaMemcpy(&nf, c->nonfinite, 4, cudaMemcpyDeviceToHost));
+  if (nf) return fail(c, MCQ_ESTATE, "the integration diverged: a non-finite magnetisation was produced (time step too large?); set a new state with mcq_set_m");
   return MCQ_OK;
 }
 
@@ -1245,6 +1280,8 @@ int mcq_get_m_device(mcq_ctx* c, float* d_out) {
 int mcq_get_field(mcq_ctx* c, float* b_out, unsigned terms) {
   if (!c || !b_out) return MCQ_EINVAL;
   if (!c->m_set) return fail(c, MCQ_ESTATE, "mcq_get_field before mcq_set_m");
+  if ((terms & MCQ_TERM_THERM) && c->temperature > 0 && !(c->th_dt > 0))
+    return fail(c, MCQ_ESTATE, "thermal field before any mcq_run (its scale needs the run's dt)");
   for (auto& s : c->sl) {
     if (!s.field) {
       CK(c, cudaMalloc(&s.field, 3ULL * s.d.cs * 4));
@@ -1254,7 +1291,7 @@ int mcq_get_field(mcq_ctx* c, float* b_out, unsigned terms) {
   const CavParams p = cav_params(c, 1e-12);
   launch_cav_prepare(p, c->cav, c->stream);
   Enq q{c, c->stream};
-  q.eval(MODE_FIELD, terms & MCQ_TERM_ALL);
+  q.eval(MODE_FIELD, terms & (MCQ_TERM_ALL | MCQ_TERM_THERM));
   if (q.rc != MCQ_OK) return q.rc;
   c->launches += q.count + 1;
   slabs_to_io(c, true);

@@ -59,7 +59,7 @@ __device__ __forceinline__ float3 cross3(float3 a, float3 b) {
 __device__ __forceinline__ float dot3(float3 a, float3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
 __device__ __forceinline__ float3 nrm3(float3 v) {
   const float n2 = dot3(v, v);
-  if (n2 > 0.f) {
+  if (!(n2 <= 0.f)) {  // NaN propagates (vacuum stays 0): the divergence guard sees it
     const float r = rsqrtf(n2);
     return make_float3(v.x * r, v.y * r, v.z * r);
   }
@@ -84,6 +84,26 @@ struct RowAddr {  // shared-memory address of element pos of component-line l of
 // the demag field.  Computes B' and, by mode, the field (Bout),
 // the max torque, or the RK4 stage update (returns m_{s+1}, writes the new accumulator to
 // acc_out).  All memory traffic (and the overlap sums) stays in the caller.
+// Thermal noise (reading C-TH): the c-th output of SplitMix64 started at state `seed`, and the
+// standard normal 3-vector of a cell from the two words at counters c0, c0 + 1 (Box-Muller on
+// u1 = (h >> 40 + 1) 2^-24 in (0, 1], u2 = (h & 0xFFFFFF) 2^-24; eta = (cos0, sin0, cos1)).
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long seed, unsigned long long c) {
+  unsigned long long z = seed + (c + 1ull) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ float3 thermal_eta(unsigned long long seed, unsigned long long c0) {
+  const unsigned long long h0 = splitmix64(seed, c0), h1 = splitmix64(seed, c0 + 1ull);
+  float s0, k0, s1, k1;
+  const float r0 = sqrtf(-2.f * logf(((float)(h0 >> 40) + 1.f) * 0x1p-24f));
+  const float r1 = sqrtf(-2.f * logf(((float)(h1 >> 40) + 1.f) * 0x1p-24f));
+  sincospif(2.f * ((float)(h0 & 0xFFFFFFull) * 0x1p-24f), &s0, &k0);
+  sincospif(2.f * ((float)(h1 & 0xFFFFFFull) * 0x1p-24f), &s1, &k1);
+  return make_float3(r0 * k0, r0 * s0, r1 * k1);
+}
+
 template <bool GEN>
 __device__ __forceinline__ float3 cell_core(const UpdateArgs& a, float3 m, const float3 (&nb)[6], const bool (&ok)[6],
                                             float3 mn, float3 ap, float3 bcav, float gmul, float3 Bd,
@@ -351,6 +371,9 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
     any_cav = any_cav || gs[k] != 0.f;
   }
   const float gsum = gs[0];
+  // thermal draw of this step: counters 2 (n N + g) (+1), N the global cell count (C-TH)
+  const unsigned long long th_base =
+      (GEN && a.th != 0.f) ? 2ull * (unsigned long long)a.cav->step * ((unsigned long long)nx * ny * d.nzg) : 0ull;
   double wacc[MM];
 #pragma unroll
   for (int k = 0; k < MM; ++k) wacc[k] = 0.0;
@@ -436,7 +459,14 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
         const float3 mn = make_float3(MCQ_PICK(mn2[0]), MCQ_PICK(mn2[1]), MCQ_PICK(mn2[2]));
         const float3 ap = make_float3(MCQ_PICK(ap2[0]), MCQ_PICK(ap2[1]), MCQ_PICK(ap2[2]));
         const float3 br = make_float3(MCQ_PICK(br2[0]), MCQ_PICK(br2[1]), MCQ_PICK(br2[2]));
-        const float3 Bd = make_float3(MCQ_PICK(v[0][i]), MCQ_PICK(v[1][i]), MCQ_PICK(v[2][i]));
+        float3 Bd = make_float3(MCQ_PICK(v[0][i]), MCQ_PICK(v[1][i]), MCQ_PICK(v[2][i]));
+        if (GEN && a.th != 0.f) {
+          const unsigned long long g = ((unsigned long long)(d.zg0 + z) * ny + y) * nx + x;
+          const float3 eta = thermal_eta(a.th_seed, th_base + 2ull * g);
+          Bd.x += a.th * eta.x;
+          Bd.y += a.th * eta.y;
+          Bd.z += a.th * eta.z;
+        }
         float3 accn = make_float3(0.f, 0.f, 0.f), Bf = make_float3(0.f, 0.f, 0.f);
         float3 out;
         if constexpr (MM == 1) {
@@ -533,6 +563,9 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
         for (int w = 0; w < nw; ++w) s += red[w * kNPart + threadIdx.x];
       const int nps = gridDim.x * gridDim.y;
       a.partials[threadIdx.x * nps + blockIdx.y * gridDim.x + blockIdx.x] = s;
+      // divergence guard at no per-cell cost: br . m_{n+1} is NaN for any non-finite m_{n+1}
+      // (0 * inf and 0 * NaN are NaN), so a non-finite W_0 partial flags the step
+      if (threadIdx.x == 0 && a.nonfinite && !isfinite(s)) atomicOr(a.nonfinite, 1);
     }
   }
   if (dp && a.stage == 7) {  // the step's error estimate: max over cells (fp32 bits, >= 0)
@@ -619,7 +652,7 @@ void launch_update(const UpdateArgs& a, const float2* tw, cudaStream_t st) {
   MCQ_DISPATCH_N2(a.d.N2, {
     using Cf = UCfg<N2>;
     dim3 grid((a.d.ny + Cf::RY - 1) / Cf::RY, a.d.nz);
-    if (a.mode == MODE_DP || a.dmi[0] != 0.f || a.dmi[1] != 0.f)
+    if (a.mode == MODE_DP || a.dmi[0] != 0.f || a.dmi[1] != 0.f || a.th != 0.f)
       launch_pdl(a.d.pdl, k_update<N2, kMaxModes, true>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
     else if (a.nmodes > 1)
       launch_pdl(a.d.pdl, k_update<N2, kMaxModes, false>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);

@@ -355,3 +355,29 @@ def test_dmi_field_and_steps_parity(kind, grid, D):
     assert rel_l2(s2.m()[mag], ref2.m.reshape(-1, 3)[mag]) < 1e-4
     s.close()
     s2.close()
+
+
+def test_divergence_is_detected_and_cleared_by_set_m():
+    """Failure detection (include/mcq.h, mcq_synchronize): an absurd time step overflows the
+    stage slopes, the step's m_{n+1} turns non-finite, and mcq_synchronize reports ESTATE
+    "diverged" until a fresh state is installed (m and, since alpha diverged with it, the cavity
+    memory); a sane run on the same context is then clean."""
+    cfg = small_config("sphere", (16, 12, 8), seed=3, state="phys")
+    s = mcq.Solver.from_config(cfg)
+    s.run(cfg.dt, 5)
+    mcq.mcq_synchronize(s.ctx)                       # healthy: no error
+    s.run(1e30, 3)
+    with pytest.raises(mcq.MCQError) as e:
+        mcq.mcq_synchronize(s.ctx)
+    assert e.value.code == -2 and "diverged" in str(e.value)
+    assert not np.all(np.isfinite(s.m()))
+    s.set_m(cfg.m0)                                  # clears the flag ...
+    s.run(cfg.dt, 1)
+    with pytest.raises(mcq.MCQError):                # ... but the cavity memory diverged too
+        mcq.mcq_synchronize(s.ctx)
+    s.set_m(cfg.m0)
+    mcq.mcq_reset_memory(s.ctx)                      # a fresh state: m and alpha
+    s.run(cfg.dt, 5)
+    mcq.mcq_synchronize(s.ctx)
+    assert np.all(np.isfinite(s.m()))
+    s.close()
