@@ -194,6 +194,11 @@ def main():
                     help="N == 1: run the decomposed schedule with this many z slabs on the one GPU")
     ap.add_argument("--batch", type=int, default=1,
                     help="independent replicas per GPU (one bias point each, own stream; latency-bound grids)")
+    ap.add_argument("--integrator", default="rk4", choices=["rk4", "dp"],
+                    help="dp: fixed-step Dormand-Prince 5(4) steps (7 RHS each, NEXT-1)")
+    ap.add_argument("--modes", type=int, default=1, help="cavity modes (NEXT-2; extra modes: dark map)")
+    ap.add_argument("--temperature", type=float, default=0.0, help="thermal field, K (NEXT-4)")
+    ap.add_argument("--dmi", type=float, default=0.0, help="interfacial DMI constant, J/m^2 (NEXT-4)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -228,7 +233,19 @@ def main():
         dd = slab_dist(rank, world, local) if slab else None
         if world == 1 and args.loopback > 1:
             dd = {"rank": -1, "world": args.loopback}
-        sv = mcq.Solver.from_config(cfg, stream=s_j.cuda_stream, dist=dd)
+        sv = mcq.Solver.from_config(cfg, stream=s_j.cuda_stream, dist=dd, set_state=args.modes <= 1)
+        if args.modes > 1:  # extra modes k >= 1: the dark two-wire map, f_c shifted by 0.3 GHz per mode
+            from synth.configs import two_wire_map
+            dark, _, _ = two_wire_map(cfg.grid, cfg.cell, cfg.Ms, cfg.mask, 1e9, "dark")
+            mcq.mcq_set_modes(sv.ctx, args.modes)
+            for k in range(1, args.modes):
+                mcq.mcq_set_brms_mode(sv.ctx, k, dark)
+                mcq.mcq_set_cavity_mode(sv.ctx, k, cfg.f_c + 0.3e9 * k, cfg.kappa)
+            sv.set_m(cfg.m0)
+        if args.temperature > 0:
+            mcq.mcq_set_temperature(sv.ctx, args.temperature, 1234 + j)
+        if args.dmi != 0:
+            mcq.mcq_set_dmi(sv.ctx, args.dmi)
         if cfg.relax_first:
             sv.relax(cfg.dt * 0.5, 1e-3, 2000)
             mcq.mcq_reset_memory(sv.ctx)
@@ -247,12 +264,18 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    def advance(sv, steps):
+        if args.integrator == "dp":
+            mcq.mcq_run_dp(sv.ctx, cfg.dt, steps)
+        else:
+            sv.run(cfg.dt, steps)
+
     def run_all(steps):  # every replica on its own stream, fork / join through events
         fork = torch.cuda.Event()
         fork.record(stream)
         for s_j, sv in zip(streams, solvers):
             s_j.wait_event(fork)
-            sv.run(cfg.dt, steps)
+            advance(sv, steps)
         for s_j in streams[1:]:
             join = torch.cuda.Event()
             join.record(s_j)
@@ -282,7 +305,7 @@ def main():
     for sv in solvers:
         mcq.mcq_set_m(sv.ctx, m_host.numpy())
     for sv in solvers:
-        sv.run(cfg.dt, e2e_steps)
+        advance(sv, e2e_steps)
     for sv in solvers:
         mcq.mcq_get_m(sv.ctx, cfg.n, out_host.numpy().reshape(-1))
     torch.cuda.synchronize()
@@ -314,11 +337,15 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if slab else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg.name, "grid": list(cfg.grid), "cells": cfg.n,
-                       "magnetic_cells": cfg.n_magnetic(), "dt_s": cfg.dt, "integrator": "RK4 (4 RHS/step)",
+                       "magnetic_cells": cfg.n_magnetic(), "dt_s": cfg.dt,
+                       "integrator": "RK4 (4 RHS/step)" if args.integrator == "rk4" else
+                       "Dormand-Prince 5(4), fixed dt (7 RHS/step; roofline/kernels from an RK4 profile)",
                        "parallelism": (f"z-slab x{world} (NCCL)" if slab else f"replicas x{world}")
                        if world > 1 else (f"single GPU, loopback z-slab x{args.loopback}"
                                           if args.loopback > 1 else "single GPU"),
                        "replicas_per_gpu": R,
+                       **({"variant": {"modes": args.modes, "temperature_K": args.temperature, "dmi": args.dmi}}
+                          if (args.modes > 1 or args.temperature > 0 or args.dmi != 0) else {}),
                        "l2": l2_note,
                        "padded_fft": [L["Lx"], L["Ly"], L["Lz"]]},
             "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": pk["hbm_gbs"],
@@ -333,7 +360,7 @@ def main():
             "kernels": {k: {"ms": v[0], "per_step": v[1], "share": share.get(k, 0.0) / max(1e-12, sum(share.values())),
                             "alg_gbs": (ab[k] / (v[0] * 1e-3) / 1e9) if v[0] > 0 else None}
                         for k, v in prof.items() if v[1] > 0},
-            "rhs_evals_per_s": 4 * value,
+            "rhs_evals_per_s": (4 if args.integrator == "rk4" else 7) * value,
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "e2e": {"value": e2e_val, "unit": "cell-updates/s", "h2d_bytes_per_step": 12 * cfg.n * jobs / e2e_steps,

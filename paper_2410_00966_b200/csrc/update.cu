@@ -225,7 +225,7 @@ __device__ __forceinline__ float2 sm_pair(const float* p) { return *reinterpret_
 #ifndef MCQ_UMINB
 #define MCQ_UMINB 5  // min resident CTAs per SM requested from ptxas (96-register cap: 84.8 vs 86.8 us on configs[1])
 #endif
-// MM: cavity modes compiled in (1, or kMaxModes with a.nmodes <= MM at run time); GEN: the
+// MM: cavity modes compiled in (1, 2 or kMaxModes with a.nmodes <= MM at run time); GEN: the
 // general instance (Dormand-Prince stages, interfacial DMI) — kept out of the plain RK4 ones
 template <int N2, int MM, bool GEN>
 __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a, const float2* __restrict__ gtw) {
@@ -652,10 +652,15 @@ void launch_update(const UpdateArgs& a, const float2* tw, cudaStream_t st) {
   MCQ_DISPATCH_N2(a.d.N2, {
     using Cf = UCfg<N2>;
     dim3 grid((a.d.ny + Cf::RY - 1) / Cf::RY, a.d.nz);
-    if (a.mode == MODE_DP || a.dmi[0] != 0.f || a.dmi[1] != 0.f || a.th != 0.f)
+    const bool gen = a.mode == MODE_DP || a.dmi[0] != 0.f || a.dmi[1] != 0.f || a.th != 0.f;
+    if (gen && a.nmodes > 1)
       launch_pdl(a.d.pdl, k_update<N2, kMaxModes, true>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
-    else if (a.nmodes > 1)
+    else if (gen)  // one mode: no per-mode registers (the 4-mode general instance spills)
+      launch_pdl(a.d.pdl, k_update<N2, 1, true>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
+    else if (a.nmodes > 2)
       launch_pdl(a.d.pdl, k_update<N2, kMaxModes, false>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
+    else if (a.nmodes == 2)  // two modes (bright + dark): half the per-mode registers of MM = 4
+      launch_pdl(a.d.pdl, k_update<N2, 2, false>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
     else
       launch_pdl(a.d.pdl, k_update<N2, 1, false>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
   })
@@ -669,6 +674,8 @@ void configure_update_kernels() {
                            (int)UCfg<N2>::SMEM);
       cudaFuncSetAttribute(k_update<N2, kMaxModes, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)UCfg<N2>::SMEM);
+      cudaFuncSetAttribute(k_update<N2, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UCfg<N2>::SMEM);
+      cudaFuncSetAttribute(k_update<N2, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UCfg<N2>::SMEM);
     })
   }
 }
