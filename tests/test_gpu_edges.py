@@ -1,0 +1,54 @@
+"""Edge cases of the grid (include/mcq.h mcq_create: 2 <= nx, ny <= 512, 1 <= nz <= 512) against
+the oracle: the smallest mesh, odd sizes, each axis at its maximum with the others minimal (the
+largest row FFTs: Lx, Ly or Lz = 1024), and a single magnetic cell in vacuum.  Field terms
+within 1e-5 and 20 steps within 1e-4, as in test_gpu_parity.py."""
+import numpy as np
+import pytest
+
+from helpers import oracle_from, magmask, rel_l2, TERMS
+from synth import small_config
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2410_00966_b200 as mcq  # noqa: E402
+
+GRIDS = [(2, 2, 1), (3, 5, 2), (2, 3, 7), (512, 2, 1), (2, 512, 1), (2, 2, 512), (511, 3, 2)]
+
+
+def _check(cfg, steps=20):
+    s = mcq.Solver.from_config(cfg)
+    ref = oracle_from(cfg)
+    ref.m = s.m().astype(np.float64).reshape(ref.m.shape)
+    mag = magmask(cfg)
+    for name, bit in list(TERMS.items()) + [("total", 63)]:
+        b = s.field(bit)[mag]
+        r = ref.field(ref.m, 0.0, bit).reshape(-1, 3)[mag]
+        if np.all(r == 0):
+            assert np.all(b == 0), name
+            continue
+        assert rel_l2(b, r) < 1e-5, (name, rel_l2(b, r))
+    s.run(cfg.dt, steps)
+    ref.run(cfg.dt, steps)
+    assert rel_l2(s.m()[mag], ref.m.reshape(-1, 3)[mag]) < 1e-4
+    a = ref.mem.alpha()
+    cav = s.cavity()
+    assert abs(complex(cav["re_alpha"], cav["im_alpha"]) - a) <= 1e-4 * max(abs(a), 1e-12)
+    s.close()
+
+
+@pytest.mark.parametrize("grid", GRIDS)
+def test_extreme_grids(grid):
+    _check(small_config("film", grid, seed=5, state="phys"))
+
+
+def test_single_magnetic_cell_in_vacuum():
+    cfg = small_config("film", (8, 6, 3), seed=6, state="phys")
+    mask = np.zeros(cfg.n, np.uint8)
+    mask[(1 * 6 + 2) * 8 + 5] = 1                     # cell (x=5, y=2, z=1)
+    cfg.mask = mask
+    cfg.m0 = (cfg.m0 * mask[:, None]).astype(np.float32)
+    _check(cfg)
