@@ -421,15 +421,27 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
                          : make_float2(a.brms_u[0][c], a.brms_u[0][c]);
       }
       if (dp) {  // ap = sum_{j < s} comb[j-1] k_j (the earlier stages' slopes, from HBM)
+        // two slopes per iteration: their loads are in flight together (same summation order)
 #pragma unroll 1
-        for (int j = 1; j < a.stage; ++j) {
-          const float w = a.comb[j - 1];
-          const float* Kj = a.K + (size_t)(j - 1) * 3 * Nu;
+        for (int j = 1; j < a.stage; j += 2) {
+          float2 kk[2][3];
 #pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const float2 kk = ld_pair(Kj, c * Nu + idx, vec, two);
-            ap2[c].x += w * kk.x;
-            ap2[c].y += w * kk.y;
+          for (int q = 0; q < 2; ++q) {
+            const float* Kj = a.K + (size_t)(j + q - 1) * 3 * Nu;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              kk[q][c] = j + q < a.stage ? ld_pair(Kj, c * Nu + idx, vec, two) : make_float2(0.f, 0.f);
+          }
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            if (j + q < a.stage) {
+              const float w = a.comb[j + q - 1];
+#pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                ap2[c].x += w * kk[q][c].x;
+                ap2[c].y += w * kk[q][c].y;
+              }
+            }
           }
         }
       }
