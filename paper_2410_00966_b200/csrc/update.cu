@@ -104,7 +104,7 @@ __device__ __forceinline__ float3 thermal_eta(unsigned long long seed, unsigned 
   return make_float3(r0 * k0, r0 * s0, r1 * k1);
 }
 
-template <bool GEN>
+template <int GEN>
 __device__ __forceinline__ float3 cell_core(const UpdateArgs& a, float3 m, const float3 (&nb)[6], const bool (&ok)[6],
                                             float3 mn, float3 ap, float3 bcav, float gmul, float3 Bd,
                                             float& tmax, float3& acc_out, float3& Bout) {
@@ -177,7 +177,7 @@ __device__ __forceinline__ float3 cell_core(const UpdateArgs& a, float3 m, const
   }
   const float3 mmxB = cross3(m, mxB);
   float3 k;
-  if (a.mode == MODE_LLG || (GEN && a.mode == MODE_DP)) {
+  if (a.mode == MODE_LLG || (GEN == 2 && a.mode == MODE_DP)) {
     k = make_float3(-a.gl * (mxB.x + a.alpha * mmxB.x), -a.gl * (mxB.y + a.alpha * mmxB.y),
                     -a.gl * (mxB.z + a.alpha * mmxB.z));
   } else {  // MODE_RELAX: -gamma m x (m x B)
@@ -185,7 +185,7 @@ __device__ __forceinline__ float3 cell_core(const UpdateArgs& a, float3 m, const
   }
   const int stage = a.stage;
   if (stage == 1) mn = m;
-  if (GEN && a.mode == MODE_DP) {  // ap = sum_{j < s} comb[j-1] k_j from the caller (reading C-DP)
+  if (GEN == 2 && a.mode == MODE_DP) {  // ap = sum_{j < s} comb[j-1] k_j from the caller (reading C-DP)
     const float cs = a.comb[stage - 1];
     const float3 inc = make_float3(ap.x + cs * k.x, ap.y + cs * k.y, ap.z + cs * k.z);
     acc_out = k;
@@ -225,9 +225,9 @@ __device__ __forceinline__ float2 sm_pair(const float* p) { return *reinterpret_
 #ifndef MCQ_UMINB
 #define MCQ_UMINB 5  // min resident CTAs per SM requested from ptxas (96-register cap: 84.8 vs 86.8 us on configs[1])
 #endif
-// MM: cavity modes compiled in (1, 2 or kMaxModes with a.nmodes <= MM at run time); GEN: the
-// general instance (Dormand-Prince stages, interfacial DMI) — kept out of the plain RK4 ones
-template <int N2, int MM, bool GEN>
+// MM: cavity modes compiled in (1, 2 or kMaxModes with a.nmodes <= MM at run time); GEN: 0 the
+// plain RK4 instances, 1 + interfacial DMI and the thermal draw, 2 + the Dormand-Prince stages
+template <int N2, int MM, int GEN>
 __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a, const float2* __restrict__ gtw) {
   using Cf = UCfg<N2>;
   constexpr int E = Cf::E, TL = Cf::TL, RY = Cf::RY, NT = Cf::NT, LX = 2 * N2, PITCH = Cf::PITCH;
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
   double wacc[MM];
 #pragma unroll
   for (int k = 0; k < MM; ++k) wacc[k] = 0.0;
-  const bool dp = GEN && a.mode == MODE_DP;
+  const bool dp = GEN == 2 && a.mode == MODE_DP;
   // overlaps (and the trace's sum m) of the step result: RK4 stage 4's output, DP stage 7's input
   const bool wsum = (a.mode == MODE_LLG && a.stage == 4) || (dp && a.stage == 7);
   float tmax = 0.f;
@@ -664,30 +664,34 @@ void launch_update(const UpdateArgs& a, const float2* tw, cudaStream_t st) {
   MCQ_DISPATCH_N2(a.d.N2, {
     using Cf = UCfg<N2>;
     dim3 grid((a.d.ny + Cf::RY - 1) / Cf::RY, a.d.nz);
-    const bool gen = a.mode == MODE_DP || a.dmi[0] != 0.f || a.dmi[1] != 0.f || a.th != 0.f;
-    if (gen && a.nmodes > 1)
-      launch_pdl(a.d.pdl, k_update<N2, kMaxModes, true>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
-    else if (gen)  // one mode: no per-mode registers (the 4-mode general instance spills)
-      launch_pdl(a.d.pdl, k_update<N2, 1, true>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
+    const bool xf = a.dmi[0] != 0.f || a.dmi[1] != 0.f || a.th != 0.f;  // extra field terms
+    if (a.mode == MODE_DP && a.nmodes > 1)
+      launch_pdl(a.d.pdl, k_update<N2, kMaxModes, 2>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
+    else if (a.mode == MODE_DP)  // one mode: no per-mode registers (the 4-mode general instance spills)
+      launch_pdl(a.d.pdl, k_update<N2, 1, 2>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
+    else if (xf && a.nmodes > 1)
+      launch_pdl(a.d.pdl, k_update<N2, kMaxModes, 2>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
+    else if (xf)  // DMI / thermal without the Dormand-Prince code
+      launch_pdl(a.d.pdl, k_update<N2, 1, 1>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
     else if (a.nmodes > 2)
-      launch_pdl(a.d.pdl, k_update<N2, kMaxModes, false>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
+      launch_pdl(a.d.pdl, k_update<N2, kMaxModes, 0>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
     else if (a.nmodes == 2)  // two modes (bright + dark): half the per-mode registers of MM = 4
-      launch_pdl(a.d.pdl, k_update<N2, 2, false>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
+      launch_pdl(a.d.pdl, k_update<N2, 2, 0>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
     else
-      launch_pdl(a.d.pdl, k_update<N2, 1, false>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
+      launch_pdl(a.d.pdl, k_update<N2, 1, 0>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
   })
 }
 
 void configure_update_kernels() {
   for (int n = 2; n <= 512; n *= 2) {
     MCQ_DISPATCH_N2(n, {
-      cudaFuncSetAttribute(k_update<N2, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UCfg<N2>::SMEM);
-      cudaFuncSetAttribute(k_update<N2, kMaxModes, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)UCfg<N2>::SMEM);
-      cudaFuncSetAttribute(k_update<N2, kMaxModes, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)UCfg<N2>::SMEM);
-      cudaFuncSetAttribute(k_update<N2, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UCfg<N2>::SMEM);
-      cudaFuncSetAttribute(k_update<N2, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UCfg<N2>::SMEM);
+      const int smem = (int)UCfg<N2>::SMEM;
+      cudaFuncSetAttribute(k_update<N2, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(k_update<N2, 2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(k_update<N2, kMaxModes, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(k_update<N2, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(k_update<N2, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(k_update<N2, kMaxModes, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     })
   }
 }
