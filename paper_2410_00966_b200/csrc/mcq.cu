@@ -1241,11 +1241,11 @@ int mcq_run_adaptive(mcq_ctx* c, double duration, double dt0, double tol, long l
 
 int mcq_synchronize(mcq_ctx* c) {
   if (!c) return MCQ_EINVAL;
+  int nf = 0;  // stream-ordered read (no legacy-stream sync with the caller's other work)
+  CK(c, cudaMemcpyAsync(&nf, c->nonfinite, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
   CK(c, cudaGetLastError());
-  int nf = 0;
-  CK(c, cudaMemcpy(&nf, c->nonfinite, 4, cudaMemcpyDeviceToHost));
-  if (nf) return fail(c, MCQ_ESTATE, "the integration diverged: a non-finite magnetisation was produced (time step too large?); set a new state with mcq_set_m");
+  if (nf) return fail(c, MCQ_ESTATE, "the integration diverged: a non-finite magnetisation was produced (time step too large?); install a fresh state (mcq_set_m, mcq_reset_memory)");
   return MCQ_OK;
 }
 
