@@ -174,17 +174,17 @@ int mcq_ovf_write(const char* path, const int grid[3], const double cell[3], con
   std::string h;
   char tmp[256];
   auto line = [&](const char* fmt, auto... args) {
-    std::snprintf(tmp, sizeof(tmp), fmt, args...);
-    h += tmp;
+    if constexpr (sizeof...(args) == 0) {
+      h += fmt;
+    } else {
+      std::snprintf(tmp, sizeof(tmp), fmt, args...);
+      h += tmp;
+    }
     h += '\n';
   };
-  h += "# OOMMF OVF 2.0\n# Segment count: 1\n# Begin: Segment\n# Begin: Header\n";
-  line("# Title: mcq");
-  line("# meshtype: rectangular");
-  line("# meshunit: m");
-  line("# xmin: 0");
-  line("# ymin: 0");
-  line("# zmin: 0");
+  h += "# OOMMF OVF 2.0\n# Segment count: 1\n# Begin: Segment\n# Begin: Header\n"
+       "# Title: mcq\n# meshtype: rectangular\n# meshunit: m\n"
+       "# xmin: 0\n# ymin: 0\n# zmin: 0\n";
   line("# xmax: %.17g", grid[0] * cell[0]);
   line("# ymax: %.17g", grid[1] * cell[1]);
   line("# zmax: %.17g", grid[2] * cell[2]);
