@@ -156,7 +156,9 @@ MCQ_API int mcq_set_dmi(mcq_ctx *, double D);
 /* Temperature T (K, >= 0; 0 = off) and the seed of the thermal stream (P:188 lists the thermal
  * field among the Mumax3 terms).  Reading C-TH (Mumax3's Brown field):
  * B_th = eta sqrt(2 alpha k_B T / (gamma M_s V_cell dt)) in magnetic cells, eta a standard normal
- * 3-vector per cell drawn once per mcq_run step and held for its four RK4 stages.  eta is
+ * 3-vector per cell drawn once per mcq_run step and held for its four RK4 stages (stage 1
+ * draws it and stores it in a 12-byte-per-cell device buffer the context allocates on the
+ * first mcq_run with T > 0, ENOMEM if that fails; stages 2-4 reload it).  eta is
  * counter-based and reproducible: SplitMix64 started at state `seed`, counters
  * 2 (n N + g) and 2 (n N + g) + 1 for global cell g = (z ny + y) nx + x at step n (the cavity
  * state's step count), N cells; Box-Muller on u1 = (h >> 40 + 1) 2^-24, u2 = (h & 0xFFFFFF)

@@ -170,6 +170,7 @@ struct UpdateArgs {
   // once per step (counter = the cavity state's step count) and held for all its stages
   float th;
   unsigned long long th_seed;
+  float* eta;         // MODE_LLG: the step's draw [3][cs], written by stage 1, read by 2-4 (or nullptr)
   int demag;          // run the x-C2R demag phase
   int trace;          // stage 4: also accumulate sum m for the trace
   // MODE_DP (Dormand-Prince, reading C-DP), stage s = 1..7 with h = dt: K[j] = k_{j+1} ([3][cs]

@@ -85,6 +85,7 @@ struct Slab {
   float2 *X = nullptr, *Y = nullptr, *R = nullptr;  // X [3][nz][ny][P]; Y, R [NS][3][nz][Ly][KXS]
   float* K = nullptr;  // Dormand-Prince slopes k_1..k_6, [6][3][cs] (allocated on first use)
   float* brms[kMaxModes] = {nullptr, nullptr, nullptr, nullptr};  // [3][cs] per mode (maps)
+  float* eta = nullptr;    // thermal draw of the current step, [3][cs] (allocated while T > 0)
   float* field = nullptr;                           // [3][cs]
   uint8_t* mask = nullptr;                          // [nz][ny][nx]
   double* partials = nullptr;                       // into ctx partials (loopback) or own (NCCL)
@@ -420,6 +421,7 @@ struct Enq {
       if (mode == MODE_LLG && c->temperature > 0) {  // one draw per step, held for its stages
         a.th = (float)th_sigma(c, dt);
         a.th_seed = c->th_seed;
+        a.eta = sl.eta;
       }
       update(a);
     }
@@ -650,7 +652,7 @@ void free_all(mcq_ctx* c) {
   invalidate_graphs(c);
   for (auto& s : c->sl) {
     void* ptrs[] = {s.mN, s.mA, s.mB, s.acc, s.X, s.Y, s.R, s.K, s.brms[0], s.brms[1], s.brms[2], s.brms[3],
-                    s.field, s.mask};
+                    s.field, s.mask, s.eta};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (c->mode == 2 && s.partials) cudaFree(s.partials);
@@ -1117,6 +1119,9 @@ int mcq_run(mcq_ctx* c, double dt, long long steps) {
   if (!c->m_set) return fail(c, MCQ_ESTATE, "mcq_run before mcq_set_m");
   if (steps == 0) return MCQ_OK;
   c->th_dt = dt;
+  if (c->temperature > 0)
+    for (auto& s : c->sl)
+      if (!s.eta) CK(c, cudaMalloc(&s.eta, 3ULL * s.d.cs * sizeof(float)));
   const CavParams p = cav_params(c, dt);
   launch_cav_prepare(p, c->cav, c->stream);
   c->launches += 1;

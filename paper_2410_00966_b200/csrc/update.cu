@@ -389,6 +389,8 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
   const bool st = a.mode == MODE_LLG || a.mode == MODE_RELAX || (dp && a.stage < 7);  // writes a state
   const bool need_mn = st && a.stage > 1, need_acc = !dp && st && a.stage > 1;
   const bool need_br = a.brms[0] && (gsum != 0.f || wsum);
+  const bool th_st = GEN && a.eta && a.mode == MODE_LLG && a.stage == 1;  // thermal draw stored
+  const bool th_ld = GEN && a.eta && a.mode == MODE_LLG && a.stage > 1;   // and reloaded
 #pragma unroll
   for (int i = 0; i < E; ++i) {
     const int x0 = 2 * (t + TL * i);
@@ -445,6 +447,26 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
           }
         }
       }
+      // the step's thermal draw: drawn by stage 1 and stored, reloaded by stages 2-4 (the
+      // same values a redraw would give, at 12 bytes per cell instead of the generator's cost)
+      float2 th2[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      if (GEN && a.th != 0.f) {
+        if (th_ld) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) th2[c] = ld_pair(a.eta, c * Nu + idx, vec, two);
+        } else {
+          const unsigned long long g0 = ((unsigned long long)(d.zg0 + z) * ny + y) * nx + x0;
+          const float3 e0 = thermal_eta(a.th_seed, th_base + 2ull * g0);
+          const float3 e1 = two ? thermal_eta(a.th_seed, th_base + 2ull * (g0 + 1ull)) : e0;
+          th2[0] = make_float2(e0.x, e1.x);
+          th2[1] = make_float2(e0.y, e1.y);
+          th2[2] = make_float2(e0.z, e1.z);
+          if (th_st) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) st_pair(a.eta, c * Nu + idx, th2[c], vec, two);
+          }
+        }
+      }
       float2 bk2[MM > 1 ? MM - 1 : 1][3];  // extra modes' B_rms (maps or uniform values)
 #pragma unroll
       for (int k = 1; k < MM; ++k)
@@ -473,11 +495,9 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
         const float3 br = make_float3(MCQ_PICK(br2[0]), MCQ_PICK(br2[1]), MCQ_PICK(br2[2]));
         float3 Bd = make_float3(MCQ_PICK(v[0][i]), MCQ_PICK(v[1][i]), MCQ_PICK(v[2][i]));
         if (GEN && a.th != 0.f) {
-          const unsigned long long g = ((unsigned long long)(d.zg0 + z) * ny + y) * nx + x;
-          const float3 eta = thermal_eta(a.th_seed, th_base + 2ull * g);
-          Bd.x += a.th * eta.x;
-          Bd.y += a.th * eta.y;
-          Bd.z += a.th * eta.z;
+          Bd.x += a.th * MCQ_PICK(th2[0]);
+          Bd.y += a.th * MCQ_PICK(th2[1]);
+          Bd.z += a.th * MCQ_PICK(th2[2]);
         }
         float3 accn = make_float3(0.f, 0.f, 0.f), Bf = make_float3(0.f, 0.f, 0.f);
         float3 out;
