@@ -1,6 +1,7 @@
-mkdir -p gpurun_out/v2
-timeout 1200 python -m pytest tests/ -q -m gpu > gpurun_out/v2/tests.log 2>&1; echo "pytest exit $?" >> gpurun_out/v2/tests.log
-B="timeout 300 python bench.py --steps 200 --warmup 5 --no-cpu-baseline"
-$B --temperature 300 > gpurun_out/v2/c1_t300.json 2> gpurun_out/v2/c1_t300.err
-$B > gpurun_out/v2/c1.json 2> gpurun_out/v2/c1.err
-tail -n 3 gpurun_out/v2/tests.log; for f in gpurun_out/v2/*.json; do echo $f; cut -c1-200 $f; done
+mkdir -p gpurun_out/v4
+B="timeout 200 python bench.py --steps 400 --warmup 5 --no-cpu-baseline"
+$B > gpurun_out/v4/base.json 2>&1
+for v in pdl1 uminb4 zse8; do MCQ_LIB_PATH=$PWD/variants/$v.so $B > gpurun_out/v4/$v.json 2>&1; done
+MCQ_ZVARIANT=tma $B > gpurun_out/v4/ztma.json 2>&1
+$B > gpurun_out/v4/base2.json 2>&1
+for f in gpurun_out/v4/*.json; do echo $f $(grep -o '"ms_per_step": [0-9.]*' $f); done
