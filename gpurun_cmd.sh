@@ -1,4 +1,3 @@
-mkdir -p gpurun_out/v5
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/v5/smoke.log 2>&1
-timeout 600 python bench.py > gpurun_out/v5/bench.json 2> gpurun_out/v5/bench.err
-tail -n 2 gpurun_out/v5/smoke.log; cut -c1-220 gpurun_out/v5/bench.json
+mkdir -p gpurun_out/v6
+timeout 600 python -m pytest tests/test_gpu_thermal.py -q -m gpu > gpurun_out/v6/tests.log 2>&1; echo "pytest exit $?" >> gpurun_out/v6/tests.log
+tail -n 15 gpurun_out/v6/tests.log

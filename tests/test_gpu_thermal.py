@@ -115,3 +115,21 @@ def test_langevin_equilibrium_on_gpu():
     langevin = 1.0 / math.tanh(x) - 1.0 / x
     assert abs(np.mean(acc) - langevin) < 0.02, (np.mean(acc), langevin)
     s.close()
+
+
+def test_stored_draw_follows_temperature_and_dt_changes():
+    """Stage 1 stores the step's draw and stages 2-4 reload it (12 B per cell): the stored draw
+    must always be the current step's, across changes of T, seed and dt between runs and after
+    a run with the thermal term off."""
+    cfg = small_config("sphere", (16, 12, 8), seed=23, state="phys")
+    s, ref = _pair(cfg)
+    mag = magmask(cfg)
+    plan = [(T_K, SEED, cfg.dt, 3), (100.0, SEED + 7, 0.5 * cfg.dt, 4), (0.0, SEED, cfg.dt, 2),
+            (T_K, SEED, cfg.dt, 3)]
+    for T, seed, dt, n in plan:
+        mcq.mcq_set_temperature(s.ctx, T, seed)
+        ref.temperature, ref.seed = T, seed
+        s.run(dt, n)
+        ref.run(dt, n)
+        assert rel_l2(s.m()[mag], ref.m.reshape(-1, 3)[mag]) < 1e-4
+    s.close()
