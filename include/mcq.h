@@ -103,15 +103,21 @@ typedef struct {
 MCQ_API int mcq_nccl_get_unique_id(unsigned char out[128]);
 
 /* Cavity state at t_n (all ranks identical).  S, C are the paper's accumulators,
- * reconstructed from alpha: S - i C = (hbar/V_c)(alpha_0 - e^{(kappa + i w_c) t} alpha). */
+ * reconstructed from alpha: S - i C = (hbar/V_c)(alpha_0 - e^{(kappa + i w_c) t} alpha); the
+ * rescaled pair e^{-kappa t}(S - i C) = (hbar/V_c)(e^{-kappa t} alpha_0 - e^{i w_c t} alpha) is
+ * reported as well (S_resc, C_resc), finite where S, C overflow (long ring-downs, SPEC's
+ * conditioning decision). */
 typedef struct {
   double t;                  /* cavity clock since the last reset (s)                   */
   double re_alpha, im_alpha; /* alpha(t_n) = <a>                             */
   double gamma;              /* Gamma(t_n) = 2 Re alpha = x(t_n) (eq:gammadiscretefinal) */
   double W;                  /* overlap of the last completed step, A/m * T      */
-  double S, C;               /* literal accumulators (overflow beyond kappa t ~ 700)     */
+  double S, C;               /* literal accumulators; they grow as e^{kappa t} and are   */
+                             /* +-inf once kappa t exceeds ~709 (fp64 range)             */
   double n_photon;           /* |alpha|^2                                        */
   long long step;            /* completed steps since the last reset                    */
+  double S_resc, C_resc;     /* e^{-kappa t} S, e^{-kappa t} C: finite for every t,      */
+                             /* computed without the growing exponential (reading C5)    */
 } mcq_cavity_state;
 
 /* Create a context.  grid[3] = (nx, ny, nz) with 2 <= nx, ny <= 512 and 1 <= nz <= 512;
@@ -126,7 +132,10 @@ MCQ_API int mcq_create(mcq_ctx **out, const int grid[3], const double cell[3], d
 MCQ_API int mcq_set_stream(mcq_ctx *, void *stream);
 
 /* Geometry mask, N bytes, x fastest, 0 = vacuum (M_s = 0, m = 0).  NULL = full box.
- * Applies to subsequent mcq_set_m calls and zeroes m in vacuum now. */
+ * Applies to subsequent mcq_set_m calls and zeroes m in vacuum now.  If a magnetisation is
+ * installed and the new geometry makes magnetic some cells that hold no magnetisation (they
+ * were vacuum), the geometry is applied but the call returns ESTATE and mcq_run / mcq_relax /
+ * mcq_get_field refuse (ESTATE) until mcq_set_m installs a state for the new geometry. */
 MCQ_API int mcq_set_geometry(mcq_ctx *, const unsigned char *mask);
 
 /* Magnetisation, 3N floats interleaved (host).  Normalised on entry (vectors already unit to
@@ -160,13 +169,20 @@ MCQ_API int mcq_set_dmi(mcq_ctx *, double D);
  * draws it and stores it in a 12-byte-per-cell device buffer the context allocates on the
  * first mcq_run with T > 0, ENOMEM if that fails; stages 2-4 reload it).  eta is
  * counter-based and reproducible: SplitMix64 started at state `seed`, counters
- * 2 (n N + g) and 2 (n N + g) + 1 for global cell g = (z ny + y) nx + x at step n (the cavity
- * state's step count), N cells; Box-Muller on u1 = (h >> 40 + 1) 2^-24, u2 = (h & 0xFFFFFF)
+ * 2 (n N + g) and 2 (n N + g) + 1 for global cell g = (z ny + y) nx + x at noise step n, N
+ * cells.  The noise step n counts the mcq_run steps taken since the last mcq_set_temperature
+ * (or mcq_set_thermal_step): it is NOT the cavity step count and is not restarted by
+ * mcq_reset_memory, mcq_relax or the cavity setters, so segments of one run never reuse a
+ * draw.  Box-Muller on u1 = (h >> 40 + 1) 2^-24, u2 = (h & 0xFFFFFF)
  * 2^-24 gives eta = (r0 cos 2pi u2_0, r0 sin 2pi u2_0, r1 cos 2pi u2_1), r = sqrt(-2 ln u1).
  * mcq_get_field with MCQ_TERM_THERM returns the draw of the next step scaled for the last
  * mcq_run's dt (ESTATE before any run).  With T > 0, mcq_run_dp / mcq_run_adaptive return
  * ESTATE (defined for the fixed-step RK4 path only); mcq_relax ignores the thermal field. */
 MCQ_API int mcq_set_temperature(mcq_ctx *, double T, unsigned long long seed);
+/* The thermal noise step n (see mcq_set_temperature): read it (e.g. into a checkpoint) and
+ * set it (resume a noisy run bit-exactly).  EINVAL for n < 0. */
+MCQ_API int mcq_get_thermal_step(mcq_ctx *, long long *n);
+MCQ_API int mcq_set_thermal_step(mcq_ctx *, long long n);
 
 /* Excitation a * sinc(w_cut t) * B_rms, unnormalised sinc, t = cavity clock (C13). */
 MCQ_API int mcq_set_excitation(mcq_ctx *, double amplitude, double omega_cut);

@@ -52,6 +52,10 @@ class Simulation:
         self.aniso = aniso or {}
         self.dmi = float(dmi)       # interfacial DMI constant D (J/m^2), reading C-DMI
         self.temperature, self.seed = float(temperature), int(seed)   # reading C-TH
+        # noise step n of the thermal stream: RK4 steps since the temperature / seed were set;
+        # independent of the cavity memory clock (reset_memory / relax do not restart it, so
+        # the segments of one run never reuse a draw) — reading C-TH
+        self.th_step = 0
         self.th_dt = None           # dt of the last run: the thermal field's scale
         self._bth = None            # B_th of the step in progress
         self.exc_amp, self.exc_omega = float(exc_amp), float(exc_omega)
@@ -130,10 +134,15 @@ class Simulation:
             B += self.thermal(self.th_dt)
         return np.where(self.mag[..., None], B, 0.0)
 
+    def set_temperature(self, temperature, seed):
+        """mcq_set_temperature: new T and seed; the noise step restarts at 0 (reading C-TH)."""
+        self.temperature, self.seed, self.th_step = float(temperature), int(seed), 0
+
     def thermal(self, dt):
-        """B_th of step n = mem.step (steps completed), for time step dt (reading C-TH)."""
+        """B_th of noise step n = th_step (RK4 steps since set_temperature), for time step dt
+        (reading C-TH)."""
         sig = TH.sigma(self.alpha, self.temperature, self.gamma, self.Ms, self.vcell, dt)
-        return TH.thermal_field(self.shape, self.mag, self.seed, self.mem.step, sig)
+        return TH.thermal_field(self.shape, self.mag, self.seed, self.th_step, sig)
 
     def W(self, m):
         """Overlap W = sum_i M_s,i m_i . B_rms(r_i)."""
@@ -152,6 +161,7 @@ class Simulation:
             self._bth = self.thermal(dt)
         self.m = rk4_step(self.rhs, self.m, self.mem.t, dt)
         self._bth = None
+        self.th_step += 1
         W = self.W(self.m) if self.cavity_enabled else 0.0
         self.mem.update(W, dt)
         for b, mem, _, _ in self.extra:              # every mode advances on its own overlap

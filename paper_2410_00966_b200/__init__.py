@@ -126,6 +126,17 @@ def mcq_set_temperature(ctx, T, seed=0):
     _check(ctx, lib.mcq_set_temperature(ctx, float(T), int(seed) & (2**64 - 1)))
 
 
+def mcq_get_thermal_step(ctx):
+    """The thermal noise step n (counts mcq_run steps since mcq_set_temperature; reading C-TH)."""
+    n = C.c_longlong()
+    _check(ctx, lib.mcq_get_thermal_step(ctx, C.byref(n)))
+    return n.value
+
+
+def mcq_set_thermal_step(ctx, n):
+    _check(ctx, lib.mcq_set_thermal_step(ctx, int(n)))
+
+
 def mcq_reset_memory(ctx):
     _check(ctx, lib.mcq_reset_memory(ctx))
 

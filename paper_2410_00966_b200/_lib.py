@@ -34,7 +34,7 @@ class mcq_dist(C.Structure):
 class mcq_cavity_state(C.Structure):
     _fields_ = [("t", C.c_double), ("re_alpha", C.c_double), ("im_alpha", C.c_double),
                 ("gamma", C.c_double), ("W", C.c_double), ("S", C.c_double), ("C", C.c_double),
-                ("n_photon", C.c_double), ("step", C.c_longlong)]
+                ("n_photon", C.c_double), ("step", C.c_longlong), ("S_resc", C.c_double), ("C_resc", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -66,6 +66,8 @@ _sig = {
     "mcq_set_excitation": (C.c_int, [_P, C.c_double, C.c_double]),
     "mcq_set_dmi": (C.c_int, [_P, C.c_double]),
     "mcq_set_temperature": (C.c_int, [_P, C.c_double, C.c_ulonglong]),
+    "mcq_get_thermal_step": (C.c_int, [_P, C.POINTER(C.c_longlong)]),
+    "mcq_set_thermal_step": (C.c_int, [_P, C.c_longlong]),
     "mcq_reset_memory": (C.c_int, [_P]),
     "mcq_set_modes": (C.c_int, [_P, C.c_int]),
     "mcq_set_brms_mode": (C.c_int, [_P, C.c_int, _P, C.POINTER(C.c_double)]),

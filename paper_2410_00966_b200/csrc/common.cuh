@@ -132,6 +132,8 @@ struct CavParams {
   long long trace_cap;
   int trace_every;            // record after every trace_every-th step
   double inv_nmag;            // 1 / number of magnetic cells (spatial mean)
+  long long* thstep;          // thermal noise step (reading C-TH): advanced by K-CAV iff th_count
+  int th_count;               // 1 on the RK4 path (mcq_run), 0 for Dormand-Prince commits
 };
 
 enum UpdateMode : int { MODE_LLG = 0, MODE_RELAX = 1, MODE_FIELD = 2, MODE_MAXTORQUE = 3, MODE_X0 = 4, MODE_DP = 5 };
@@ -165,12 +167,13 @@ struct UpdateArgs {
   float* bout;        // MODE_FIELD output (SoA)
   unsigned* maxbits;  // MODE_MAXTORQUE output (float bits, >= 0)
   int* nonfinite;     // set to 1 by the step's last stage when some m_{n+1} is not finite
-  // thermal field (reading C-TH): B_th = th * eta(th_seed, step, global cell), th = sqrt(2 alpha
+  // thermal field (reading C-TH): B_th = th * eta(th_seed, n, global cell), th = sqrt(2 alpha
   // k_B T / (gamma M_s V dt)) for the run's dt (0: off); eta from SplitMix64 + Box-Muller, drawn
-  // once per step (counter = the cavity state's step count) and held for all its stages
+  // once per step (n = *thstep, the noise step) and held for all its stages
   float th;
   unsigned long long th_seed;
   float* eta;         // MODE_LLG: the step's draw [3][cs], written by stage 1, read by 2-4 (or nullptr)
+  const long long* thstep;  // noise step n of the draw (device word; not the cavity step count)
   int demag;          // run the x-C2R demag phase
   int trace;          // stage 4: also accumulate sum m for the trace
   // MODE_DP (Dormand-Prince, reading C-DP), stage s = 1..7 with h = dt: K[j] = k_{j+1} ([3][cs]

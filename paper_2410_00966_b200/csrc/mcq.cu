@@ -129,6 +129,7 @@ struct mcq_ctx {
   int trace_every = 1;
   long long n_magnetic = 0;
   unsigned* maxbits = nullptr;
+  long long* thstep = nullptr;  // thermal noise step n (reading C-TH), device word
   int* nonfinite = nullptr;  // divergence flag (set by the update kernel, read by mcq_synchronize)
   int* bad = nullptr;
   float* io = nullptr;  // AoS staging for the cells this context holds
@@ -216,6 +217,8 @@ CavParams cav_params(const mcq_ctx* c, double dt, bool dp = false) {
   p.trace_every = c->trace_every;
   p.inv_nmag = c->n_magnetic > 0 ? 1.0 / (double)c->n_magnetic : 0.0;
   p.pdl = c->sl.empty() ? 0 : c->sl[0].d.pdl;
+  p.thstep = c->thstep;
+  p.th_count = dp ? 0 : 1;
   return p;
 }
 
@@ -270,6 +273,7 @@ UpdateArgs base_args(const mcq_ctx* c, const Slab& s) {
   a.bout = s.field;
   a.maxbits = c->maxbits;
   a.nonfinite = c->nonfinite;
+  a.thstep = c->thstep;
   a.X = s.X;
   a.acc = s.acc;
   a.demag = 1;
@@ -658,7 +662,7 @@ void free_all(mcq_ctx* c) {
     if (c->mode == 2 && s.partials) cudaFree(s.partials);
   }
   c->sl.clear();
-  void* ptrs[] = {c->tw, c->khat, c->cav, c->partials, c->maxbits, c->bad, c->nonfinite, c->io, c->trace};
+  void* ptrs[] = {c->tw, c->khat, c->cav, c->partials, c->maxbits, c->bad, c->nonfinite, c->io, c->trace, c->thstep};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->comm) nccl_api()->commDestroy(c->comm);
@@ -849,7 +853,7 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
             cudaMalloc(&c->tw, kTwMax * 8) == cudaSuccess && cudaMalloc(&c->cav, sizeof(CavState)) == cudaSuccess &&
             cudaMalloc(&c->partials, (size_t)c->nparts * kNPart * 8) == cudaSuccess &&
             cudaMalloc(&c->maxbits, 4) == cudaSuccess && cudaMalloc(&c->bad, 4) == cudaSuccess &&
-            cudaMalloc(&c->nonfinite, 4) == cudaSuccess &&
+            cudaMalloc(&c->nonfinite, 4) == cudaSuccess && cudaMalloc(&c->thstep, 8) == cudaSuccess &&
             cudaMalloc(&c->io, 3ULL * c->cells_here() * 4) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
@@ -866,7 +870,8 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
   if (cudaMemsetAsync(c->khat, 0, 6ULL * (g.Lz / 2 + 1) * (g.Ly / 2 + 1) * g.P * 4, c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->partials, 0, (size_t)c->nparts * kNPart * 8, c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->maxbits, 0, 4, c->stream) != cudaSuccess ||
-      cudaMemsetAsync(c->nonfinite, 0, 4, c->stream) != cudaSuccess)
+      cudaMemsetAsync(c->nonfinite, 0, 4, c->stream) != cudaSuccess ||
+      cudaMemsetAsync(c->thstep, 0, 8, c->stream) != cudaSuccess)
     return bail(MCQ_ECUDA);
   // twiddles w_1024^m = exp(-2 pi i m / 1024), generated in fp64
   {
@@ -910,16 +915,45 @@ int mcq_set_stream(mcq_ctx* c, void* stream) {
 // the cells of slab i inside the global host arrays (x fastest): offset and count
 static long long slab_cell0(const mcq_ctx* c, int i) { return (long long)c->sl[i].d.zg0 * c->dg.nx * c->dg.ny; }
 
+// After a geometry change on an installed state: every magnetic cell must hold a vector.  Cells
+// the new geometry makes magnetic that were vacuum hold m = 0; aos_to_soa counts them in bad.
+// Then the state is unusable until mcq_set_m: mark it and report ESTATE.
+static int remask_state(mcq_ctx* c) {
+  CK(c, cudaMemsetAsync(c->bad, 0, 4, c->stream));
+  for (int i = 0; i < (int)c->sl.size(); ++i) {
+    Slab& s = c->sl[i];
+    const long long off = (long long)s.d.zoff * s.d.nx * s.d.ny;
+    float* io = c->io + 3 * i * s.d.N;
+    launch_soa_to_aos(s.mN, io, s.d.N, s.d.cs, off, c->stream);
+    launch_aos_to_soa(io, s.mN, s.mask, s.d.N, s.d.cs, off, c->bad, c->stream);
+    c->launches += 2;
+  }
+  Enq q{c, c->stream};
+  q.x0();
+  c->launches += q.count;
+  int bad = 0;
+  CK(c, cudaMemcpyAsync(&bad, c->bad, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  if (bad) {
+    c->m_set = false;
+    return fail(c, MCQ_ESTATE, "the new geometry makes " + std::to_string(bad) +
+                                   " former vacuum cell(s) magnetic with no magnetisation: call mcq_set_m");
+  }
+  return MCQ_OK;
+}
+
 int mcq_set_geometry(mcq_ctx* c, const unsigned char* mask) {
   if (!c) return MCQ_EINVAL;
   invalidate_graphs(c);  // the trace's mean uses the magnetic cell count
   if (!mask) {
+    const bool had = c->have_mask;
     for (auto& s : c->sl) {
       if (s.mask) cudaFree(s.mask);
       s.mask = nullptr;
     }
     c->have_mask = false;
     c->n_magnetic = c->dg.N;
+    if (had && c->m_set) return remask_state(c);
     return MCQ_OK;
   }
   {
@@ -934,21 +968,7 @@ int mcq_set_geometry(mcq_ctx* c, const unsigned char* mask) {
   }
   CK(c, cudaStreamSynchronize(c->stream));
   c->have_mask = true;
-  if (c->m_set) {  // zero m in vacuum now
-    for (int i = 0; i < (int)c->sl.size(); ++i) {
-      Slab& s = c->sl[i];
-      const long long off = (long long)s.d.zoff * s.d.nx * s.d.ny;
-      float* io = c->io + 3 * i * s.d.N;
-      launch_soa_to_aos(s.mN, io, s.d.N, s.d.cs, off, c->stream);
-      CK(c, cudaMemsetAsync(c->bad, 0, 4, c->stream));
-      launch_aos_to_soa(io, s.mN, s.mask, s.d.N, s.d.cs, off, c->bad, c->stream);
-      c->launches += 2;
-    }
-    Enq q{c, c->stream};
-    q.x0();
-    c->launches += q.count;
-    CK(c, cudaStreamSynchronize(c->stream));
-  }
+  if (c->m_set) return remask_state(c);  // zero m in vacuum now; new magnetic cells need a state
   return MCQ_OK;
 }
 
@@ -1082,9 +1102,26 @@ int mcq_set_cavity(mcq_ctx* c, double f_c, double kappa, double x0, double p0) {
 
 int mcq_set_temperature(mcq_ctx* c, double T, unsigned long long seed) {
   if (!c || !std::isfinite(T) || T < 0) return MCQ_EINVAL;
+  CK(c, cudaMemsetAsync(c->thstep, 0, 8, c->stream));  // a new stream starts at noise step 0
   c->temperature = T;
   c->th_seed = seed;
   invalidate_graphs(c);
+  return MCQ_OK;
+}
+
+int mcq_get_thermal_step(mcq_ctx* c, long long* n) {
+  if (!c || !n) return MCQ_EINVAL;
+  CK(c, cudaMemcpyAsync(n, c->thstep, 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  return MCQ_OK;
+}
+
+int mcq_set_thermal_step(mcq_ctx* c, long long n) {
+  if (!c || n < 0) return MCQ_EINVAL;
+  static long long h;  // pageable source: synchronise before it can change
+  h = n;
+  CK(c, cudaMemcpyAsync(c->thstep, &h, 8, cudaMemcpyHostToDevice, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
   return MCQ_OK;
 }
 
@@ -1328,6 +1365,12 @@ int mcq_get_cavity_mode(mcq_ctx* c, int k, mcq_cavity_state* out) {
   const double dr = 0.5 * c->x0[k] - ar, di = -0.5 * c->p0[k] - ai;
   out->S = kHbar / vc * dr;
   out->C = -kHbar / vc * di;
+  // e^{-kappa t}(S - i C) = (hbar/V_c)(e^{-kappa t} alpha_0 - e^{i w t} alpha): no growing factor
+  const double dec = std::exp(-c->kappa[k] * h.t);
+  const double br = std::cos(w * h.t) * re - std::sin(w * h.t) * im;
+  const double bi = std::cos(w * h.t) * im + std::sin(w * h.t) * re;
+  out->S_resc = kHbar / vc * (dec * 0.5 * c->x0[k] - br);
+  out->C_resc = -kHbar / vc * (-dec * 0.5 * c->p0[k] - bi);
   return MCQ_OK;
 }
 

@@ -18,11 +18,14 @@
 // compute-bound pass.)
 #include <cuda.h>  // CUtensorMap (the encode call itself goes through cudaGetDriverEntryPoint)
 
+#include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "regfft.cuh"
 #include "tma.cuh"
+#include "zconv2.cuh"
 
 namespace mcq {
 
@@ -160,9 +163,10 @@ __device__ __forceinline__ void khat_apply(const float* __restrict__ khat, const
   const float kxy = sy * k23.y;
   const float kxz = sz * k45.x;
   const float kyz = sy * sz * k45.y;
-  const float2 bx = make_float2(kxx * mx.x + kxy * my.x + kxz * mz.x, kxx * mx.y + kxy * my.y + kxz * mz.y);
-  const float2 by = make_float2(kxy * mx.x + kyy * my.x + kyz * mz.x, kxy * mx.y + kyy * my.y + kyz * mz.y);
-  const float2 bz = make_float2(kxz * mx.x + kyz * my.x + kzz * mz.x, kxz * mx.y + kyz * my.y + kzz * mz.y);
+  // packed: each output component is one FMUL2 + two FFMA2 on (re, im)
+  const float2 bx = fma2(bc2(kxz), mz, fma2(bc2(kxy), my, mul2(bc2(kxx), mx)));
+  const float2 by = fma2(bc2(kyz), mz, fma2(bc2(kyy), my, mul2(bc2(kxy), mx)));
+  const float2 bz = fma2(bc2(kzz), mz, fma2(bc2(kyz), my, mul2(bc2(kxz), mx)));
   mx = bx;
   my = by;
   mz = bz;
@@ -522,9 +526,42 @@ static int zconv_seq_cols(const Dims& d, float2* Y, const float* khat, const flo
   return 1;
 }
 
+static int sm_count() {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return nsm;
+}
+
+// K-Z v2 (zconv2.cuh) for Lz = 256 / 512: persistent, 2 CTAs per SM
+template <int L, bool SPLIT>
+static int zconv2_cols(const Dims& d, float2* Y, const float* khat, const float2* tw, int cols, cudaStream_t st) {
+  using Z = Z2Cfg<L>;
+  const int rem = cols % Z::C;
+  const int nkt = cols / Z::C + (rem > 1 ? 1 : 0);
+  const int nlone = rem == 1 ? (d.Ly + Z::C - 1) / Z::C : 0;
+  const int ntiles = nlone + nkt * d.Ly;
+  const int grid = std::min(ntiles, 2 * sm_count());
+  launch_pdl(d.pdl, k_zconv2<L, SPLIT>, dim3(grid), dim3(Z::NT), Z::SMEM, st, Y, khat, d, tw, nkt, nlone, ntiles);
+  return 1;
+}
+
+#ifndef MCQ_ZV2
+#define MCQ_ZV2 1  // K-Z v2 for Lz = 256 / 512 (0: the component-sequential kernel everywhere)
+#endif
+
 int launch_zconv_seq(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t st) {
   const int cols = d.kxw;  // valid columns of this slab
   if (cols <= 0) return 0;
+  static const char* zv = getenv("MCQ_ZVARIANT");
+  const bool v2 = MCQ_ZV2 && !(zv && !strcmp(zv, "seq"));
+  if (v2 && d.Lz == 256) return d.NS > 1 ? zconv2_cols<256, true>(d, Y, khat, tw, cols, st)
+                                         : zconv2_cols<256, false>(d, Y, khat, tw, cols, st);
+  if (v2 && d.Lz == 512) return d.NS > 1 ? zconv2_cols<512, true>(d, Y, khat, tw, cols, st)
+                                         : zconv2_cols<512, false>(d, Y, khat, tw, cols, st);
   int n = 0;
   MCQ_DISPATCH_L(d.Lz, {
     n = d.NS > 1 ? zconv_seq_cols<L, true>(d, Y, khat, tw, cols, st) : zconv_seq_cols<L, false>(d, Y, khat, tw, cols, st);
@@ -592,6 +629,10 @@ void configure_pass_kernels() {
       cudaFuncSetAttribute(k_zconv_tma<L, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZTCfg<L>::SMEM);
     })
   }
+  cudaFuncSetAttribute(k_zconv2<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cfg<256>::SMEM);
+  cudaFuncSetAttribute(k_zconv2<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cfg<256>::SMEM);
+  cudaFuncSetAttribute(k_zconv2<512, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cfg<512>::SMEM);
+  cudaFuncSetAttribute(k_zconv2<512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cfg<512>::SMEM);
   cudaGetLastError();
 }
 

@@ -53,3 +53,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 }
 
 }  // namespace mcq
+
+namespace mcq {
+// L2 prefetch of a contiguous global range (TMA bulk prefetch, no completion tracking): the data
+// is pulled into L2 while the SM works on something else, so the later loads hit L2.
+// addr 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+// per-thread L2 prefetch of the 128-byte line holding p (the bulk form takes uniform operands:
+// issued by every lane with different addresses it serialises across the warp)
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+}  // namespace mcq

@@ -39,7 +39,10 @@ struct UCfg {
   static constexpr int E = N2 < EU ? N2 : EU;
   static constexpr int TL = N2 / E;                       // threads per row
   static constexpr int RY0 = 128 / TL;
-  static constexpr int RY = RY0 < 1 ? 1 : (RY0 > 16 ? 16 : RY0);
+  // at most 16 rows, but at least one full warp (NT >= 32): the warp reductions below use the
+  // full mask (tiny rows, nx <= 8, would otherwise leave lanes 16-31 inactive)
+  static constexpr int RY1 = RY0 < 1 ? 1 : (RY0 > 16 ? 16 : RY0);
+  static constexpr int RY = RY1 * TL < 32 ? 32 / TL : RY1;
   static constexpr int NT = RY * TL;
   // row pitch (complex): a pad slot every 16 positions; even, so rows are 16-byte aligned for TMA
   static constexpr int P0 = N2 + (N2 >= 16 ? N2 / 16 : 1);
@@ -373,7 +376,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
   const float gsum = gs[0];
   // thermal draw of this step: counters 2 (n N + g) (+1), N the global cell count (C-TH)
   const unsigned long long th_base =
-      (GEN && a.th != 0.f) ? 2ull * (unsigned long long)a.cav->step * ((unsigned long long)nx * ny * d.nzg) : 0ull;
+      (GEN && a.th != 0.f) ? 2ull * (unsigned long long)(*a.thstep) * ((unsigned long long)nx * ny * d.nzg) : 0ull;
   double wacc[MM];
 #pragma unroll
   for (int k = 0; k < MM; ++k) wacc[k] = 0.0;
@@ -786,6 +789,7 @@ __global__ void __launch_bounds__(kCavThreads) k_cavity(CavParams p, CavState* s
     }
     st->t += p.dt;
     st->step += 1;
+    if (p.th_count) *p.thstep += 1;  // thermal noise step: never restarted by a memory reset
     if (p.trace && st->step % p.trace_every == 0) {  // NEXT-3: the per-step observables
       const long long r = st->trace_rows;
       if (r < p.trace_cap) {

@@ -52,3 +52,48 @@ def test_single_magnetic_cell_in_vacuum():
     cfg.mask = mask
     cfg.m0 = (cfg.m0 * mask[:, None]).astype(np.float32)
     _check(cfg)
+
+
+def test_geometry_growing_the_magnet_needs_a_fresh_state():
+    """a geometry change that makes former vacuum cells (m = 0) magnetic is applied,
+    reports ESTATE and blocks the run until mcq_set_m; shrinking the magnet keeps the state."""
+    cfg = small_config("sphere", (12, 10, 6), seed=7, state="phys")
+    s = mcq.Solver.from_config(cfg)
+    mask = cfg.mask.copy()
+    smaller = mask.copy()
+    smaller[np.flatnonzero(mask)[:5]] = 0
+    mcq.mcq_set_geometry(s.ctx, smaller)           # shrink: fine, vacuum zeroed
+    assert np.all(s.m()[~smaller.astype(bool)] == 0)
+    s.run(cfg.dt, 2)
+    with pytest.raises(mcq.MCQError) as e:         # grow back: the 5 cells have no m
+        mcq.mcq_set_geometry(s.ctx, mask)
+    assert e.value.code == -2
+    with pytest.raises(mcq.MCQError) as e:
+        s.run(cfg.dt, 1)
+    assert e.value.code == -2
+    s.set_m(cfg.m0)
+    s.run(cfg.dt, 1)
+    with pytest.raises(mcq.MCQError) as e:         # removing the mask: every vacuum cell has m = 0
+        mcq.mcq_set_geometry(s.ctx, None)
+    assert e.value.code == -2
+    s.close()
+
+
+def test_rescaled_accumulators_stay_finite():
+    """S, C grow as e^{kappa t}; the rescaled pair e^{-kappa t}(S, C) is finite for any
+    t and equals the literal pair times e^{-kappa t} while that is representable."""
+    cfg = small_config("film", (8, 6, 1), seed=8, state="phys")
+    cfg.kappa = 2e11                                # kappa t = 700 after 3.5 ns
+    s = mcq.Solver.from_config(cfg)
+    ref = oracle_from(cfg)
+    s.run(1e-12, 200)
+    ref.run(1e-12, 200)
+    cav = s.cavity()
+    k = np.exp(-cfg.kappa * cav["t"])
+    assert np.isfinite(cav["S"]) and abs(cav["S_resc"] - ref.mem.S * k) <= 1e-4 * abs(ref.mem.S * k) + 1e-30
+    assert abs(cav["C_resc"] - ref.mem.C * k) <= 1e-4 * abs(ref.mem.C * k) + 1e-30
+    s.run(1e-12, 4000)                              # kappa t = 840: S, C overflow
+    cav = s.cavity()
+    assert not np.isfinite(cav["S"]) or not np.isfinite(cav["C"]) or abs(cav["S"]) > 1e300
+    assert np.isfinite(cav["S_resc"]) and np.isfinite(cav["C_resc"])
+    s.close()

@@ -27,7 +27,7 @@ def _pair(cfg):
     s = mcq.Solver.from_config(cfg)
     mcq.mcq_set_temperature(s.ctx, T_K, SEED)
     ref = oracle_from(cfg)
-    ref.temperature, ref.seed = T_K, SEED
+    ref.set_temperature(T_K, SEED)
     return s, ref
 
 
@@ -128,8 +128,39 @@ def test_stored_draw_follows_temperature_and_dt_changes():
             (T_K, SEED, cfg.dt, 3)]
     for T, seed, dt, n in plan:
         mcq.mcq_set_temperature(s.ctx, T, seed)
-        ref.temperature, ref.seed = T, seed
+        ref.set_temperature(T, seed)
         s.run(dt, n)
         ref.run(dt, n)
         assert rel_l2(s.m()[mag], ref.m.reshape(-1, 3)[mag]) < 1e-4
+    s.close()
+
+
+def test_noise_step_is_not_restarted_by_memory_resets():
+    """the thermal stream is keyed on its own noise step (RK4 steps since
+    mcq_set_temperature), not on the cavity step count, so mcq_reset_memory / relax / the cavity
+    setters never make a later segment reuse an earlier segment's draws."""
+    cfg = small_config("sphere", (16, 12, 8), seed=24, state="phys")
+    s, ref = _pair(cfg)
+    mag = magmask(cfg)
+    s.run(cfg.dt, 3)
+    ref.run(cfg.dt, 3)
+    assert mcq.mcq_get_thermal_step(s.ctx) == 3 == ref.th_step
+    before = s.field(mcq.TERM_THERM)
+    mcq.mcq_reset_memory(s.ctx)                   # cavity step back to 0, noise step stays 3
+    ref.reset_memory()
+    after = s.field(mcq.TERM_THERM)
+    assert np.array_equal(before, after)
+    assert mcq.mcq_get_thermal_step(s.ctx) == 3
+    s.run(cfg.dt, 2)
+    ref.run(cfg.dt, 2)
+    assert rel_l2(s.m()[mag], ref.m.reshape(-1, 3)[mag]) < 1e-4
+    nxt = s.field(mcq.TERM_THERM)                 # noise step 5: a fresh draw
+    assert rel_l2(nxt[mag], ref.field(ref.m, ref.mem.t, S.THERM).reshape(-1, 3)[mag]) < 1e-5
+    assert not np.allclose(nxt[mag], before[mag])
+    # checkpoint / resume of the noise step
+    mcq.mcq_set_thermal_step(s.ctx, 40)
+    ref.th_step = 40
+    assert rel_l2(s.field(mcq.TERM_THERM)[mag], ref.field(ref.m, ref.mem.t, S.THERM).reshape(-1, 3)[mag]) < 1e-5
+    with pytest.raises(mcq.MCQError):
+        mcq.mcq_set_thermal_step(s.ctx, -1)
     s.close()
