@@ -1,14 +1,15 @@
 #!/usr/bin/env python
-"""Benchmark: LLG + cavity RK4 steps (cell-updates/s) on BASELINE.json configs[1] by default.
+"""Benchmark: LLG + cavity RK4 steps (cell-updates/s) on BASELINE.json configs[4] by default
+(512 x 512 x 256: the grid the metric's 1/2/4/8-GPU strong-scaling target is quoted on).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config k] [--impl mcq|reference]
 
 One process per GPU (torchrun for N > 1).  N > 1 (default --decomp slab): the SAME grid z-slab
 decomposed over the ranks (libmcq's NCCL halos, demag all-to-all transpose and W all-gather;
-"scaling": "strong"); --decomp replicas: independent replicas, one bias-field
-sweep point per rank ("scaling": "weak").  Timing: W
-untimed warm-up steps, then exactly K steps between barrier + synchronize, CUDA events on the
-library's stream, max over ranks.  Rank 0 prints one JSON line.
+"scaling": "strong"), with a bitwise self-check against the undecomposed run
+("self_check"); --decomp replicas: independent replicas, one bias-field sweep point per rank
+("scaling": "weak").  Timing: W untimed warm-up steps, then exactly K steps between barrier +
+synchronize, CUDA events on the library's stream, max over ranks.  Rank 0 prints one JSON line.
 """
 from __future__ import annotations
 
@@ -122,9 +123,13 @@ def step_alg_bytes(L, grid, has_map, slabs=1):
 
 
 # ---------------------------------------------------------------- oracle timing
-def cpu_baseline(cfg, rhs_evals=1):
+def cpu_baseline(cfg, rhs_evals=1, full=None):
     """Oracle (fp64 NumPy, as it stands) on the same workload, bounded sample: `rhs_evals`
-    right-hand-side evaluations (one RK4 step = 4), scaled to cell-updates/s = N * evals/4 / t."""
+    right-hand-side evaluations (one RK4 step = 4), scaled to cell-updates/s = N * evals/4 / t.
+    `full`: the full-size config when `cfg` is its downscaled construction (configs[4]: the
+    direct-DFT oracle needs ~100 GB and hours per RHS at 512 x 512 x 256); the line then also
+    carries the per-cell rate extrapolated to the full grid by the oracle's cost model
+    N (Lx + Ly + Lz) (one DFT-matrix product per padded axis)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from helpers import oracle_from
     t0 = time.perf_counter()
@@ -138,9 +143,19 @@ def cpu_baseline(cfg, rhs_evals=1):
     for _ in range(rhs_evals):
         ref.rhs(ref.m, 0.0)
     dt = time.perf_counter() - t0
-    return {"value": cfg.n * rhs_evals / 4 / dt, "unit": "cell-updates/s", "cores": len(os.sched_getaffinity(0)),
-            "kind": "oracle", "sample": f"{rhs_evals} RHS evaluation(s) (1/4 RK4 step each) of {cfg.name} "
-            f"{tuple(cfg.grid)}, direct-DFT demag in fp64; tensor setup {setup:.1f} s untimed", "seconds": dt}
+    out = {"value": cfg.n * rhs_evals / 4 / dt, "unit": "cell-updates/s", "cores": len(os.sched_getaffinity(0)),
+           "kind": "oracle", "sample": f"{rhs_evals} RHS evaluation(s) (1/4 RK4 step each) of {cfg.name} "
+           f"{tuple(cfg.grid)}, direct-DFT demag in fp64; tensor setup {setup:.1f} s untimed", "seconds": dt}
+    if full is not None:
+        def pad(n):
+            return 1 if n == 1 else 1 << math.ceil(math.log2(2 * n))
+        ls = sum(pad(g) for g in cfg.grid)
+        lf = sum(pad(g) for g in full.grid)
+        out["sample"] = ("downscaled construction: " + out["sample"] +
+                         f"; the full {tuple(full.grid)} grid does not fit the oracle's direct DFT")
+        out["extrapolated_full_grid"] = {"value": out["value"] * ls / lf, "unit": "cell-updates/s",
+                                         "model": "oracle cost per cell ~ Lx + Ly + Lz (padded)"}
+    return out
 
 
 def run_reference(args):
@@ -182,9 +197,11 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
-    ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None, help="default: 40 (configs[4]), 500 (others)")
+    ap.add_argument("--warmup", type=int, default=None, help="default: 5 (configs[4]), 20 (others)")
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=None, help="steps of the end-to-end run (default: --steps)")
+    ap.add_argument("--check-steps", type=int, default=2, help="N > 1 slab runs: steps of the bitwise self-check")
     ap.add_argument("--impl", default="mcq", choices=["mcq", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=5)
@@ -200,6 +217,10 @@ def main():
     ap.add_argument("--temperature", type=float, default=0.0, help="thermal field, K (NEXT-4)")
     ap.add_argument("--dmi", type=float, default=0.0, help="interfacial DMI constant, J/m^2 (NEXT-4)")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 40 if args.config == 4 else 500
+    if args.warmup is None:
+        args.warmup = 5 if args.config == 4 else 20
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
         return run_reference(args)
@@ -296,21 +317,55 @@ def main():
     ms_max = max_over_ranks(ev0.elapsed_time(ev1), device="cuda")
     value = cfg.n * args.steps * jobs / (ms_max * 1e-3)
 
-    # e2e through the public API with host buffers: set_m (H2D) + run + get_m (D2H)
+    # e2e through the public API with host buffers, timed on the host: the state in from pinned
+    # host memory (mcq_set_m, H2D), then every step one mcq_run(dt, 1) call and a device-to-host
+    # read of that step's result (mcq_get_cavity: alpha, W, t, S, C; it synchronises), and the
+    # final state out (mcq_get_m, D2H).  Bytes per step count these copies.
     m_host = torch.from_numpy(np.ascontiguousarray(cfg.m0, np.float32)).pin_memory()
     out_host = torch.empty_like(m_host).pin_memory()
-    e2e_steps = args.steps
+    e2e_steps = args.e2e_steps or args.steps
+    cav_bytes = mcq.mcq_cavity_state_size()
+    for sv in solvers:                       # the 1-step graphs are captured before timing
+        mcq.mcq_set_m(sv.ctx, m_host.numpy())
+        advance(sv, 1)
     barrier()
     t0 = time.perf_counter()
     for sv in solvers:
         mcq.mcq_set_m(sv.ctx, m_host.numpy())
-    for sv in solvers:
-        advance(sv, e2e_steps)
+    for _ in range(e2e_steps):
+        for sv in solvers:
+            advance(sv, 1)
+        for sv in solvers:
+            mcq.mcq_get_cavity(sv.ctx)
     for sv in solvers:
         mcq.mcq_get_m(sv.ctx, cfg.n, out_host.numpy().reshape(-1))
     torch.cuda.synchronize()
     e2e_s = max_over_ranks(time.perf_counter() - t0, device="cuda")
     e2e_val = cfg.n * e2e_steps * jobs / e2e_s
+    h2d_step = 12 * cfg.n * jobs / e2e_steps / (world if slab else 1)
+    d2h_step = (12 * cfg.n * jobs / e2e_steps / (world if slab else 1)) + cav_bytes * len(solvers)
+
+    # N > 1 slab decomposition: every rank replays `check_steps` steps of the undecomposed grid on
+    # its own GPU and compares its planes bitwise with the decomposed result
+    self_check = None
+    if slab:
+        k = args.check_steps
+        for sv in solvers:
+            sv.set_m(cfg.m0)
+            mcq.mcq_reset_memory(sv.ctx)
+            advance(sv, k)
+        got = solvers[0].m()
+        ref1 = mcq.Solver.from_config(cfg, stream=stream.cuda_stream)
+        advance(ref1, k)
+        want = ref1.m()
+        ref1.close()
+        from paper_2410_00966_b200.slabs import cell_range
+        i0, i1 = cell_range(cfg.grid, world, rank)
+        same = bool(np.array_equal(got[i0:i1], want[i0:i1]))
+        allsame = max_over_ranks(0.0 if same else 1.0, device="cuda") == 0.0
+        self_check = {"bitwise_vs_p1": allsame, "steps": k,
+                      "what": "each rank's planes of m after k steps from the same state vs the "
+                              "undecomposed 1-GPU run of the same grid on that rank's GPU"}
 
     # per-kernel timing (CUDA events around each launch, same stream) -> roofline of the top kernel
     prof = mcq.mcq_profile_run(solver.ctx, cfg.dt, args.profile_steps)
@@ -363,11 +418,18 @@ def main():
             "rhs_evals_per_s": (4 if args.integrator == "rk4" else 7) * value,
             "gpu_launches": launches,
             "clocks": clk.summary(),
-            "e2e": {"value": e2e_val, "unit": "cell-updates/s", "h2d_bytes_per_step": 12 * cfg.n * jobs / e2e_steps,
-                    "d2h_bytes_per_step": 12 * cfg.n * jobs / e2e_steps, "steps": e2e_steps},
+            "e2e": {"value": e2e_val, "unit": "cell-updates/s", "h2d_bytes_per_step": h2d_step,
+                    "d2h_bytes_per_step": d2h_step, "steps": e2e_steps,
+                    "calls": "mcq_set_m (pinned H2D) once; per step mcq_run(dt, 1) + mcq_get_cavity "
+                             "(D2H of the step's cavity state, synchronising); mcq_get_m (D2H) at the end"},
         }
+        if self_check is not None:
+            res["self_check"] = self_check
         if world == 1 and not args.no_cpu_baseline:
-            res["cpu_baseline"] = cpu_baseline(cfg)
+            if args.config == 4:
+                res["cpu_baseline"] = cpu_baseline(make_config(4, grid=(128, 128, 64)), rhs_evals=2, full=cfg)
+            else:
+                res["cpu_baseline"] = cpu_baseline(cfg)
         print(json.dumps(res), flush=True)
     for sv in solvers:
         sv.close()

@@ -267,6 +267,9 @@ MCQ_API int mcq_get_m_device(mcq_ctx *, float *d_out);
 MCQ_API int mcq_get_field(mcq_ctx *, float *b_out, unsigned terms);
 
 MCQ_API int mcq_get_cavity(mcq_ctx *, mcq_cavity_state *out);
+/* Bytes one mcq_get_cavity / mcq_get_cavity_mode call copies device -> host (the device-side
+ * cavity record of all modes), for end-to-end traffic accounting. */
+MCQ_API long long mcq_cavity_state_bytes(void);
 /* Resume: sets t, alpha (re/im) and step from `in` (other fields ignored). */
 MCQ_API int mcq_set_cavity_state(mcq_ctx *, const mcq_cavity_state *in);
 

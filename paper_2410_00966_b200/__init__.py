@@ -259,6 +259,11 @@ def mcq_get_cavity(ctx):
     return s.as_dict()
 
 
+def mcq_cavity_state_size():
+    """Bytes one mcq_get_cavity call copies device -> host."""
+    return int(lib.mcq_cavity_state_bytes())
+
+
 def mcq_set_cavity_state(ctx, state):
     s = mcq_cavity_state()
     s.t = float(state["t"])

@@ -85,6 +85,7 @@ _sig = {
     "mcq_get_m_device": (C.c_int, [_P, _P]),
     "mcq_get_field": (C.c_int, [_P, _P, C.c_uint]),
     "mcq_get_cavity": (C.c_int, [_P, C.POINTER(mcq_cavity_state)]),
+    "mcq_cavity_state_bytes": (C.c_longlong, []),
     "mcq_set_cavity_state": (C.c_int, [_P, C.POINTER(mcq_cavity_state)]),
     "mcq_cavity_status": (C.c_int, [_P]),
     "mcq_kernel_launches": (C.c_longlong, [_P]),

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>  // types only: libnccl is dlopen'ed when a multi-process context is created
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX: no-ops unless a profiler attaches
 
 #include <algorithm>
 #include <cmath>
@@ -149,6 +150,18 @@ struct mcq_ctx {
 };
 
 namespace {
+
+// NVTX ranges: one per public call that enqueues work, one per kernel class at enqueue time
+// (visible in eager paths: mcq_profile_run, relax checks, the adaptive integrator, and the
+// graph captures)
+struct NvtxRange {
+  explicit NvtxRange(const char* n) { nvtxRangePushA(n); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+const char* kclass_name(int k) {
+  static const char* n[] = {"K-Y", "K-Z", "K-YI", "K-Y2D", "K-U", "K-CAV"};
+  return k >= 0 && k < 6 ? n[k] : "?";
+}
 
 constexpr int kGraphSteps = 8;
 constexpr long long kPdlMaxCells = 1 << 16;  // PDL only where the step is launch-latency bound
@@ -292,11 +305,13 @@ struct Enq {
   long long count = 0;
   int rc = MCQ_OK;  // first failure of a copy / NCCL call
   void pre(int k) {
+    nvtxRangePushA(kclass_name(k));
     if (hook) hook(user, k, true);
   }
   void post(int k, int n = 1) {  // n: kernels the launcher issued
     count += n;
     if (hook) hook(user, k, false);
+    nvtxRangePop();
   }
   void copy(void* dst, const void* src, size_t bytes) {
     if (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s) != cudaSuccess && rc == MCQ_OK)
@@ -1152,6 +1167,7 @@ int mcq_reset_memory(mcq_ctx* c) {
 
 int mcq_run(mcq_ctx* c, double dt, long long steps) {
   if (!c) return MCQ_EINVAL;
+  NvtxRange nv("mcq_run");
   if (!(dt > 0) || steps < 0) return fail(c, MCQ_EINVAL, "dt must be > 0 and steps >= 0");
   if (!c->m_set) return fail(c, MCQ_ESTATE, "mcq_run before mcq_set_m");
   if (steps == 0) return MCQ_OK;
@@ -1173,6 +1189,7 @@ int mcq_run(mcq_ctx* c, double dt, long long steps) {
 
 int mcq_relax(mcq_ctx* c, double dt, double tol, long long max_steps, long long* taken) {
   if (!c) return MCQ_EINVAL;
+  NvtxRange nv("mcq_relax");
   if (!(dt > 0) || max_steps < 0 || !(tol >= 0)) return fail(c, MCQ_EINVAL, "relax: dt > 0, tol >= 0");
   if (!c->m_set) return fail(c, MCQ_ESTATE, "mcq_relax before mcq_set_m");
   int rc;
@@ -1217,6 +1234,7 @@ static int ensure_dp(mcq_ctx* c) {
 
 int mcq_run_dp(mcq_ctx* c, double dt, long long steps) {
   if (!c) return MCQ_EINVAL;
+  NvtxRange nv("mcq_run_dp");
   if (!(dt > 0) || steps < 0) return fail(c, MCQ_EINVAL, "dt must be > 0 and steps >= 0");
   if (!c->m_set) return fail(c, MCQ_ESTATE, "mcq_run_dp before mcq_set_m");
   if (c->temperature > 0) return fail(c, MCQ_ESTATE, "the thermal field is defined for mcq_run (RK4) only");
@@ -1238,6 +1256,7 @@ int mcq_run_dp(mcq_ctx* c, double dt, long long steps) {
 int mcq_run_adaptive(mcq_ctx* c, double duration, double dt0, double tol, long long max_attempts,
                      long long* accepted, long long* rejected, double* dt_next) {
   if (!c) return MCQ_EINVAL;
+  NvtxRange nv("mcq_run_adaptive");
   if (!(duration >= 0) || !(dt0 > 0) || !(tol > 0) || max_attempts < 0)
     return fail(c, MCQ_EINVAL, "adaptive: duration >= 0, dt0 > 0, tol > 0, max_attempts >= 0");
   if (c->temperature > 0) return fail(c, MCQ_ESTATE, "the thermal field is defined for mcq_run (RK4) only");
@@ -1321,6 +1340,7 @@ int mcq_get_m_device(mcq_ctx* c, float* d_out) {
 
 int mcq_get_field(mcq_ctx* c, float* b_out, unsigned terms) {
   if (!c || !b_out) return MCQ_EINVAL;
+  NvtxRange nv("mcq_get_field");
   if (!c->m_set) return fail(c, MCQ_ESTATE, "mcq_get_field before mcq_set_m");
   if ((terms & MCQ_TERM_THERM) && c->temperature > 0 && !(c->th_dt > 0))
     return fail(c, MCQ_ESTATE, "thermal field before any mcq_run (its scale needs the run's dt)");
@@ -1375,6 +1395,8 @@ int mcq_get_cavity_mode(mcq_ctx* c, int k, mcq_cavity_state* out) {
 }
 
 int mcq_get_cavity(mcq_ctx* c, mcq_cavity_state* out) { return c ? mcq_get_cavity_mode(c, 0, out) : MCQ_EINVAL; }
+
+long long mcq_cavity_state_bytes(void) { return (long long)sizeof(CavState); }
 
 int mcq_set_cavity_state_mode(mcq_ctx* c, int k, const mcq_cavity_state* in) {
   if (!c || !in) return MCQ_EINVAL;
@@ -1463,6 +1485,7 @@ void prof_hook(void* u, int k, bool begin) {
 
 int mcq_profile_run(mcq_ctx* c, double dt, long long steps, double* kernel_ms, int* per_step) {
   if (!c || !kernel_ms) return MCQ_EINVAL;
+  NvtxRange nv("mcq_profile_run");
   if (!(dt > 0) || steps <= 0) return fail(c, MCQ_EINVAL, "profile: dt > 0, steps > 0");
   if (!c->m_set) return fail(c, MCQ_ESTATE, "profile before set_m");
   const CavParams p = cav_params(c, dt);

@@ -26,6 +26,7 @@
 #include "regfft.cuh"
 #include "tma.cuh"
 #include "zconv2.cuh"
+#include "zconv3.cuh"
 
 namespace mcq {
 
@@ -52,9 +53,6 @@ __device__ __forceinline__ void pass_tw(float2* tw, const float2* __restrict__ g
 // more than the mostly idle tile it replaces)
 #ifndef MCQ_YE
 #define MCQ_YE 16   // points per thread per line in K-Y / K-YI
-#endif
-#ifndef MCQ_YREV
-#define MCQ_YREV 1  // K-Y / K-YI CTA order: z descending, components inner (1.013 vs 1.025 ms/step)
 #endif
 #ifndef MCQ_YNT
 #define MCQ_YNT 256  // target threads per CTA in K-Y / K-YI
@@ -89,9 +87,13 @@ struct ColAddr {
 };
 
 // ---------------------------------------------------------------- K-Y forward / inverse
-template <int L, bool INV, int CW = 0>
+// grid (column tiles, 3 nz): blockIdx.y = (z descending, component inner) — the passes meet the
+// planes the previous kernel (K-U, z ascending) wrote last, while they are still in L2.
+// SPLIT: kx-slab-major Y (z slabs over NS ranks, common.cuh); the single-slab instance has no
+// owner arithmetic.  No integer division in the prologue (it was ~1/4 of a thread's work).
+template <int L, bool INV, bool SPLIT, int CW = 0>
 __global__ void __launch_bounds__(PassCfg<L, CW>::NT) k_ypass(const float2* __restrict__ in, float2* __restrict__ out,
-                                                              Dims d, const float2* __restrict__ gtw, int nfull) {
+                                                              Dims d, const float2* __restrict__ gtw) {
   using Cf = PassCfg<L, CW>;
   constexpr int E = Cf::E, TL = Cf::TL, C = Cf::C;
   extern __shared__ __align__(128) float2 sm[];
@@ -101,32 +103,23 @@ __global__ void __launch_bounds__(PassCfg<L, CW>::NT) k_ypass(const float2* __re
   __syncthreads();
   pdl_wait();
   const int c = threadIdx.x % C, t = threadIdx.x / C;
-  // the first nlone CTAs are "lone column" CTAs whose C lanes take C planes of the last column
-  // (NKX = C * nfull + 1), so that column costs nz / C CTAs instead of nz mostly idle ones
-  // (scheduled first: as the last wave they would extend the kernel's tail); the others are
-  // column tile (b % nfull) at plane b / nfull
-#if MCQ_YREV
-  // z descending with the components inner: the passes meet the planes the previous kernel
-  // (K-U, which runs z ascending) wrote last, while they are still in L2
-  const int b = blockIdx.x, rest = b / nfull;
-  const int comp = rest % 3, kx = (b % nfull) * C + c, z = d.nz - 1 - rest / 3;
-#else
-  const int nlone = (gridDim.x - nfull * d.nz), comp = blockIdx.y;
-  const bool lone = (int)blockIdx.x < nlone;
-  const int b = blockIdx.x - nlone;
-  const int kx = lone ? d.NKX - 1 : (b % nfull) * C + c;
-  const int z = lone ? blockIdx.x * C + c : b / nfull;
-#endif
-  const bool ok = kx < d.NKX && z < d.nz;
+  const int rest = blockIdx.y, comp = rest % 3, z = d.nz - 1 - rest / 3;
+  const int kx = blockIdx.x * C + c;
+  const bool ok = kx < d.NKX;
   const int nin = INV ? L : d.ny, nout = INV ? d.ny : L;
-  // X side: X[c][z][y][P]; Y side: kx-slab-major Y[q][c][z][ky][KXS] (common.cuh)
-  const int q = kx_owner(d, kx), kxl = kx - (q > 0 ? kx_first(d, q) : 0);  // kx slab (NS == 1: 0)
-  // 32-bit element indices (every buffer holds < 2^32 elements): an access costs one IMAD and
-  // one IMAD.WIDE.U32 instead of a 64-bit multiply-add chain
+  // X side: X[c][z][y][P]; Y side: Y[q][c][z][ky][KXS] (q = kx slab; single slab: Y[c][z][ky][P])
+  int q = 0, kxl = kx;
+  if constexpr (SPLIT) {
+    q = kx_owner(d, kx);
+    kxl = kx - (q > 0 ? kx_first(d, q) : 0);
+  }
+  // 32-bit element indices (every buffer holds < 2^32 elements)
   const unsigned xoff = ((unsigned)(comp * d.nz + z) * d.ny) * d.P + kx;
   const unsigned yoff = ((unsigned)(q * 3 + comp) * d.nz + z) * (unsigned)L * d.KXS + kxl;
-  const unsigned ioff = INV ? yoff : xoff, ooff = INV ? xoff : yoff;
   const unsigned sin_ = INV ? d.KXS : d.P, sout = INV ? d.P : d.KXS;
+  // this thread's first row and the step between its rows (32-bit offsets from the uniform base)
+  const unsigned ib = (INV ? yoff : xoff) + (unsigned)t * sin_, ob = (INV ? xoff : yoff) + (unsigned)t * sout;
+  const unsigned istep = (unsigned)TL * sin_, ostep = (unsigned)TL * sout;
   float2 v[1][E];
 #pragma unroll
   for (int i = 0; i < E; ++i) {
@@ -134,14 +127,14 @@ __global__ void __launch_bounds__(PassCfg<L, CW>::NT) k_ypass(const float2* __re
     // zero padding: forward input rows >= ny <= Ly/2 are zero, i.e. every i >= E/2 (p >= L/2)
     // statically, so the first stage's butterflies fold those operands away
     v[0][i] = (!INV && 2 * i >= E) ? make_float2(0.f, 0.f)
-                                  : ((ok && p < nin) ? in[ioff + (unsigned)p * sin_] : make_float2(0.f, 0.f));
+                                  : ((ok && p < nin) ? in[ib + i * istep] : make_float2(0.f, 0.f));
   }
   reg_fft<L, E, 1, INV, PASS_TWS>(v, sm + Cf::TWN, ColAddr<L, C>{c}, tw, t);
   if (ok) {
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       const int p = t + TL * i;
-      if ((!INV || 2 * i < E) && p < nout) out[ooff + (unsigned)p * sout] = v[0][i];  // inverse: rows < ny only
+      if ((!INV || 2 * i < E) && p < nout) out[ob + i * ostep] = v[0][i];  // inverse: rows < ny only
     }
   }
 }
@@ -482,28 +475,28 @@ __global__ void __launch_bounds__(ZTCfg<L>::NT, MINB) k_zconv_tma(const __grid_c
     default: break;                                            \
   }
 
-int launch_yfwd(const Dims& d, const float2* X, float2* Y, const float2* tw, cudaStream_t st) {
+// (lone-column CTAs as in K-Z measured slower here: 38.9 / 37.8 vs 37.8 / 35.6 us)
+template <bool INV>
+static int launch_ypass(const Dims& d, const float2* in, float2* out, const float2* tw, cudaStream_t st) {
   int n = 0;
   MCQ_DISPATCH_L(d.Ly, {
     using Cf = PassCfg<L>;
-    // (lone-column CTAs as in K-Z measured slower here: 38.9 / 37.8 vs 37.8 / 35.6 us)
-    const int nfull = (d.NKX + Cf::C - 1) / Cf::C;
-    launch_pdl(d.pdl, k_ypass<L, false>, MCQ_YREV ? dim3(nfull * d.nz * 3) : dim3(nfull * d.nz, 3), dim3(Cf::NT),
-               Cf::SMEM, st, X, Y, d, tw, nfull), ++n;
+    const dim3 grid((d.NKX + Cf::C - 1) / Cf::C, 3 * d.nz);
+    if (d.NS > 1)
+      launch_pdl(d.pdl, k_ypass<L, INV, true>, grid, dim3(Cf::NT), Cf::SMEM, st, in, out, d, tw);
+    else
+      launch_pdl(d.pdl, k_ypass<L, INV, false>, grid, dim3(Cf::NT), Cf::SMEM, st, in, out, d, tw);
+    ++n;
   })
   return n;
 }
 
+int launch_yfwd(const Dims& d, const float2* X, float2* Y, const float2* tw, cudaStream_t st) {
+  return launch_ypass<false>(d, X, Y, tw, st);
+}
+
 int launch_yinv(const Dims& d, const float2* Y, float2* X, const float2* tw, cudaStream_t st) {
-  int n = 0;
-  MCQ_DISPATCH_L(d.Ly, {
-    using Cf = PassCfg<L>;
-    // (lone-column CTAs as in K-Z measured slower here: 38.9 / 37.8 vs 37.8 / 35.6 us)
-    const int nfull = (d.NKX + Cf::C - 1) / Cf::C;
-    launch_pdl(d.pdl, k_ypass<L, true>, MCQ_YREV ? dim3(nfull * d.nz * 3) : dim3(nfull * d.nz, 3), dim3(Cf::NT),
-               Cf::SMEM, st, Y, X, d, tw, nfull), ++n;
-  })
-  return n;
+  return launch_ypass<true>(d, Y, X, tw, st);
 }
 
 int launch_zconv(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t st) {
@@ -544,20 +537,40 @@ static int zconv2_cols(const Dims& d, float2* Y, const float* khat, const float2
   const int nkt = cols / Z::C + (rem > 1 ? 1 : 0);
   const int nlone = rem == 1 ? (d.Ly + Z::C - 1) / Z::C : 0;
   const int ntiles = nlone + nkt * d.Ly;
-  const int grid = std::min(ntiles, 2 * sm_count());
+  const int grid = std::min(ntiles, Z::MINB * sm_count());
   launch_pdl(d.pdl, k_zconv2<L, SPLIT>, dim3(grid), dim3(Z::NT), Z::SMEM, st, Y, khat, d, tw, nkt, nlone, ntiles);
   return 1;
 }
 
+// K-Z v3 (zconv3.cuh) for Lz = 256 / 512: warp-autonomous columns, one CTA per tile
+template <int L, bool SPLIT>
+static int zconv3_cols(const Dims& d, float2* Y, const float* khat, const float2* tw, int cols, cudaStream_t st) {
+  using Z = Z3Cfg<L>;
+  const int rem = cols % Z::C;
+  const int nkt = cols / Z::C + (rem > 1 ? 1 : 0);
+  const int nlone = rem == 1 ? (d.Ly + Z::C - 1) / Z::C : 0;
+  const int ntiles = nlone + nkt * d.Ly;
+  launch_pdl(d.pdl, k_zconv3<L, SPLIT>, dim3(ntiles), dim3(Z::NT), Z::SMEM, st, Y, khat, d, tw, nkt, nlone);
+  return 1;
+}
+
 #ifndef MCQ_ZV2
-#define MCQ_ZV2 1  // K-Z v2 for Lz = 256 / 512 (0: the component-sequential kernel everywhere)
+#define MCQ_ZV2 3  // K-Z for Lz = 256 / 512: 3 = v3 (warp-autonomous), 2 = v2 (persistent), 0 = seq
 #endif
 
 int launch_zconv_seq(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t st) {
   const int cols = d.kxw;  // valid columns of this slab
   if (cols <= 0) return 0;
   static const char* zv = getenv("MCQ_ZVARIANT");
-  const bool v2 = MCQ_ZV2 && !(zv && !strcmp(zv, "seq"));
+  int ver = MCQ_ZV2;
+  if (zv && !strcmp(zv, "seq")) ver = 0;
+  if (zv && !strcmp(zv, "v2")) ver = 2;
+  if (zv && !strcmp(zv, "v3")) ver = 3;
+  if (ver == 3 && d.Lz == 256) return d.NS > 1 ? zconv3_cols<256, true>(d, Y, khat, tw, cols, st)
+                                               : zconv3_cols<256, false>(d, Y, khat, tw, cols, st);
+  if (ver == 3 && d.Lz == 512) return d.NS > 1 ? zconv3_cols<512, true>(d, Y, khat, tw, cols, st)
+                                               : zconv3_cols<512, false>(d, Y, khat, tw, cols, st);
+  const bool v2 = ver == 2;
   if (v2 && d.Lz == 256) return d.NS > 1 ? zconv2_cols<256, true>(d, Y, khat, tw, cols, st)
                                          : zconv2_cols<256, false>(d, Y, khat, tw, cols, st);
   if (v2 && d.Lz == 512) return d.NS > 1 ? zconv2_cols<512, true>(d, Y, khat, tw, cols, st)
@@ -619,8 +632,10 @@ int launch_y2d(const Dims& d, float2* X, const float* khat, const float2* tw, cu
 void configure_pass_kernels() {
   for (int Lv = 2; Lv <= 1024; Lv *= 2) {
     MCQ_DISPATCH_L(Lv, {
-      cudaFuncSetAttribute(k_ypass<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PassCfg<L>::SMEM);
-      cudaFuncSetAttribute(k_ypass<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PassCfg<L>::SMEM);
+      cudaFuncSetAttribute(k_ypass<L, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PassCfg<L>::SMEM);
+      cudaFuncSetAttribute(k_ypass<L, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PassCfg<L>::SMEM);
+      cudaFuncSetAttribute(k_ypass<L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PassCfg<L>::SMEM);
+      cudaFuncSetAttribute(k_ypass<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PassCfg<L>::SMEM);
       cudaFuncSetAttribute(k_conv<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZCfg<L>::SMEM);
       cudaFuncSetAttribute(k_conv<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZCfg<L>::SMEM);
       cudaFuncSetAttribute(k_zconv_tma<L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZTCfg<L>::SMEM);
@@ -629,6 +644,10 @@ void configure_pass_kernels() {
       cudaFuncSetAttribute(k_zconv_tma<L, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZTCfg<L>::SMEM);
     })
   }
+  cudaFuncSetAttribute(k_zconv3<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z3Cfg<256>::SMEM);
+  cudaFuncSetAttribute(k_zconv3<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z3Cfg<256>::SMEM);
+  cudaFuncSetAttribute(k_zconv3<512, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z3Cfg<512>::SMEM);
+  cudaFuncSetAttribute(k_zconv3<512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z3Cfg<512>::SMEM);
   cudaFuncSetAttribute(k_zconv2<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cfg<256>::SMEM);
   cudaFuncSetAttribute(k_zconv2<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cfg<256>::SMEM);
   cudaFuncSetAttribute(k_zconv2<512, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cfg<512>::SMEM);

@@ -32,6 +32,9 @@
 
 namespace mcq {
 
+#ifndef MCQ_Z2C
+#define MCQ_Z2C 16  // kx columns per tile at Lz = 256 (half that at Lz = 512)
+#endif
 #ifndef MCQ_Z2KB
 #define MCQ_Z2KB 8  // Khat multiply: points per batch of loads in flight
 #endif
@@ -44,8 +47,9 @@ struct Z2Cfg {
   static_assert(L == 256 || L == 512, "K-Z v2 handles Lz = 256 and 512");
   static constexpr int NCH = L / 256;      // frequency channels (kz = NCH k + ch)
   static constexpr int LC = 256, E = 16, TL = 16;
-  static constexpr int C = 16 / NCH;       // columns per tile: 128-byte / 64-byte row segments
-  static constexpr int NT = C * TL * NCH;  // 256 threads
+  static constexpr int C = MCQ_Z2C / NCH;  // columns per tile: 128-byte / 64-byte row segments
+  static constexpr int NT = C * TL * NCH;  // 256 threads (MCQ_Z2C = 16)
+  static constexpr int MINB = 512 / NT;    // resident CTAs per SM the launch bounds ask for
   static constexpr int TWP = 18;           // twiddle row pitch (complex): rows 144 B apart (banks)
   static constexpr int TWN = 2 * NCH * 16 * TWP;
   static constexpr int LINE = LC * C;      // complex per (component, channel) block
@@ -62,15 +66,18 @@ __device__ __forceinline__ float2 w32c(int i) {
   return make_float2(cs[i], i < 8 ? cs[(i + 8) & 15] : -cs[(i + 8) & 15]);
 }
 
+// index inside a (component, channel) block.  A row of C complex covers C/16 of the 32 banks; for
+// C < 16 the row's bank group is XOR-ed with bits 4.. of the position, so both the stage stores
+// (positions 16 t + r) and loads (t + 16 i) of a warp spread over all banks (2 wavefronts)
 template <int C>
-__device__ __forceinline__ int z2a(int pos, int c) {  // index inside a (component, channel) block
+__device__ __forceinline__ int z2a(int pos, int c) {
   int a = pos * C + c;
-  if constexpr (C == 8) a ^= ((pos >> 4) & 1) << 3;
+  if constexpr (C < 16) a ^= ((pos >> 4) & (16 / C - 1)) * C;
   return a;
 }
 
 template <int L, bool SPLIT>
-__global__ void __launch_bounds__(Z2Cfg<L>::NT, 2) k_zconv2(float2* __restrict__ Y, const float* __restrict__ khat,
+__global__ void __launch_bounds__(Z2Cfg<L>::NT, Z2Cfg<L>::MINB) k_zconv2(float2* __restrict__ Y, const float* __restrict__ khat,
                                                              Dims d, const float2* __restrict__ gtw, int nkt,
                                                              int nlone, int ntiles) {
   using Z = Z2Cfg<L>;

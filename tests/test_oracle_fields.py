@@ -59,6 +59,25 @@ def test_exchange_discrete_spin_wave_closed_form():
     assert np.allclose(B[0, 0, 1:-1], expect[0, 0, 1:-1], rtol=1e-12, atol=1e-9)
 
 
+@pytest.mark.parametrize("axis", [0, 1, 2])
+def test_exchange_spin_wave_along_each_axis_anisotropic_cell(axis):
+    """the spin-wave pin along x alone left the y / z scaling unpinned (a swap
+    of dy and dz passed every test).  With three distinct cell sizes, a discrete spin wave along
+    axis a gives B = -(2A/Ms)(2 - 2cos(k))/d_a^2 m in the interior — only the right d_a passes."""
+    cell = (1.0e-9, 1.7e-9, 2.9e-9)
+    n, k, A_, Ms = 24, 0.4, 1.2e-11, 9e5
+    shape = [3, 3, 3]
+    shape[2 - axis] = n                          # array axes are (z, y, x)
+    j = np.arange(n).reshape([n if a == 2 - axis else 1 for a in range(3)])
+    m = np.zeros(tuple(shape) + (3,))
+    m[..., 0] = np.cos(k * j)
+    m[..., 1] = np.sin(k * j)
+    B = F.exchange(m, np.ones(tuple(shape), bool), cell, A_, Ms)
+    expect = -(2 * A_ / Ms) * (2 - 2 * math.cos(k)) / cell[axis] ** 2 * m
+    inner = [slice(1, -1) if a == 2 - axis else slice(1, 2) for a in range(3)]   # interior, centre row
+    assert np.allclose(B[tuple(inner)], expect[tuple(inner)], rtol=1e-12, atol=1e-12 * np.abs(expect).max())
+
+
 def test_exchange_total_torque_vanishes():
     mag = rng.random((4, 5, 6)) > 0.2
     m = _rand_m((4, 5, 6), mag)
