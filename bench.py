@@ -324,7 +324,7 @@ def main():
     m_host = torch.from_numpy(np.ascontiguousarray(cfg.m0, np.float32)).pin_memory()
     out_host = torch.empty_like(m_host).pin_memory()
     e2e_steps = args.e2e_steps or args.steps
-    cav_bytes = mcq.mcq_cavity_state_size()
+    cav_bytes = mcq.mcq_cavity_state_bytes()
     for sv in solvers:                       # the 1-step graphs are captured before timing
         mcq.mcq_set_m(sv.ctx, m_host.numpy())
         advance(sv, 1)

@@ -259,7 +259,7 @@ def mcq_get_cavity(ctx):
     return s.as_dict()
 
 
-def mcq_cavity_state_size():
+def mcq_cavity_state_bytes():
     """Bytes one mcq_get_cavity call copies device -> host."""
     return int(lib.mcq_cavity_state_bytes())
 
