@@ -296,6 +296,32 @@ MCQ_API int mcq_set_trace(mcq_ctx *, long long capacity, int every);
  * stored.  max_rows = 0 with out = NULL queries the count. */
 MCQ_API int mcq_get_trace(mcq_ctx *, double *out, long long max_rows, long long *rows);
 
+/* Spectroscopy on the device (the spectra are the numerical Fourier
+ * transform of the spatially averaged magnetisation; couplings read off the anticrossing
+ * of a bias sweep).  fp64 throughout, reading C23:
+ *   x = (s - mean(s)) * window (0: none, 1: Hann = numpy.hanning), zero padded to the power of two
+ *   L >= pad * n; |X_k| of its DFT for 0 < k < L/2; local maxima (|X_k| >= |X_{k-1}|,
+ *   |X_k| > |X_{k+1}|) with f_k = k / (L dt) >= fmin; the npeaks (1..16) largest (ties: lower k),
+ *   each at f = (k + delta) / (L dt), delta the vertex of the parabola through log|X_{k-1,k,k+1}|;
+ *   written to f_out / a_out (Hz, |X|) in ascending frequency, *nfound = how many.
+ * mcq_trace_peaks: s = column `column` (1..7, MCQ_TRACE_COLS order) of this context's recorded
+ *   trace, dt = the recorded clock spacing; ESTATE with fewer than 3 rows.
+ * mcq_trace_peaks_batch: the same for n contexts of one device at once (a bias sweep's replicas:
+ *   one batched launch per FFT stage); outputs [n][npeaks], nfound[n].
+ * mcq_spectrum_peaks: s = a host array of n samples spaced dt (context-free; the current device).
+ * mcq_fit_anticrossing: least squares (omega_c, g) (rad/s) of the normal modes of two position-
+ *   coupled oscillators, lo/hi = sqrt((w1^2 + w2^2 -+ sqrt((w1^2 - w2^2)^2 + 16 g^2 w1 w2)) / 2)
+ *   with w1 = w_mag[i], w2 = omega_c, to n >= 2 measured branch pairs lo[i] < hi[i] (rad/s);
+ *   Levenberg-Marquardt in fp64 on the device from (wc0, g0). */
+MCQ_API int mcq_trace_peaks(mcq_ctx *, int column, int pad, int window, double fmin, int npeaks, double *f_out,
+                            double *a_out, int *nfound);
+MCQ_API int mcq_trace_peaks_batch(mcq_ctx **ctxs, int n, int column, int pad, int window, double fmin, int npeaks,
+                                  double *f_out, double *a_out, int *nfound);
+MCQ_API int mcq_spectrum_peaks(const double *signal, long long n, double dt, int pad, int window, double fmin,
+                               int npeaks, double *f_out, double *a_out, int *nfound);
+MCQ_API int mcq_fit_anticrossing(int n, const double *w_mag, const double *lo, const double *hi, double wc0,
+                                 double g0, double *wc, double *g);
+
 /* Measurement hook: runs `steps` steps with CUDA events around every kernel (no graph) and
  * writes the mean device time (ms) per launch of each MCQ_K_* class to kernel_ms[MCQ_NKCLASS]
  * (0 for classes not launched) and launches per step to per_step[MCQ_NKCLASS] (may be NULL). */
@@ -309,7 +335,8 @@ MCQ_API int mcq_debug_layout(const mcq_ctx *, long long out[6]);
  * order, for index offsets (i, j, k); zero where i >= nx, j >= ny or k >= nz. */
 MCQ_API int mcq_debug_tensor_octant(mcq_ctx *, double *out);
 /* Folded kernel spectrum, fp32 (Lz/2+1, Ly/2+1, P, 6), the 6 components (XX,YY,ZZ,XY,XZ,YZ) fastest:
- * Khat = -mu0 Ms/(Lx Ly Lz) DFT(N) (real: every component is even or odd along each axis). */
+ * Khat = -mu0 Ms/(Lx Ly Lz) DFT(N) (real: every component is even or odd along each axis).
+ * ESTATE on a z-slab rank under NCCL, which stores only the columns of its kx slab. */
 MCQ_API int mcq_debug_khat(mcq_ctx *, float *out);
 
 MCQ_API const char *mcq_last_error(const mcq_ctx *);

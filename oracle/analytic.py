@@ -98,3 +98,19 @@ def peaks(signal, dt, n=2, fmin=0.0, window=None, pad=1):
         delta = 0.5 * (y0 - y2) / d if d != 0 else 0.0
         out.append((k + delta) * (f[1] - f[0]))
     return sorted(out)
+
+
+def fit_two_oscillator(w_mag, lo, hi, wc0, g0):
+    """Least-squares (omega_c, g) (rad/s) of the two_oscillator normal modes (w1 = w_mag,
+    w2 = omega_c) to measured branches lo < hi (the anticrossing read-out of P:14-22, P:419 with
+    lambda -> g), with SciPy's least_squares from (wc0, g0); parameters scaled by wc0."""
+    from scipy.optimize import least_squares
+
+    w_mag, lo, hi = (np.asarray(v, float) for v in (w_mag, lo, hi))
+
+    def res(q):
+        m = np.array([two_oscillator(w, q[0] * wc0, q[1] * wc0) for w in w_mag])
+        return np.concatenate([m[:, 0] - lo, m[:, 1] - hi]) / wc0
+
+    r = least_squares(res, [1.0, g0 / wc0], xtol=1e-15, ftol=1e-15, gtol=1e-15)
+    return float(r.x[0] * wc0), float(abs(r.x[1]) * wc0)

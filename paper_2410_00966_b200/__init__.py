@@ -301,6 +301,59 @@ def mcq_get_trace(ctx, max_rows=None):
     return out
 
 
+# ---------------------------------------------------------------- NEXT-3: device spectroscopy
+def mcq_trace_peaks(ctx, column=2, pad=8, window=1, fmin=0.0, npeaks=2):
+    """Peaks (Hz, |X|) of a recorded trace column (1..7: <mx>, <my>, <mz>, Re a, Im a, W, step),
+    computed on the device (include/mcq.h: FFT, parabolic interpolation, reading C23)."""
+    f = np.zeros(npeaks)
+    a = np.zeros(npeaks)
+    n = C.c_int()
+    _check(ctx, lib.mcq_trace_peaks(ctx, int(column), int(pad), int(window), float(fmin), int(npeaks),
+                                    f.ctypes.data, a.ctypes.data, C.byref(n)))
+    return f[:n.value].copy(), a[:n.value].copy()
+
+
+def mcq_trace_peaks_batch(ctxs, column=2, pad=8, window=1, fmin=0.0, npeaks=2):
+    """mcq_trace_peaks for several contexts (a sweep's replicas) in one batched device pass:
+    list of (f, a) per context."""
+    n = len(ctxs)
+    arr = (C.c_void_p * n)(*[int(c) if not isinstance(c, C.c_void_p) else c.value for c in ctxs])
+    f = np.zeros((n, npeaks))
+    a = np.zeros((n, npeaks))
+    nf = np.zeros(n, np.int32)
+    rc = lib.mcq_trace_peaks_batch(arr, n, int(column), int(pad), int(window), float(fmin), int(npeaks),
+                                   f.ctypes.data, a.ctypes.data, nf.ctypes.data)
+    if rc != 0:
+        raise MCQError(rc, lib.mcq_last_error(ctxs[0]).decode())
+    return [(f[i, :nf[i]].copy(), a[i, :nf[i]].copy()) for i in range(n)]
+
+
+def mcq_spectrum_peaks(signal, dt, pad=8, window=1, fmin=0.0, npeaks=2):
+    """Device spectrum peaks of a host signal (context-free; include/mcq.h)."""
+    x = np.ascontiguousarray(signal, np.float64)
+    f = np.zeros(npeaks)
+    a = np.zeros(npeaks)
+    n = C.c_int()
+    rc = lib.mcq_spectrum_peaks(x.ctypes.data, x.size, float(dt), int(pad), int(window), float(fmin), int(npeaks),
+                                f.ctypes.data, a.ctypes.data, C.byref(n))
+    if rc != 0:
+        raise MCQError(rc, "mcq_spectrum_peaks")
+    return f[:n.value].copy(), a[:n.value].copy()
+
+
+def mcq_fit_anticrossing(w_mag, lo, hi, wc0, g0):
+    """Device least-squares (omega_c, g) (rad/s) of the two-oscillator normal modes to two branches."""
+    w = np.ascontiguousarray(w_mag, np.float64)
+    lo = np.ascontiguousarray(lo, np.float64)
+    hi = np.ascontiguousarray(hi, np.float64)
+    wc, g = C.c_double(), C.c_double()
+    rc = lib.mcq_fit_anticrossing(w.size, w.ctypes.data, lo.ctypes.data, hi.ctypes.data, float(wc0), float(g0),
+                                  C.byref(wc), C.byref(g))
+    if rc != 0:
+        raise MCQError(rc, "mcq_fit_anticrossing")
+    return wc.value, g.value
+
+
 def mcq_kernel_launches(ctx):
     return int(lib.mcq_kernel_launches(ctx))
 

@@ -91,6 +91,11 @@ _sig = {
     "mcq_kernel_launches": (C.c_longlong, [_P]),
     "mcq_set_trace": (C.c_int, [_P, C.c_longlong, C.c_int]),
     "mcq_get_trace": (C.c_int, [_P, _P, C.c_longlong, C.POINTER(C.c_longlong)]),
+    "mcq_trace_peaks": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, _P, _P, _P]),
+    "mcq_trace_peaks_batch": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, _P, _P, _P]),
+    "mcq_spectrum_peaks": (C.c_int, [_P, C.c_longlong, C.c_double, C.c_int, C.c_int, C.c_double, C.c_int, _P, _P, _P]),
+    "mcq_fit_anticrossing": (C.c_int, [C.c_int, _P, _P, _P, C.c_double, C.c_double, C.POINTER(C.c_double),
+                                       C.POINTER(C.c_double)]),
     "mcq_profile_run": (C.c_int, [_P, C.c_double, C.c_longlong, C.POINTER(C.c_double), C.POINTER(C.c_int)]),
     "mcq_debug_layout": (C.c_int, [_P, C.POINTER(C.c_longlong)]),
     "mcq_debug_tensor_octant": (C.c_int, [_P, _P]),

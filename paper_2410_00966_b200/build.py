@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmcq.so")
-SOURCES = ["mcq.cu", "passes.cu", "update.cu", "tensor.cu", "ovf.cpp"]
+SOURCES = ["mcq.cu", "passes.cu", "update.cu", "tensor.cu", "spectro.cu", "ovf.cpp"]
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
          "-Xptxas", "-O3"]

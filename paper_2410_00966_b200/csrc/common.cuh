@@ -55,7 +55,7 @@ constexpr int kTwMax = 1024;                     // global twiddle table length 
 // Sizes of one context's padded spectral layout.  Row layout, kx fastest:
 //   X[c][z][y][P]    complex64 (x-spectrum of m; the demag spectrum in place), rows 16-byte aligned
 //   Y[c][z][ky][P]   complex64 (after the y transform; only the nz real z planes)
-//   Khat[kz][ky][P][g] fp32, kz <= Lz/2, ky <= Ly/2 (real, folded; g = XX,YY,ZZ,XY,XZ,YZ
+//   Khat[kz][ky][kpitch][g] fp32, kz <= Lz/2, ky <= Ly/2 (real, folded; g = XX,YY,ZZ,XY,XZ,YZ
 //                       interleaved: one multiply reads 24 contiguous bytes, three 8-byte loads)
 //
 // z-slab decomposition over NS ranks: nz below is the rank's number of planes,
@@ -79,6 +79,8 @@ struct Dims {
   int NS, KXS;        // kx slabs (ranks) and their storage width (KXS >= every slab's width)
   int kx0, kxw;       // first kx column and width of this rank's slab in the z pass
   int KG, KB;         // kx split: block size (power of two) and number of whole blocks
+  int kpitch, kxoff;  // Khat storage: row pitch (columns) and first stored column — P and 0 unless
+                      // a z-slab rank keeps only its kx slab [kxoff, kxoff + kpitch) (NCCL mode)
   int pdl;            // launch the passes with programmatic dependent launch (see above)
 };
 
@@ -147,6 +149,13 @@ struct UpdateArgs {
   const float* mS;    // stage state (SoA [3][N])
   const float* mN;    // m_n (SoA)
   float* mOut;        // m_{s+1} (stages 1-3) or m_{n+1} (stage 4, may alias mN)
+  // z-slab halos as remote stores (SURVEY §8(e) "halos move P2P over NVLink"): the same-role
+  // buffer of the z-neighbour slab — another slab of this context (loopback) or a peer rank's
+  // buffer mapped over NVLink with CUDA IPC (NCCL mode) — or nullptr.  A CTA writing local plane
+  // 0 also writes it into halo_lo's top halo plane (storage plane nz + 1); local plane nz - 1 goes
+  // into halo_hi's bottom halo plane (storage plane 0).
+  float* halo_lo;
+  float* halo_hi;
   float* acc;         // RK4 accumulator k1 + 2k2 + 2k3 (SoA)
   float2* X;          // x-spectrum rows [3][nz][ny][P]: demag in, FFT(m_{s+1}) out
   const float* brms[kMaxModes];  // SoA map per mode or nullptr (then the uniform value)
@@ -201,18 +210,28 @@ int launch_y2d(const Dims& d, float2* X, const float* khat, const float2* tw, cu
 void configure_update_kernels();
 void launch_update(const UpdateArgs& a, const float2* tw, cudaStream_t s);
 int update_grid_blocks(const Dims& d);
-void launch_cavity(const CavParams& p, CavState* st, const double* partials, int n, int nps, cudaStream_t s);
+void launch_cavity(const CavParams& p, CavState* st, const double* partials, int nps, int nbx, int nzl, int nzg,
+                   const double* psum_in, cudaStream_t s);
+void launch_plane_sums(const CavParams& p, const double* partials, int nps, int nbx, int nzl, double* psum,
+                       cudaStream_t s);
 void launch_cav_prepare(const CavParams& p, CavState* st, cudaStream_t s);
 void launch_aos_to_soa(const float* in, float* out, const uint8_t* mask, long long N, long long cs, long long off,
                        int* bad, cudaStream_t s);
 void launch_soa_to_aos(const float* in, float* out, long long N, long long cs, long long off, cudaStream_t s);
 void launch_deinterleave(const float* in, float* out, long long N, long long cs, long long off, cudaStream_t s);
+// spectro.cu (NEXT-3: spectra, peaks and the anticrossing fit on the device)
+int spectrum_peaks_device(int nb, const double* const* d_sig, const long long* d_n, const int* d_stride,
+                          const double* d_dt, long long nmax, int pad, int window, double fmin, int npeaks,
+                          double* f_out, double* a_out, int* nfound, cudaStream_t s);
+int fit_anticrossing_device(int n, const double* w_mag, const double* lo, const double* hi, double wc0, double g0,
+                            double* wc, double* g);
+void launch_sp_dt(const double* const* d_trace, const long long* d_rows, double* d_dt, int nb, cudaStream_t s);
 // tensor.cu
 void launch_tensor_octant(double* oct, const Dims& d, double dx, double dy, double dz,
                           cudaStream_t s);
 void launch_axis_transform(const double* in, double* out, int m0, int m1, int m2, int axis,
                            const double* Tcos, const double* Tsin, cudaStream_t s);
-void launch_khat_finalize(const double* in, float* khat, const Dims& d, double scale,
+void launch_khat_finalize(const double* in, float* khat, const Dims& d, int kxoff, int kpitch, double scale,
                           cudaStream_t s);
 
 }  // namespace mcq

@@ -90,7 +90,8 @@ struct Slab {
   float* field = nullptr;                           // [3][cs]
   uint8_t* mask = nullptr;                          // [nz][ny][nx]
   double* partials = nullptr;                       // into ctx partials (loopback) or own (NCCL)
-  int nparts = 0;
+  int nparts = 0;                                   // K-U CTAs of one stage (nbx * nz)
+  double* psum = nullptr;                           // NCCL: this rank's plane sums [nz][kNPart]
 };
 
 }  // namespace
@@ -104,6 +105,11 @@ struct mcq_ctx {
   int rank = 0;     // this process's slab (NCCL mode)
   int mode = 0;     // 0 single, 1 loopback (all slabs here), 2 NCCL (one slab per process)
   ncclComm_t comm = nullptr;
+  // z-slab halos as remote stores from K-U (loopback: the neighbour slab's buffers; NCCL: the
+  // neighbour ranks' buffers mapped with CUDA IPC, P2P over NVLink); false: copy / NCCL halos
+  bool remote_halo = false;
+  float* peer_lo[3] = {nullptr, nullptr, nullptr};  // NCCL: rank - 1's mN, mA, mB (IPC-mapped)
+  float* peer_hi[3] = {nullptr, nullptr, nullptr};  // NCCL: rank + 1's
   cudaStream_t stream = nullptr;  // work stream (user's or own)
   cudaStream_t own = nullptr;
   cudaStream_t cap = nullptr;     // capture stream
@@ -125,6 +131,7 @@ struct mcq_ctx {
   CavState* cav = nullptr;
   double* partials = nullptr;  // all slabs' per-CTA partials [CTA][kNPart] in global z order
   int nparts = 0;              // CTAs of one stage-4 update (all slabs)
+  double* psums = nullptr;     // NCCL: gathered plane sums [nzg][kNPart] (update.cu, K-CAV)
   double* trace = nullptr;     // NEXT-3 observables [trace_cap][kTraceCols]
   long long trace_cap = 0;
   int trace_every = 1;
@@ -304,6 +311,18 @@ struct Enq {
   void* user = nullptr;
   long long count = 0;
   int rc = MCQ_OK;  // first failure of a copy / NCCL call
+  long long halo_calls = 0;
+  // same-role buffer (0 mN, 1 mA, 2 mB) of slab i's z-neighbours for K-U's remote halo stores
+  float* halo_peer(int i, int role, bool lo) const {
+    if (!c->remote_halo) return nullptr;
+    auto buf = [&](const Slab& t) { return role == 0 ? t.mN : (role == 1 ? t.mA : t.mB); };
+    if (c->mode == 1) {
+      const int j = lo ? i - 1 : i + 1;
+      return (j >= 0 && j < c->NS) ? buf(c->sl[j]) : nullptr;
+    }
+    if (c->mode == 2) return lo ? c->peer_lo[role] : c->peer_hi[role];
+    return nullptr;
+  }
   void pre(int k) {
     nvtxRangePushA(kclass_name(k));
     if (hook) hook(user, k, true);
@@ -323,6 +342,7 @@ struct Enq {
   // one plane per side of the state buffer `which` (0 mN, 1 mA, 2 mB) into the neighbours' halos
   void halo(int which) {
     if (c->NS == 1) return;
+    ++halo_calls;
     auto buf = [&](Slab& t) { return which == 0 ? t.mN : (which == 1 ? t.mA : t.mB); };
     const Dims& d = c->sl[0].d;
     const size_t pl = (size_t)d.nx * d.ny;
@@ -425,10 +445,14 @@ struct Enq {
   }
   void stage(int st, double dt, int mode, unsigned terms) {
     const int sin_ = st == 1 ? 0 : (st == 2 ? 1 : (st == 3 ? 2 : 1));  // stage state buffer
-    halo(sin_);
+    const int sout = st == 1 ? 1 : (st == 2 ? 2 : (st == 3 ? 1 : 0));  // its output buffer
+    if (!c->remote_halo) halo(sin_);  // else the previous K-U wrote the halo planes remotely
     demag();
-    for (auto& sl : c->sl) {
+    for (int i = 0; i < (int)c->sl.size(); ++i) {
+      Slab& sl = c->sl[i];
       UpdateArgs a = base_args(c, sl);
+      a.halo_lo = halo_peer(i, sout, true);
+      a.halo_hi = halo_peer(i, sout, false);
       a.mode = mode;
       a.stage = st;
       a.terms = terms;
@@ -445,18 +469,26 @@ struct Enq {
       update(a);
     }
   }
-  void gather_partials() {
-    if (c->mode != 2) return;  // single / loopback: every slab already wrote into c->partials
+  // NCCL: this rank's plane sums of the overlap partials, all-gathered in z order (nzg x kNPart
+  // doubles); single / loopback: K-CAV sums every slab's partials itself, in the same tree
+  void gather_partials(const CavParams& p) {
+    if (c->mode != 2) return;
     Slab& sl = c->sl[0];
-    nk(nccl_api()->allGather(sl.partials, c->partials, (size_t)sl.nparts * kNPart, ncclDouble, c->comm, s));
+    launch_plane_sums(p, sl.partials, sl.nparts, sl.nparts / sl.d.nz, sl.d.nz, sl.psum, s);
+    ++count;
+    nk(nccl_api()->allGather(sl.psum, c->psums, (size_t)sl.d.nz * kNPart, ncclDouble, c->comm, s));
+  }
+  void cavity(const CavParams& p) {
+    gather_partials(p);
+    const Slab& s0 = c->sl[0];
+    pre(MCQ_K_CAVITY);
+    launch_cavity(p, c->cav, c->partials, s0.nparts, s0.nparts / s0.d.nz, s0.d.nz, c->dg.nz,
+                  c->mode == 2 ? c->psums : nullptr, s);
+    post(MCQ_K_CAVITY);
   }
   void llg_step(double dt) {
     for (int st = 1; st <= 4; ++st) stage(st, dt, MODE_LLG, MCQ_TERM_ALL);
-    gather_partials();
-    const CavParams p = cav_params(c, dt);
-    pre(MCQ_K_CAVITY);
-    launch_cavity(p, c->cav, c->partials, c->nparts, c->sl[0].nparts, s);
-    post(MCQ_K_CAVITY);
+    cavity(cav_params(c, dt));
   }
   void relax_step(double dt) {
     for (int st = 1; st <= 4; ++st)
@@ -476,10 +508,15 @@ struct Enq {
         {35.0 / 384 - 5179.0 / 57600, 0.0, 500.0 / 1113 - 7571.0 / 16695, 125.0 / 192 - 393.0 / 640,
          -2187.0 / 6784 + 92097.0 / 339200, 11.0 / 84 - 187.0 / 2100, -1.0 / 40}};  // b5 - b4
     const int in = st == 1 ? 0 : ((st - 1) % 2 == 1 ? 1 : 2);
-    halo(in);
+    if (!c->remote_halo) halo(in);
     demag();
-    for (auto& sl : c->sl) {
+    for (int i = 0; i < (int)c->sl.size(); ++i) {
+      Slab& sl = c->sl[i];
       UpdateArgs a = base_args(c, sl);
+      if (st < 7) {
+        a.halo_lo = halo_peer(i, st % 2 == 1 ? 1 : 2, true);
+        a.halo_hi = halo_peer(i, st % 2 == 1 ? 1 : 2, false);
+      }
       a.mode = MODE_DP;
       a.stage = st;
       a.mN = sl.mN;
@@ -500,11 +537,7 @@ struct Enq {
   }
   void dp_commit(double dt) {  // m_n <- y5; every mode's alpha advances by dt on W(y5)
     for (auto& sl : c->sl) copy(sl.mN, sl.mB, 3ULL * sl.d.cs * sizeof(float));
-    gather_partials();
-    const CavParams p = cav_params(c, dt, true);
-    pre(MCQ_K_CAVITY);
-    launch_cavity(p, c->cav, c->partials, c->nparts, c->sl[0].nparts, s);
-    post(MCQ_K_CAVITY);
+    cavity(cav_params(c, dt, true));
   }
   void x0() {  // X <- R2C(m_n) in every slab
     for (auto& sl : c->sl) {
@@ -657,7 +690,9 @@ int build_khat(mcq_ctx* c, double* oct_out /* optional host copy of the octant *
     }
     if (rc == MCQ_OK) {
       const double scale = -kMu0 * c->Ms / ((double)d.Lx * d.Ly * d.Lz);
-      launch_khat_finalize(src, c->khat, d, scale, c->stream);
+      // a z-slab rank under NCCL keeps only its kx slab of Khat (1/world of the spectrum)
+      const Dims& s0 = c->sl[0].d;
+      launch_khat_finalize(src, c->khat, d, s0.kxoff, s0.kpitch, scale, c->stream);
       if (cudaStreamSynchronize(c->stream) != cudaSuccess) rc = fail(c, MCQ_ECUDA, "khat finalize");
     }
   }
@@ -669,15 +704,22 @@ int build_khat(mcq_ctx* c, double* oct_out /* optional host copy of the octant *
 
 void free_all(mcq_ctx* c) {
   invalidate_graphs(c);
+  for (int r = 0; r < 3; ++r) {
+    if (c->peer_lo[r]) cudaIpcCloseMemHandle(c->peer_lo[r]);
+    if (c->peer_hi[r]) cudaIpcCloseMemHandle(c->peer_hi[r]);
+    c->peer_lo[r] = c->peer_hi[r] = nullptr;
+  }
   for (auto& s : c->sl) {
     void* ptrs[] = {s.mN, s.mA, s.mB, s.acc, s.X, s.Y, s.R, s.K, s.brms[0], s.brms[1], s.brms[2], s.brms[3],
                     s.field, s.mask, s.eta};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (c->mode == 2 && s.partials) cudaFree(s.partials);
+    if (s.psum) cudaFree(s.psum);
   }
   c->sl.clear();
-  void* ptrs[] = {c->tw, c->khat, c->cav, c->partials, c->maxbits, c->bad, c->nonfinite, c->io, c->trace, c->thstep};
+  void* ptrs[] = {c->tw, c->khat, c->cav, c->partials, c->psums, c->maxbits, c->bad, c->nonfinite, c->io, c->trace,
+                  c->thstep};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->comm) nccl_api()->commDestroy(c->comm);
@@ -740,6 +782,47 @@ int alloc_slab(mcq_ctx* c, Slab& s) {
 
 std::once_flag g_cfg_once;
 
+// NCCL mode: map the z-neighbour ranks' state buffers (mN, mA, mB) into this process with CUDA IPC
+// (handles all-gathered over the context's communicator) so K-U can store its boundary planes
+// straight into their halo planes over NVLink.  Any failure leaves the NCCL halos in place.
+int setup_peer_halos(mcq_ctx* c) {
+  Nccl* n = nccl_api();
+  if (!n) return MCQ_ENCCL;
+  Slab& sl = c->sl[0];
+  cudaIpcMemHandle_t mine[3];
+  float* bufs[3] = {sl.mN, sl.mA, sl.mB};
+  for (int r = 0; r < 3; ++r)
+    if (cudaIpcGetMemHandle(&mine[r], bufs[r]) != cudaSuccess) {
+      cudaGetLastError();
+      return MCQ_ECUDA;
+    }
+  const size_t hb = sizeof(mine);
+  char* d = nullptr;
+  if (cudaMalloc(&d, hb * (c->NS + 1)) != cudaSuccess) return MCQ_ENOMEM;
+  std::vector<cudaIpcMemHandle_t> all(3 * c->NS);
+  int rc = MCQ_OK;
+  if (cudaMemcpyAsync(d, mine, hb, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+      n->allGather(d, d + hb, hb, ncclChar, c->comm, c->stream) != ncclSuccess ||
+      cudaMemcpyAsync(all.data(), d + hb, hb * c->NS, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess)
+    rc = MCQ_ENCCL;
+  cudaFree(d);
+  if (rc != MCQ_OK) return rc;
+  for (int side = 0; side < 2; ++side) {
+    const int peer = c->rank + (side == 0 ? -1 : 1);
+    if (peer < 0 || peer >= c->NS) continue;
+    for (int r = 0; r < 3; ++r) {
+      void* p = nullptr;
+      if (cudaIpcOpenMemHandle(&p, all[3 * peer + r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        return MCQ_ECUDA;
+      }
+      (side == 0 ? c->peer_lo : c->peer_hi)[r] = static_cast<float*>(p);
+    }
+  }
+  return MCQ_OK;
+}
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -800,6 +883,8 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
   g.kxw = g.NKX;
   g.KG = 16;
   g.KB = g.NKX / 16;
+  g.kpitch = g.P;
+  g.kxoff = 0;
   g.pdl = 0;
   auto bail = [&](int code) {
     free_all(c);
@@ -860,13 +945,19 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
     s.d.KB = split.KB;
     s.d.kx0 = kx_first(split, r);
     s.d.kxw = kx_first(split, r + 1) - s.d.kx0;
+    if (c->mode == 2) {  // Khat sharded to this rank's kx slab (even pitch: 16-byte Khat rows)
+      s.d.kxoff = s.d.kx0;
+      s.d.kpitch = std::max(2, (s.d.kxw + 1) & ~1);
+    }
     s.d.pdl = (c->mode == 0 && g.N <= kPdlMaxCells) ? 1 : 0;  // see common.cuh
     s.nparts = update_grid_blocks(s.d);
     if (alloc_slab(c, s) != MCQ_OK) return bail(MCQ_ENOMEM);
   }
-  bool ok = cudaMalloc(&c->khat, 6ULL * (g.Lz / 2 + 1) * (g.Ly / 2 + 1) * g.P * 4) == cudaSuccess &&
+  const size_t nkhat = 6ULL * (g.Lz / 2 + 1) * (g.Ly / 2 + 1) * c->sl[0].d.kpitch;
+  bool ok = cudaMalloc(&c->khat, nkhat * 4) == cudaSuccess &&
             cudaMalloc(&c->tw, kTwMax * 8) == cudaSuccess && cudaMalloc(&c->cav, sizeof(CavState)) == cudaSuccess &&
-            cudaMalloc(&c->partials, (size_t)c->nparts * kNPart * 8) == cudaSuccess &&
+            cudaMalloc(&c->partials, (size_t)(c->mode == 2 ? 1 : c->nparts) * kNPart * 8) == cudaSuccess &&
+            cudaMalloc(&c->psums, (size_t)g.nz * kNPart * 8) == cudaSuccess &&
             cudaMalloc(&c->maxbits, 4) == cudaSuccess && cudaMalloc(&c->bad, 4) == cudaSuccess &&
             cudaMalloc(&c->nonfinite, 4) == cudaSuccess && cudaMalloc(&c->thstep, 8) == cudaSuccess &&
             cudaMalloc(&c->io, 3ULL * c->cells_here() * 4) == cudaSuccess;
@@ -877,13 +968,18 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
   for (int i = 0; i < count; ++i) {
     Slab& s = c->sl[i];
     if (c->mode == 2) {
-      if (cudaMalloc(&s.partials, (size_t)s.nparts * kNPart * 8) != cudaSuccess) return bail(MCQ_ENOMEM);
+      if (cudaMalloc(&s.partials, (size_t)s.nparts * kNPart * 8) != cudaSuccess ||
+          cudaMalloc(&s.psum, (size_t)s.d.nz * kNPart * 8) != cudaSuccess)
+        return bail(MCQ_ENOMEM);
+      cudaMemsetAsync(s.partials, 0, (size_t)s.nparts * kNPart * 8, c->stream);
+      cudaMemsetAsync(s.psum, 0, (size_t)s.d.nz * kNPart * 8, c->stream);
     } else {
       s.partials = c->partials + (size_t)i * s.nparts * kNPart;  // global z order = slab order
     }
   }
-  if (cudaMemsetAsync(c->khat, 0, 6ULL * (g.Lz / 2 + 1) * (g.Ly / 2 + 1) * g.P * 4, c->stream) != cudaSuccess ||
-      cudaMemsetAsync(c->partials, 0, (size_t)c->nparts * kNPart * 8, c->stream) != cudaSuccess ||
+  if (cudaMemsetAsync(c->khat, 0, nkhat * 4, c->stream) != cudaSuccess ||
+      cudaMemsetAsync(c->partials, 0, (size_t)(c->mode == 2 ? 1 : c->nparts) * kNPart * 8, c->stream) != cudaSuccess ||
+      cudaMemsetAsync(c->psums, 0, (size_t)g.nz * kNPart * 8, c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->maxbits, 0, 4, c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->nonfinite, 0, 4, c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->thstep, 0, 8, c->stream) != cudaSuccess)
@@ -901,6 +997,12 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
   }
   if (build_khat(c, nullptr) != MCQ_OK) return bail(MCQ_ECUDA);
   make_y_tensor_map(c);
+  {
+    static const char* hv = getenv("MCQ_HALO");  // "copy": copy / NCCL halos (comparison)
+    const bool want = !(hv && !strcmp(hv, "copy"));
+    if (c->mode == 1) c->remote_halo = want;
+    if (c->mode == 2 && want) c->remote_halo = setup_peer_halos(c) == MCQ_OK;
+  }
   if (c->mode == 2) {
     // one eager round of every exchange (on zeroed buffers): NCCL sets up its peer connections
     // here, outside any graph capture
@@ -910,7 +1012,7 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
       q.alltoall(true);
       q.alltoall(false);
     }
-    q.nk(nccl_api()->allGather(c->sl[0].partials, c->partials, (size_t)c->sl[0].nparts * kNPart, ncclDouble, c->comm,
+    q.nk(nccl_api()->allGather(c->sl[0].psum, c->psums, (size_t)c->sl[0].d.nz * kNPart, ncclDouble, c->comm,
                                c->stream));
     q.nk(nccl_api()->allReduce(c->maxbits, c->maxbits, 1, ncclFloat, ncclMax, c->comm, c->stream));
     if (q.rc != MCQ_OK || cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(MCQ_ENCCL);
@@ -944,6 +1046,7 @@ static int remask_state(mcq_ctx* c) {
     c->launches += 2;
   }
   Enq q{c, c->stream};
+  q.halo(0);
   q.x0();
   c->launches += q.count;
   int bad = 0;
@@ -1001,6 +1104,8 @@ static int set_m_from_io(mcq_ctx* c) {
   if (bad) return fail(c, MCQ_EINVAL, std::to_string(bad) + " magnetic cells with a zero or non-finite vector");
   for (auto& s : c->sl) CK(c, cudaMemcpyAsync(s.mN, s.mA, 3ULL * s.d.cs * 4, cudaMemcpyDeviceToDevice, c->stream));
   Enq q{c, c->stream};
+  q.halo(0);  // a fresh state: its halo planes (later steps keep them current from K-U)
+  if (q.rc != MCQ_OK) return q.rc;
   q.x0();
   c->launches += q.count + (long long)c->sl.size();
   CK(c, cudaMemsetAsync(c->nonfinite, 0, 4, c->stream));  // a fresh state clears a divergence
@@ -1463,6 +1568,96 @@ int mcq_get_trace(mcq_ctx* c, double* out, long long max_rows, long long* rows) 
 
 long long mcq_kernel_launches(const mcq_ctx* c) { return c ? c->launches : -1; }
 
+// ---------------------------------------------------------------- NEXT-3: device spectroscopy
+int mcq_trace_peaks_batch(mcq_ctx** ctxs, int n, int column, int pad, int window, double fmin, int npeaks,
+                          double* f_out, double* a_out, int* nfound) {
+  if (!ctxs || n < 1 || n > 1024 || column < 1 || column >= kTraceCols || !f_out || !a_out || !nfound)
+    return MCQ_EINVAL;
+  std::vector<const double*> ptr(n), tptr(n);
+  std::vector<long long> rows(n);
+  std::vector<int> stride(n, kTraceCols);
+  long long nmax = 0;
+  for (int b = 0; b < n; ++b) {
+    mcq_ctx* c = ctxs[b];
+    if (!c) return MCQ_EINVAL;
+    if (c->device != ctxs[0]->device) return fail(ctxs[0], MCQ_EINVAL, "traces on different devices");
+    CavState h{};
+    CK(c, cudaMemcpyAsync(&h, c->cav, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    rows[b] = std::min(h.trace_rows, c->trace_cap);
+    if (rows[b] < 3 || !c->trace) return fail(c, MCQ_ESTATE, "fewer than 3 trace rows recorded (mcq_set_trace)");
+    ptr[b] = c->trace + column;
+    tptr[b] = c->trace;  // column 0: the clock t
+    nmax = std::max(nmax, rows[b]);
+  }
+  mcq_ctx* c0 = ctxs[0];
+  void* dmem = nullptr;
+  const size_t bytes = (size_t)n * (8 + 8 + 8 + 8 + 4) + 64;
+  CK(c0, cudaMalloc(&dmem, bytes));
+  char* p = static_cast<char*>(dmem);
+  const double** dptr = reinterpret_cast<const double**>(p);
+  long long* drows = reinterpret_cast<long long*>(p + 8 * n);
+  double* ddt = reinterpret_cast<double*>(p + 16 * n);
+  const double** dtp = reinterpret_cast<const double**>(p + 24 * n);
+  int* dstride = reinterpret_cast<int*>(p + 32 * n);
+  int rc = MCQ_OK;
+  if (cudaMemcpyAsync(dptr, ptr.data(), 8 * n, cudaMemcpyHostToDevice, c0->stream) != cudaSuccess ||
+      cudaMemcpyAsync(drows, rows.data(), 8 * n, cudaMemcpyHostToDevice, c0->stream) != cudaSuccess ||
+      cudaMemcpyAsync(dtp, tptr.data(), 8 * n, cudaMemcpyHostToDevice, c0->stream) != cudaSuccess ||
+      cudaMemcpyAsync(dstride, stride.data(), 4 * n, cudaMemcpyHostToDevice, c0->stream) != cudaSuccess) {
+    rc = fail(c0, MCQ_ECUDA, "spectrum setup copy");
+  } else {
+    launch_sp_dt(reinterpret_cast<const double* const*>(dtp), drows, ddt, n, c0->stream);
+    rc = spectrum_peaks_device(n, dptr, drows, dstride, ddt, nmax, pad, window, fmin, npeaks, f_out, a_out, nfound,
+                               c0->stream);
+    if (rc != MCQ_OK) fail(c0, rc, "device spectrum");
+  }
+  cudaStreamSynchronize(c0->stream);
+  cudaFree(dmem);
+  return rc;
+}
+
+int mcq_trace_peaks(mcq_ctx* c, int column, int pad, int window, double fmin, int npeaks, double* f_out,
+                    double* a_out, int* nfound) {
+  return c ? mcq_trace_peaks_batch(&c, 1, column, pad, window, fmin, npeaks, f_out, a_out, nfound) : MCQ_EINVAL;
+}
+
+int mcq_spectrum_peaks(const double* signal, long long n, double dt, int pad, int window, double fmin, int npeaks,
+                       double* f_out, double* a_out, int* nfound) {
+  if (!signal || n < 3 || !(dt > 0) || !f_out || !a_out || !nfound) return MCQ_EINVAL;
+  double* d = nullptr;
+  void* meta = nullptr;
+  if (cudaMalloc(&d, (size_t)n * 8) != cudaSuccess || cudaMalloc(&meta, 64) != cudaSuccess) {
+    cudaFree(d);
+    cudaGetLastError();
+    return MCQ_ENOMEM;
+  }
+  char* p = static_cast<char*>(meta);
+  const double* ptr = d;
+  const int stride = 1;
+  int rc = MCQ_OK;
+  if (cudaMemcpy(d, signal, (size_t)n * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(p, &ptr, 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(p + 8, &n, 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(p + 16, &dt, 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(p + 24, &stride, 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+    rc = MCQ_ECUDA;
+  } else {
+    rc = spectrum_peaks_device(1, reinterpret_cast<const double* const*>(p), reinterpret_cast<const long long*>(p + 8),
+                               reinterpret_cast<const int*>(p + 24), reinterpret_cast<const double*>(p + 16), n, pad,
+                               window, fmin, npeaks, f_out, a_out, nfound, 0);
+  }
+  cudaFree(d);
+  cudaFree(meta);
+  return rc;
+}
+
+int mcq_fit_anticrossing(int n, const double* w_mag, const double* lo, const double* hi, double wc0, double g0,
+                         double* wc, double* g) {
+  if (!w_mag || !lo || !hi || !wc || !g) return MCQ_EINVAL;
+  return fit_anticrossing_device(n, w_mag, lo, hi, wc0, g0, wc, g);
+}
+
 namespace {
 struct Prof {
   cudaStream_t s;
@@ -1532,6 +1727,7 @@ int mcq_debug_tensor_octant(mcq_ctx* c, double* out) {
 
 int mcq_debug_khat(mcq_ctx* c, float* out) {
   if (!c || !out) return MCQ_EINVAL;
+  if (c->sl[0].d.kpitch != c->dg.P) return fail(c, MCQ_ESTATE, "Khat is sharded to this rank's kx slab (NCCL mode)");
   const size_t nK = 6ULL * (c->dg.Lz / 2 + 1) * (c->dg.Ly / 2 + 1) * c->dg.P;
   CK(c, cudaMemcpyAsync(out, c->khat, nK * 4, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));

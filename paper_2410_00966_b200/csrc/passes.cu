@@ -26,7 +26,6 @@
 #include "regfft.cuh"
 #include "tma.cuh"
 #include "zconv2.cuh"
-#include "zconv3.cuh"
 
 namespace mcq {
 
@@ -149,7 +148,7 @@ __device__ __forceinline__ void khat_apply(const float* __restrict__ khat, const
   const int kzf = kz <= hz ? kz : d.Lz - kz;
   const float sy = ky <= hy ? 1.f : -1.f;
   const float sz = kz <= hz ? 1.f : -1.f;
-  const unsigned b = (((unsigned)kzf * (hy + 1) + kyf) * d.P + kx) * 3;  // float2 index
+  const unsigned b = (((unsigned)kzf * (hy + 1) + kyf) * d.kpitch + kx - d.kxoff) * 3;  // float2 index
   const float2* k2 = reinterpret_cast<const float2*>(khat) + b;
   const float2 k01 = __ldg(k2), k23 = __ldg(k2 + 1), k45 = __ldg(k2 + 2);
   const float kxx = k01.x, kyy = k01.y, kzz = k23.x;
@@ -542,35 +541,24 @@ static int zconv2_cols(const Dims& d, float2* Y, const float* khat, const float2
   return 1;
 }
 
-// K-Z v3 (zconv3.cuh) for Lz = 256 / 512: warp-autonomous columns, one CTA per tile
-template <int L, bool SPLIT>
-static int zconv3_cols(const Dims& d, float2* Y, const float* khat, const float2* tw, int cols, cudaStream_t st) {
-  using Z = Z3Cfg<L>;
-  const int rem = cols % Z::C;
-  const int nkt = cols / Z::C + (rem > 1 ? 1 : 0);
-  const int nlone = rem == 1 ? (d.Ly + Z::C - 1) / Z::C : 0;
-  const int ntiles = nlone + nkt * d.Ly;
-  launch_pdl(d.pdl, k_zconv3<L, SPLIT>, dim3(ntiles), dim3(Z::NT), Z::SMEM, st, Y, khat, d, tw, nkt, nlone);
-  return 1;
-}
-
-#ifndef MCQ_ZV2
-#define MCQ_ZV2 3  // K-Z for Lz = 256 / 512: 3 = v3 (warp-autonomous), 2 = v2 (persistent), 0 = seq
+// K-Z kernel per length (measured, round 2, 1x B200; profiles/r2_zconv_variants.md):
+//   Lz = 256 (configs[1]-[3]): component-sequential k_zconv_seq 119 us, v2 153 us, warp-
+//   autonomous columns (v3, removed) 189 us;  Lz = 512 (configs[4]): v2 5.36 ms, seq 5.57 ms,
+//   v3 14.95 ms (per-warp 8-byte row pieces: 4x the L2 sector traffic)
+#ifndef MCQ_ZV2_256
+#define MCQ_ZV2_256 0
+#endif
+#ifndef MCQ_ZV2_512
+#define MCQ_ZV2_512 1
 #endif
 
 int launch_zconv_seq(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t st) {
   const int cols = d.kxw;  // valid columns of this slab
   if (cols <= 0) return 0;
-  static const char* zv = getenv("MCQ_ZVARIANT");
-  int ver = MCQ_ZV2;
-  if (zv && !strcmp(zv, "seq")) ver = 0;
-  if (zv && !strcmp(zv, "v2")) ver = 2;
-  if (zv && !strcmp(zv, "v3")) ver = 3;
-  if (ver == 3 && d.Lz == 256) return d.NS > 1 ? zconv3_cols<256, true>(d, Y, khat, tw, cols, st)
-                                               : zconv3_cols<256, false>(d, Y, khat, tw, cols, st);
-  if (ver == 3 && d.Lz == 512) return d.NS > 1 ? zconv3_cols<512, true>(d, Y, khat, tw, cols, st)
-                                               : zconv3_cols<512, false>(d, Y, khat, tw, cols, st);
-  const bool v2 = ver == 2;
+  static const char* zv = getenv("MCQ_ZVARIANT");  // experiment override: seq | v2
+  bool v2 = d.Lz == 256 ? MCQ_ZV2_256 : MCQ_ZV2_512;
+  if (zv && !strcmp(zv, "seq")) v2 = false;
+  if (zv && !strcmp(zv, "v2")) v2 = true;
   if (v2 && d.Lz == 256) return d.NS > 1 ? zconv2_cols<256, true>(d, Y, khat, tw, cols, st)
                                          : zconv2_cols<256, false>(d, Y, khat, tw, cols, st);
   if (v2 && d.Lz == 512) return d.NS > 1 ? zconv2_cols<512, true>(d, Y, khat, tw, cols, st)
@@ -644,10 +632,6 @@ void configure_pass_kernels() {
       cudaFuncSetAttribute(k_zconv_tma<L, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZTCfg<L>::SMEM);
     })
   }
-  cudaFuncSetAttribute(k_zconv3<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z3Cfg<256>::SMEM);
-  cudaFuncSetAttribute(k_zconv3<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z3Cfg<256>::SMEM);
-  cudaFuncSetAttribute(k_zconv3<512, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z3Cfg<512>::SMEM);
-  cudaFuncSetAttribute(k_zconv3<512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z3Cfg<512>::SMEM);
   cudaFuncSetAttribute(k_zconv2<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cfg<256>::SMEM);
   cudaFuncSetAttribute(k_zconv2<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cfg<256>::SMEM);
   cudaFuncSetAttribute(k_zconv2<512, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cfg<512>::SMEM);

@@ -132,16 +132,18 @@ __global__ void k_axis_transform(const double* __restrict__ in, double* __restri
 }
 
 // Khat[c][kz][ky][P] (fp32, row layout) = scale * sign_c * Nhat[c][kz][ky][kx]
+// columns [kxoff, kxoff + kpitch) of the folded spectrum (all of them: kxoff = 0, kpitch = P)
 __global__ void k_khat_finalize(const double* __restrict__ in, float* __restrict__ khat, int m0, int m1, int m2,
-                                int P, double scale) {
+                                int kxoff, int kpitch, double scale) {
   const long long per = (long long)m0 * m1 * m2;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < 6 * per; e += (long long)gridDim.x * blockDim.x) {
     const int c = (int)(e / per);
     const long long r = e - c * per;
-    const int i0 = (int)(r % m0);
+    const int i0 = (int)(r % m0) - kxoff;
+    if (i0 < 0 || i0 >= kpitch) continue;
     const long long row = r / m0;            // kz * m1 + ky
     const double sgn = c >= 3 ? -1.0 : 1.0;  // (-i)^2 of the two odd axes
-    khat[(row * P + i0) * 6 + c] = (float)(scale * sgn * in[e]);  // [kz][ky][P][6]: 6 adjacent floats
+    khat[(row * kpitch + i0) * 6 + c] = (float)(scale * sgn * in[e]);  // [kz][ky][kpitch][6]
   }
 }
 
@@ -161,9 +163,10 @@ void launch_axis_transform(const double* in, double* out, int m0, int m1, int m2
   k_axis_transform<<<grid_for(6LL * m0 * m1 * m2), 256, 0, s>>>(in, out, m0, m1, m2, axis, Tcos, Tsin);
 }
 
-void launch_khat_finalize(const double* in, float* khat, const Dims& d, double scale, cudaStream_t s) {
+void launch_khat_finalize(const double* in, float* khat, const Dims& d, int kxoff, int kpitch, double scale,
+                          cudaStream_t s) {
   const int m0 = d.Lx / 2 + 1, m1 = d.Ly / 2 + 1, m2 = d.Lz / 2 + 1;
-  k_khat_finalize<<<grid_for(6LL * m0 * m1 * m2), 256, 0, s>>>(in, khat, m0, m1, m2, d.P, scale);
+  k_khat_finalize<<<grid_for(6LL * m0 * m1 * m2), 256, 0, s>>>(in, khat, m0, m1, m2, kxoff, kpitch, scale);
 }
 
 }  // namespace mcq

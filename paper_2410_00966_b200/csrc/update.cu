@@ -550,6 +550,9 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
         if (a.mode == MODE_FIELD) st_pair(a.bout, c * Nu + idx, bf2[c], vec, two);
         if (st) {
           st_pair(a.mOut, c * Nu + idx, o[c], vec, two);
+          // z-slab halos: remote stores into the neighbours' halo planes (P2P over NVLink)
+          if (a.halo_lo && z == 0) st_pair(a.halo_lo, c * Nu + (unsigned)nx * (y + (unsigned)ny * (nz + 1)) + x0, o[c], vec, two);
+          if (a.halo_hi && z == nz - 1) st_pair(a.halo_hi, c * Nu + (unsigned)nx * y + x0, o[c], vec, two);
           if (dp)
             st_pair(a.K + (size_t)(a.stage - 1) * 3 * Nu, c * Nu + idx, acc2[c], vec, two);  // k_s
           else if (a.stage < 4)
@@ -560,6 +563,8 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
 #pragma unroll
     for (int c = 0; c < 3; ++c) v[c][i] = o[c];
   }
+
+  if ((a.halo_lo && z == 0) || (a.halo_hi && z == nz - 1)) __threadfence_system();
 
   // ---------------- reductions ----------------
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (NT + 31) / 32;
@@ -738,46 +743,80 @@ __global__ void k_cav_prepare(CavParams p, CavState* st) {
   if (threadIdx.x == 0 && blockIdx.x == 0) cav_prepare(p, st);
 }
 
-// Fixed-order reduction of the per-CTA partials (deterministic), then per mode
-// alpha_{n+1} = e^{-(kappa + i w) dt} alpha_n + i (V_c/hbar) W_{n+1} dt; t += dt (a13).
-// partials: per slab [kNPart][nps] (slab-major, global CTA order i = slab * nps + b).
-constexpr int kCavThreads = 1024;
-__global__ void __launch_bounds__(kCavThreads) k_cavity(CavParams p, CavState* st, const double* __restrict__ partials,
-                                                        int n, int nps) {
-  __shared__ double red[kNPart][kCavThreads / 32];
-  pdl_trigger();
-  pdl_wait();
-  bool use[kNPart];  // the overlaps of the active modes; the spatial sums when the trace records
+// ---- overlap reduction, two fixed-order levels (SURVEY §8(e) "per-plane partials"):
+//   level 1, per z plane: the plane's K-U CTAs (nbx of them, consecutive in the slab's partial
+//     array [q][CTA], CTA = z * nbx + bx) summed by one warp — lane-strided, then a shuffle tree;
+//   level 2, K-CAV: the nzg plane sums [zg][q] summed in global z order the same way.
+// The tree depends only on nbx and nzg, never on the slab count, so W, alpha and every later
+// step are bitwise the same for any z decomposition, and under NCCL only the nzg x kNPart plane
+// sums cross the network (all-gather; 14 KB at 512 planes) instead of every CTA's partials.
+__device__ __forceinline__ double warp_sum_fixed(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// one warp: the plane sums of local plane zl of a slab's partials (nps = CTAs per slab)
+__device__ __forceinline__ void plane_sum(const double* __restrict__ part, int nps, int nbx, int zl, double* out,
+                                          int lane, const bool (&use)[kNPart]) {
+#pragma unroll
+  for (int q = 0; q < kNPart; ++q) {
+    double s = 0.0;
+    if (use[q])
+      for (int b = lane; b < nbx; b += 32) s += part[(size_t)q * nps + zl * nbx + b];
+    s = warp_sum_fixed(s);
+    if (lane == 0) out[q] = s;
+  }
+}
+
+__device__ __forceinline__ void cav_use(const CavParams& p, bool (&use)[kNPart]) {
 #pragma unroll
   for (int k = 0; k < kNPart; ++k) use[k] = k < kMaxModes ? k < p.nmodes : p.trace != nullptr;
-  double s[kNPart];
-#pragma unroll
-  for (int k = 0; k < kNPart; ++k) s[k] = 0.0;
-  for (int i = threadIdx.x; i < n; i += kCavThreads) {
-    const int r = n == nps ? 0 : i / nps, b = i - r * nps;
-    const double* pr = partials + (size_t)r * kNPart * nps + b;
-#pragma unroll
-    for (int k = 0; k < kNPart; ++k)
-      if (use[k]) s[k] += pr[(size_t)k * nps];
-  }
+}
+
+// NCCL mode, before the all-gather: this rank's plane sums psum[zl][q]
+__global__ void k_plane_sums(CavParams p, const double* __restrict__ partials, int nps, int nbx, int nzl,
+                             double* __restrict__ psum) {
+  bool use[kNPart];
+  cav_use(p, use);
+  const int lane = threadIdx.x & 31, warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int zl = warp; zl < nzl; zl += nw) plane_sum(partials, nps, nbx, zl, psum + (size_t)zl * kNPart, lane, use);
+}
+
+// Level 2 (and, unless psum_in is given, level 1 for all slabs held here), then per mode
+// alpha_{n+1} = e^{-(kappa + i w) dt} alpha_n + i (V_c/hbar) W_{n+1} dt; t += dt (a13).
+// partials: per slab [kNPart][nps] (slab-major); psum_in: gathered plane sums [nzg][kNPart].
+constexpr int kCavThreads = 1024;
+constexpr int kMaxPlanes = 512;
+__global__ void __launch_bounds__(kCavThreads) k_cavity(CavParams p, CavState* st, const double* __restrict__ partials,
+                                                        int nps, int nbx, int nzl, int nzg,
+                                                        const double* __restrict__ psum_in) {
+  __shared__ double ps[kMaxPlanes * kNPart];
+  __shared__ double tot[kNPart];
+  pdl_trigger();
+  pdl_wait();
+  bool use[kNPart];
+  cav_use(p, use);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int k = 0; k < kNPart; ++k) {
-    if (use[k]) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s[k] += __shfl_down_sync(0xffffffffu, s[k], o);
-      if (lane == 0) red[k][warp] = s[k];
+  if (psum_in) {
+    for (int i = threadIdx.x; i < nzg * kNPart; i += kCavThreads) ps[i] = psum_in[i];
+  } else {
+    for (int zg = warp; zg < nzg; zg += kCavThreads / 32) {
+      const int slab = zg / nzl, zl = zg - slab * nzl;
+      plane_sum(partials + (size_t)slab * kNPart * nps, nps, nbx, zl, ps + zg * kNPart, lane, use);
     }
   }
   __syncthreads();
+  if (warp < kNPart) {  // warp q: the plane sums of quantity q in z order
+    double s = 0.0;
+    if (use[warp])
+      for (int zg = lane; zg < nzg; zg += 32) s += ps[zg * kNPart + warp];
+    s = warp_sum_fixed(s);
+    if (lane == 0) tot[warp] = s;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    double tot[kNPart];
-#pragma unroll
-    for (int k = 0; k < kNPart; ++k) {
-      tot[k] = 0.0;
-      if (use[k])
-        for (int w = 0; w < kCavThreads / 32; ++w) tot[k] += red[k][w];
-    }
     for (int k = 0; k < p.nmodes; ++k) {
       const double W = p.cav_on[k] ? p.Ms * tot[k] : 0.0;
       const double er = p.ecn_re[k], ei = p.ecn_im[k];
@@ -809,8 +848,15 @@ __global__ void __launch_bounds__(kCavThreads) k_cavity(CavParams p, CavState* s
   }
 }
 
-void launch_cavity(const CavParams& p, CavState* st, const double* partials, int n, int nps, cudaStream_t s) {
-  launch_pdl(p.pdl, k_cavity, dim3(1), dim3(kCavThreads), 0, s, p, st, partials, n, nps);
+void launch_cavity(const CavParams& p, CavState* st, const double* partials, int nps, int nbx, int nzl, int nzg,
+                   const double* psum_in, cudaStream_t s) {
+  launch_pdl(p.pdl, k_cavity, dim3(1), dim3(kCavThreads), 0, s, p, st, partials, nps, nbx, nzl, nzg, psum_in);
+}
+
+void launch_plane_sums(const CavParams& p, const double* partials, int nps, int nbx, int nzl, double* psum,
+                       cudaStream_t s) {
+  const int warps = nzl < 32 ? nzl : 32;
+  k_plane_sums<<<1, 32 * warps, 0, s>>>(p, partials, nps, nbx, nzl, psum);
 }
 
 void launch_cav_prepare(const CavParams& p, CavState* st, cudaStream_t s) {

@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(Z2Cfg<L>::NT, Z2Cfg<L>::MINB) k_zconv2(float2*
   using Z = Z2Cfg<L>;
   constexpr int NCH = Z::NCH, E = Z::E, TL = Z::TL, C = Z::C, NT = Z::NT, TWP = Z::TWP, LINE = Z::LINE;
   constexpr int EN = 8 * NCH;  // slots that can carry inputs / outputs (z = t + 16 i < nz <= L/2)
-  extern __shared__ __align__(16) float2 sm[];
+  extern __shared__ __align__(128) float2 sm[];
   float2* twf = sm;                   // [ch][k][TWP]: w_L^{r (NCH k + ch)}
   float2* twi = sm + NCH * 16 * TWP;  // [ch][k][TWP]: w_L^{-k (NCH r + ch)}
   float2* buf = sm + Z::TWN;          // [component][channel][LINE]
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(Z2Cfg<L>::NT, Z2Cfg<L>::MINB) k_zconv2(float2*
   const int c = threadIdx.x % C, t = (threadIdx.x / C) % TL, ch = threadIdx.x / (C * TL);
   const int nz = d.nzg, nzl = d.nz, hy = d.Ly / 2;
   const unsigned row = d.KXS, plane = (unsigned)d.Ly * row, cstr = (unsigned)nzl * plane;
-  const unsigned kzs = (unsigned)(hy + 1) * d.P * 3;  // Khat stride between kz rows (float2 units)
+  const unsigned kzs = (unsigned)(hy + 1) * d.kpitch * 3;  // Khat stride between kz rows (float2 units)
   const float inv_nzl = 1.f / (float)nzl, inv_nkt = 1.f / (float)nkt;
   // (kxl, ky) of lane cc in a tile; j / nkt in fp32: (j + 1/2) / nkt is >= 1/(2 nkt) >= 1/128 from
   // an integer and carries < 34 000 * 6e-8 of rounding error, so the truncation is exact
@@ -159,8 +159,8 @@ __global__ void __launch_bounds__(Z2Cfg<L>::NT, Z2Cfg<L>::MINB) k_zconv2(float2*
 #pragma unroll 1
       for (int g = 0; g < 3; ++g)
         for (int z = threadIdx.x; z < nz; z += NT) prefetch_l2(py + g * cstr + zoff(z));
-      const float* pkh = khat + ((unsigned)pkyf * d.P + d.kx0 + pk) * 6;
-      const unsigned kstride = (unsigned)(hy + 1) * d.P * 6;
+      const float* pkh = khat + ((unsigned)pkyf * d.kpitch + d.kx0 - d.kxoff + pk) * 6;
+      const unsigned kstride = (unsigned)(hy + 1) * d.kpitch * 6;
       for (int j = threadIdx.x; j < (L / 2 + 1) * (3 * C / 16); j += NT) {  // C x 24 B = 3C/16 lines
         const int kzf = j / (3 * C / 16), q = j - kzf * (3 * C / 16);
         prefetch_l2(pkh + kzf * kstride + q * 32);
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(Z2Cfg<L>::NT, Z2Cfg<L>::MINB) k_zconv2(float2*
       const int kx = d.kx0 + kxl;
       const int kyf = ky <= hy ? ky : d.Ly - ky;
       const float sy = ky <= hy ? 1.f : -1.f;
-      const float2* kb = reinterpret_cast<const float2*>(khat) + ((unsigned)kyf * d.P + kx) * 3;
+      const float2* kb = reinterpret_cast<const float2*>(khat) + ((unsigned)kyf * d.kpitch + kx - d.kxoff) * 3;
       constexpr int KB = MCQ_Z2KB;
 #pragma unroll
       for (int b = 0; b < E; b += KB) {
