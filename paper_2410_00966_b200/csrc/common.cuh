@@ -198,13 +198,14 @@ struct UpdateArgs {
 void configure_pass_kernels();
 // (pass launchers return the number of kernels they launched: a narrow tail launch covers the
 // last kx columns beyond the final full column tile)
-int launch_yfwd(const Dims& d, const float2* X, float2* Y, const float2* tw, cudaStream_t s);
+// comp < 0: all three components in one launch; 0..2: that component only
+int launch_yfwd(const Dims& d, const float2* X, float2* Y, const float2* tw, cudaStream_t s, int comp = -1);
 int launch_zconv(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t s);
 int launch_zconv_seq(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t s);
 int zconv_tma_box_c(int Lz);  // kx columns per K-Z tile of the TMA-pipelined variant
 int launch_zconv_tma(const Dims& d, const void* tmap /* CUtensorMap over Y */, float2* Y, const float* khat,
                      const float2* tw, cudaStream_t s);
-int launch_yinv(const Dims& d, const float2* Y, float2* X, const float2* tw, cudaStream_t s);
+int launch_yinv(const Dims& d, const float2* Y, float2* X, const float2* tw, cudaStream_t s, int comp = -1);
 int launch_y2d(const Dims& d, float2* X, const float* khat, const float2* tw, cudaStream_t s);
 // update.cu
 void configure_update_kernels();

@@ -113,6 +113,8 @@ struct mcq_ctx {
   cudaStream_t stream = nullptr;  // work stream (user's or own)
   cudaStream_t own = nullptr;
   cudaStream_t cap = nullptr;     // capture stream
+  cudaStream_t side = nullptr;    // z-slab transposes, overlapped with the per-component y passes
+  cudaEvent_t ev[8] = {};         // fork / join events of the overlapped schedule
   std::vector<Slab> sl;
   float2* tw = nullptr;
   float* khat = nullptr;
@@ -372,37 +374,82 @@ struct Enq {
       nk(n->groupEnd());
     }
   }
-  // Y[q] of every slab r  <->  R[r] of slab q  (the z-slab <-> kx-slab transpose)
-  void alltoall(bool forward) {
+  // Y[q] of every slab r  <->  R[r] of slab q  (the z-slab <-> kx-slab transpose); comp < 0: the
+  // whole (source, destination) block, else that component's contiguous third of it; on stream st
+  void alltoall(bool forward, int comp = -1, cudaStream_t st = nullptr) {
+    if (!st) st = s;
     const Dims& d = c->sl[0].d;
-    const size_t blk = (size_t)3 * d.nz * d.Ly * d.KXS;  // complex per (source, destination) block
+    const size_t cb = (size_t)d.nz * d.Ly * d.KXS;  // complex per component of a block
+    const size_t blk = 3 * cb;                      // complex per (source, destination) block
+    const size_t off = comp < 0 ? 0 : comp * cb, len = comp < 0 ? blk : cb;
     if (c->mode == 1) {
       for (int r = 0; r < c->NS; ++r)
         for (int q = 0; q < c->NS; ++q) {
-          float2* y = c->sl[r].Y + q * blk;
-          float2* rr = c->sl[q].R + r * blk;
-          if (forward)
-            copy(rr, y, blk * sizeof(float2));
-          else
-            copy(y, rr, blk * sizeof(float2));
+          float2* y = c->sl[r].Y + q * blk + off;
+          float2* rr = c->sl[q].R + r * blk + off;
+          cudaError_t e = forward ? cudaMemcpyAsync(rr, y, len * sizeof(float2), cudaMemcpyDeviceToDevice, st)
+                                  : cudaMemcpyAsync(y, rr, len * sizeof(float2), cudaMemcpyDeviceToDevice, st);
+          if (e != cudaSuccess && rc == MCQ_OK) rc = fail(c, MCQ_ECUDA, "slab transpose copy");
         }
     } else {
       Nccl* n = nccl_api();
       Slab& sl = c->sl[0];
       nk(n->groupStart());
       for (int q = 0; q < c->NS; ++q) {
-        float2* y = sl.Y + q * blk;
-        float2* rr = sl.R + q * blk;
-        nk(n->send(forward ? (const void*)y : (const void*)rr, 2 * blk, ncclFloat, q, c->comm, s));
-        nk(n->recv(forward ? (void*)rr : (void*)y, 2 * blk, ncclFloat, q, c->comm, s));
+        float2* y = sl.Y + q * blk + off;
+        float2* rr = sl.R + q * blk + off;
+        nk(n->send(forward ? (const void*)y : (const void*)rr, 2 * len, ncclFloat, q, c->comm, st));
+        nk(n->recv(forward ? (void*)rr : (void*)y, 2 * len, ncclFloat, q, c->comm, st));
       }
       nk(n->groupEnd());
     }
   }
+  void record(int e, cudaStream_t st) {
+    if (cudaEventRecord(c->ev[e], st) != cudaSuccess && rc == MCQ_OK) rc = fail(c, MCQ_ECUDA, "event record");
+  }
+  void wait(cudaStream_t st, int e) {
+    if (cudaStreamWaitEvent(st, c->ev[e], 0) != cudaSuccess && rc == MCQ_OK) rc = fail(c, MCQ_ECUDA, "event wait");
+  }
   void demag() {
     const int NS = c->NS;
     const Dims& d0 = c->sl[0].d;
-    if (d0.nzg > 1) {
+    // z slabs, overlapped schedule: the y pass runs one component at a time and
+    // each component's transpose goes out on the side stream while the next one is transformed;
+    // after K-Z the transposes back come in component by component ahead of the inverse y pass
+    const bool ovl = NS > 1 && c->side && !pipeline_off();
+    if (d0.nzg > 1 && ovl) {
+      record(0, s);
+      wait(c->side, 0);  // fork: the side stream joins this stream (and an open graph capture)
+      for (int g = 0; g < 3; ++g) {
+        for (auto& sl : c->sl) {
+          pre(MCQ_K_YFWD);
+          const int n = launch_yfwd(sl.d, sl.X, sl.Y, c->tw, s, g);
+          post(MCQ_K_YFWD, n);
+        }
+        record(1 + g, s);
+        wait(c->side, 1 + g);
+        alltoall(true, g, c->side);
+      }
+      record(4, c->side);
+      wait(s, 4);
+      for (auto& sl : c->sl) {
+        pre(MCQ_K_ZCONV);
+        const int n = launch_zconv_seq(sl.d, sl.R, c->khat, c->tw, s);
+        post(MCQ_K_ZCONV, n);
+      }
+      record(5, s);
+      wait(c->side, 5);
+      for (int g = 0; g < 3; ++g) {
+        alltoall(false, g, c->side);
+        record(g == 0 ? 6 : (g == 1 ? 7 : 4), c->side);
+        wait(s, g == 0 ? 6 : (g == 1 ? 7 : 4));
+        for (auto& sl : c->sl) {
+          pre(MCQ_K_YINV);
+          const int n = launch_yinv(sl.d, sl.Y, sl.X, c->tw, s, g);
+          post(MCQ_K_YINV, n);
+        }
+      }
+    } else if (d0.nzg > 1) {
       for (auto& sl : c->sl) {
         pre(MCQ_K_YFWD);
         const int n = launch_yfwd(sl.d, sl.X, sl.Y, c->tw, s);
@@ -437,6 +484,10 @@ struct Enq {
         post(MCQ_K_Y2D, n);
       }
     }
+  }
+  static bool pipeline_off() {
+    static const char* e = getenv("MCQ_SLAB_SERIAL");  // comparison: the serial schedule
+    return e && e[0] == '1';
   }
   void update(const UpdateArgs& a) {
     pre(MCQ_K_UPDATE);
@@ -726,6 +777,9 @@ void free_all(mcq_ctx* c) {
   c->comm = nullptr;
   if (c->own) cudaStreamDestroy(c->own);
   if (c->cap) cudaStreamDestroy(c->cap);
+  if (c->side) cudaStreamDestroy(c->side);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
 }
 
 // TMA descriptor of Y[3][nz][Ly][P] viewed as a 3D tensor (P, Ly, 3 nz) of 8-byte elements;
@@ -902,6 +956,11 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
   if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess)
     return bail(MCQ_ECUDA);
+  if (c->mode != 0) {
+    if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess) return bail(MCQ_ECUDA);
+    for (auto& e : c->ev)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return bail(MCQ_ECUDA);
+  }
   c->stream = (dist && dist->cuda_stream) ? (cudaStream_t)dist->cuda_stream : c->own;
   if (c->mode == 2) {
     Nccl* n = nccl_api();

@@ -92,7 +92,8 @@ struct ColAddr {
 // owner arithmetic.  No integer division in the prologue (it was ~1/4 of a thread's work).
 template <int L, bool INV, bool SPLIT, int CW = 0>
 __global__ void __launch_bounds__(PassCfg<L, CW>::NT) k_ypass(const float2* __restrict__ in, float2* __restrict__ out,
-                                                              Dims d, const float2* __restrict__ gtw) {
+                                                              Dims d, const float2* __restrict__ gtw, int comp0,
+                                                              int ncomp) {
   using Cf = PassCfg<L, CW>;
   constexpr int E = Cf::E, TL = Cf::TL, C = Cf::C;
   extern __shared__ __align__(128) float2 sm[];
@@ -102,7 +103,9 @@ __global__ void __launch_bounds__(PassCfg<L, CW>::NT) k_ypass(const float2* __re
   __syncthreads();
   pdl_wait();
   const int c = threadIdx.x % C, t = threadIdx.x / C;
-  const int rest = blockIdx.y, comp = rest % 3, z = d.nz - 1 - rest / 3;
+  // components [comp0, comp0 + ncomp): all three in one launch, or one at a time when the slab
+  // transpose of each component overlaps the next component's pass (mcq.cu, Enq::demag)
+  const int rest = blockIdx.y, comp = comp0 + (ncomp == 3 ? rest % 3 : 0), z = d.nz - 1 - (ncomp == 3 ? rest / 3 : rest);
   const int kx = blockIdx.x * C + c;
   const bool ok = kx < d.NKX;
   const int nin = INV ? L : d.ny, nout = INV ? d.ny : L;
@@ -476,26 +479,27 @@ __global__ void __launch_bounds__(ZTCfg<L>::NT, MINB) k_zconv_tma(const __grid_c
 
 // (lone-column CTAs as in K-Z measured slower here: 38.9 / 37.8 vs 37.8 / 35.6 us)
 template <bool INV>
-static int launch_ypass(const Dims& d, const float2* in, float2* out, const float2* tw, cudaStream_t st) {
+static int launch_ypass(const Dims& d, const float2* in, float2* out, const float2* tw, int comp, cudaStream_t st) {
   int n = 0;
+  const int c0 = comp < 0 ? 0 : comp, nc = comp < 0 ? 3 : 1;
   MCQ_DISPATCH_L(d.Ly, {
     using Cf = PassCfg<L>;
-    const dim3 grid((d.NKX + Cf::C - 1) / Cf::C, 3 * d.nz);
+    const dim3 grid((d.NKX + Cf::C - 1) / Cf::C, nc * d.nz);
     if (d.NS > 1)
-      launch_pdl(d.pdl, k_ypass<L, INV, true>, grid, dim3(Cf::NT), Cf::SMEM, st, in, out, d, tw);
+      launch_pdl(d.pdl, k_ypass<L, INV, true>, grid, dim3(Cf::NT), Cf::SMEM, st, in, out, d, tw, c0, nc);
     else
-      launch_pdl(d.pdl, k_ypass<L, INV, false>, grid, dim3(Cf::NT), Cf::SMEM, st, in, out, d, tw);
+      launch_pdl(d.pdl, k_ypass<L, INV, false>, grid, dim3(Cf::NT), Cf::SMEM, st, in, out, d, tw, c0, nc);
     ++n;
   })
   return n;
 }
 
-int launch_yfwd(const Dims& d, const float2* X, float2* Y, const float2* tw, cudaStream_t st) {
-  return launch_ypass<false>(d, X, Y, tw, st);
+int launch_yfwd(const Dims& d, const float2* X, float2* Y, const float2* tw, cudaStream_t st, int comp) {
+  return launch_ypass<false>(d, X, Y, tw, comp, st);
 }
 
-int launch_yinv(const Dims& d, const float2* Y, float2* X, const float2* tw, cudaStream_t st) {
-  return launch_ypass<true>(d, Y, X, tw, st);
+int launch_yinv(const Dims& d, const float2* Y, float2* X, const float2* tw, cudaStream_t st, int comp) {
+  return launch_ypass<true>(d, Y, X, tw, comp, st);
 }
 
 int launch_zconv(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t st) {

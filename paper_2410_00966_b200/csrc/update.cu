@@ -73,11 +73,20 @@ __device__ __forceinline__ float3 ld3(const float* __restrict__ p, long long N, 
 }
 __device__ __forceinline__ float3 sm3(const float* p, int cs, int i) { return make_float3(p[i], p[cs + i], p[2 * cs + i]); }
 
+// shared-memory address of element pos of component-line l of row yl.  N2 >= 128 (one row per
+// warp): pos ^ ((pos >> 2) & 15) — every Stockham store (positions (b - k) R + k + r Ns) and load
+// (t + TL i) of the radix-4/2 row transforms takes 2 wavefronts per warp, the minimum for 256 B
+// (the 1-in-16 padding it replaces left 1/3 of the wavefronts as bank conflicts: round 1 ncu);
+// shorter rows (several per warp) keep the padding
+#ifndef MCQ_USWZ
+#define MCQ_USWZ 1  // XOR-swizzled row exchange buffer for N2 >= 128 (0: 1-in-16 padding)
+#endif
 template <int N2>
-struct RowAddr {  // shared-memory address of element pos of component-line l of row yl
+struct RowAddr {
   int yl;
   __device__ __forceinline__ int operator()(int l, int pos) const {
-    return (l * UCfg<N2>::RY + yl) * UCfg<N2>::PITCH + pos + (N2 >= 16 ? (pos >> 4) : 0);
+    if constexpr (MCQ_USWZ && N2 >= 128) return (l * UCfg<N2>::RY + yl) * UCfg<N2>::PITCH + (pos ^ ((pos >> 2) & 15));
+    else return (l * UCfg<N2>::RY + yl) * UCfg<N2>::PITCH + pos + (N2 >= 16 ? (pos >> 4) : 0);
   }
 };
 
