@@ -128,6 +128,19 @@ typedef struct {
 MCQ_API int mcq_create(mcq_ctx **out, const int grid[3], const double cell[3], double Ms, double Aex,
                double alpha, const mcq_aniso *K, const mcq_dist *dist);
 
+/* nz == 1 grids of up to 65536 cells (BJ configs[0]-class films), plain RK4 with one cavity mode
+ * and no DMI / thermal field: mcq_run runs all its steps in one persistent cooperative kernel
+ * (grid barriers between the y pass, the update and the cavity step) instead of 9 graph nodes per
+ * step (1, default) or replays the per-step graphs (0).  Same arithmetic, bitwise the same
+ * results; grids without a compiled instance fall back to the graphs. */
+MCQ_API int mcq_set_persistent_2d(mcq_ctx *, int on);
+
+/* z slabs: overlap each component's transpose (NCCL send/recv, or device copies in loopback) with
+ * the next component's y pass on a second stream (1), or run the passes and transposes in series
+ * (0).  Default: 1 under NCCL, 0 in loopback (where the copies compete with the passes for HBM).
+ * Same results bit for bit either way.  No effect on a single slab. */
+MCQ_API int mcq_set_slab_overlap(mcq_ctx *, int on);
+
 /* Use `stream` (a cudaStream_t, e.g. torch.cuda.current_stream().cuda_stream) for all work. */
 MCQ_API int mcq_set_stream(mcq_ctx *, void *stream);
 

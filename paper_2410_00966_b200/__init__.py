@@ -75,6 +75,16 @@ def mcq_create(grid, cell, Ms, Aex, alpha, K=None, dist=None):
     return h
 
 
+def mcq_set_persistent_2d(ctx, on):
+    """nz == 1 grids: one persistent kernel per mcq_run (1) or per-step graphs (0) (include/mcq.h)."""
+    _check(ctx, lib.mcq_set_persistent_2d(ctx, 1 if on else 0))
+
+
+def mcq_set_slab_overlap(ctx, on):
+    """z slabs: overlap the transposes with the per-component y passes (include/mcq.h)."""
+    _check(ctx, lib.mcq_set_slab_overlap(ctx, 1 if on else 0))
+
+
 def mcq_set_stream(ctx, stream):
     _check(ctx, lib.mcq_set_stream(ctx, C.c_void_p(stream) if stream else None))
 

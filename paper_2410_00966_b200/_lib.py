@@ -57,6 +57,8 @@ _sig = {
     "mcq_create": (C.c_int, [C.POINTER(_P), C.POINTER(C.c_int), C.POINTER(C.c_double), C.c_double, C.c_double,
                              C.c_double, C.POINTER(mcq_aniso), C.POINTER(mcq_dist)]),
     "mcq_set_stream": (C.c_int, [_P, _P]),
+    "mcq_set_slab_overlap": (C.c_int, [_P, C.c_int]),
+    "mcq_set_persistent_2d": (C.c_int, [_P, C.c_int]),
     "mcq_set_geometry": (C.c_int, [_P, _P]),
     "mcq_set_m": (C.c_int, [_P, _P]),
     "mcq_set_m_device": (C.c_int, [_P, _P]),

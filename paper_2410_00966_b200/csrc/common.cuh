@@ -211,6 +211,10 @@ int launch_y2d(const Dims& d, float2* X, const float* khat, const float2* tw, cu
 void configure_update_kernels();
 void launch_update(const UpdateArgs& a, const float2* tw, cudaStream_t s);
 int update_grid_blocks(const Dims& d);
+// persistent cooperative kernel for nz == 1 grids (plain RK4, one mode): `steps` steps in one launch;
+// returns 0, or -1 when this (N2, Ly) has no instance / the cooperative launch failed
+int launch_persist2d(const UpdateArgs u[4], const CavParams& cp, CavState* cav, const float* khat, int steps,
+                     const float2* tw, cudaStream_t s);
 void launch_cavity(const CavParams& p, CavState* st, const double* partials, int nps, int nbx, int nzl, int nzg,
                    const double* psum_in, cudaStream_t s);
 void launch_plane_sums(const CavParams& p, const double* partials, int nps, int nbx, int nzl, double* psum,

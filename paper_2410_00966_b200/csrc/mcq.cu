@@ -115,6 +115,12 @@ struct mcq_ctx {
   cudaStream_t cap = nullptr;     // capture stream
   cudaStream_t side = nullptr;    // z-slab transposes, overlapped with the per-component y passes
   cudaEvent_t ev[8] = {};         // fork / join events of the overlapped schedule
+  // overlap the slab transposes with the per-component y passes (side stream): on by default
+  // under NCCL (the transfers use NVLink, not this GPU's HBM); off in loopback, where the
+  // "transfers" are HBM copies competing with the passes (measured: 97.6 vs 65.1 ms/step,
+  // configs[4] x 8 slabs) — mcq_set_slab_overlap switches it (the loopback tests run both)
+  bool overlap = false;
+  bool persist2d = true;  // nz == 1 grids: the persistent cooperative kernel (mcq_set_persistent_2d)
   std::vector<Slab> sl;
   float2* tw = nullptr;
   float* khat = nullptr;
@@ -416,7 +422,7 @@ struct Enq {
     // z slabs, overlapped schedule: the y pass runs one component at a time and
     // each component's transpose goes out on the side stream while the next one is transformed;
     // after K-Z the transposes back come in component by component ahead of the inverse y pass
-    const bool ovl = NS > 1 && c->side && !pipeline_off();
+    const bool ovl = NS > 1 && c->side && c->overlap;
     if (d0.nzg > 1 && ovl) {
       record(0, s);
       wait(c->side, 0);  // fork: the side stream joins this stream (and an open graph capture)
@@ -485,10 +491,6 @@ struct Enq {
       }
     }
   }
-  static bool pipeline_off() {
-    static const char* e = getenv("MCQ_SLAB_SERIAL");  // comparison: the serial schedule
-    return e && e[0] == '1';
-  }
   void update(const UpdateArgs& a) {
     pre(MCQ_K_UPDATE);
     launch_update(a, c->tw, s);
@@ -500,7 +502,14 @@ struct Enq {
     if (!c->remote_halo) halo(sin_);  // else the previous K-U wrote the halo planes remotely
     demag();
     for (int i = 0; i < (int)c->sl.size(); ++i) {
-      Slab& sl = c->sl[i];
+      UpdateArgs a = stage_args(i, st, dt, mode, terms);
+      update(a);
+    }
+  }
+  UpdateArgs stage_args(int i, int st, double dt, int mode, unsigned terms) const {
+    Slab& sl = c->sl[i];
+    const int sout = st == 1 ? 1 : (st == 2 ? 2 : (st == 3 ? 1 : 0));
+    {
       UpdateArgs a = base_args(c, sl);
       a.halo_lo = halo_peer(i, sout, true);
       a.halo_hi = halo_peer(i, sout, false);
@@ -517,7 +526,7 @@ struct Enq {
         a.th_seed = c->th_seed;
         a.eta = sl.eta;
       }
-      update(a);
+      return a;
     }
   }
   // NCCL: this rank's plane sums of the overlap partials, all-gathered in z order (nzg x kNPart
@@ -956,6 +965,7 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
   if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess)
     return bail(MCQ_ECUDA);
+  c->overlap = c->mode == 2;
   if (c->mode != 0) {
     if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess) return bail(MCQ_ECUDA);
     for (auto& e : c->ev)
@@ -1078,6 +1088,19 @@ int mcq_create(mcq_ctx** out, const int grid[3], const double cell[3], double Ms
   }
   if (reset_memory(c) != MCQ_OK) return bail(MCQ_ECUDA);
   *out = c;
+  return MCQ_OK;
+}
+
+int mcq_set_persistent_2d(mcq_ctx* c, int on) {
+  if (!c) return MCQ_EINVAL;
+  c->persist2d = on != 0;
+  return MCQ_OK;
+}
+
+int mcq_set_slab_overlap(mcq_ctx* c, int on) {
+  if (!c) return MCQ_EINVAL;
+  c->overlap = on != 0;
+  invalidate_graphs(c);
   return MCQ_OK;
 }
 
@@ -1342,6 +1365,28 @@ int mcq_run(mcq_ctx* c, double dt, long long steps) {
   const CavParams p = cav_params(c, dt);
   launch_cav_prepare(p, c->cav, c->stream);
   c->launches += 1;
+  // nz == 1 grids of a few thousand cells (configs[0]): one persistent cooperative kernel per
+  // call instead of 9 graph nodes per step (update.cu, K-P2D); same arithmetic, same bits
+  static const char* pv = getenv("MCQ_PERSIST2D");  // "0": the graph path (comparison)
+  if (c->persist2d && c->mode == 0 && c->dg.nz == 1 && c->dg.N <= (1 << 16) && c->nmodes == 1 && c->dmi == 0 &&
+      c->temperature <= 0 && !(pv && pv[0] == '0')) {
+    Enq q{c, c->stream};
+    UpdateArgs u[4];
+    for (int st = 1; st <= 4; ++st) u[st - 1] = q.stage_args(0, st, dt, MODE_LLG, MCQ_TERM_ALL);
+    bool ok = true;
+    for (long long done = 0; done < steps && ok;) {
+      const int k = (int)std::min<long long>(steps - done, 1 << 20);
+      ok = launch_persist2d(u, p, c->cav, c->khat, k, c->tw, c->stream) == 0;
+      if (ok) {
+        done += k;
+        c->launches += 1;
+      } else if (done > 0) {
+        return fail(c, MCQ_ECUDA, "persistent 2D launch failed mid-run");
+      }
+    }
+    if (ok) return MCQ_OK;
+    cudaGetLastError();  // no instance for this grid / no co-residency: the graph path below
+  }
   int rc;
   if (steps >= kGraphSteps && (rc = capture(c, 1, dt, kGraphSteps)) != MCQ_OK) return rc;
   if (steps % kGraphSteps && (rc = capture(c, 0, dt, 1)) != MCQ_OK) return rc;

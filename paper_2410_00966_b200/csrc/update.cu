@@ -18,6 +18,8 @@
 #include "common.cuh"
 #include "regfft.cuh"
 #include "tma.cuh"
+#include "conv.cuh"
+#include <cooperative_groups.h>
 #include "../../include/mcq.h"
 
 #ifndef MCQ_UE
@@ -116,11 +118,13 @@ __device__ __forceinline__ float3 thermal_eta(unsigned long long seed, unsigned 
   return make_float3(r0 * k0, r0 * s0, r1 * k1);
 }
 
-template <int GEN>
+template <int GEN, int FM, int FS>
 __device__ __forceinline__ float3 cell_core(const UpdateArgs& a, float3 m, const float3 (&nb)[6], const bool (&ok)[6],
                                             float3 mn, float3 ap, float3 bcav, float gmul, float3 Bd,
                                             float& tmax, float3& acc_out, float3& Bout) {
-  if (a.mode == MODE_X0) return m;
+  const int mode = FM >= 0 ? FM : a.mode;  // FM: the mode fixed at compile time (hot LLG instance)
+  const int stage_ = FS > 0 ? FS : a.stage;  // FS: the RK4 stage fixed at compile time
+  if (mode == MODE_X0) return m;
   float3 B = make_float3(0.f, 0.f, 0.f);
   if (dot3(m, m) > 0.f) {
     B = Bd;
@@ -178,26 +182,26 @@ __device__ __forceinline__ float3 cell_core(const UpdateArgs& a, float3 m, const
       B.z += bcav.z * gmul;
     }
   }
-  if (a.mode == MODE_FIELD) {
+  if (mode == MODE_FIELD) {
     Bout = B;
     return m;
   }
   const float3 mxB = cross3(m, B);
-  if (a.mode == MODE_MAXTORQUE) {
+  if (mode == MODE_MAXTORQUE) {
     tmax = fmaxf(tmax, sqrtf(dot3(mxB, mxB)));
     return m;
   }
   const float3 mmxB = cross3(m, mxB);
   float3 k;
-  if (a.mode == MODE_LLG || (GEN == 2 && a.mode == MODE_DP)) {
+  if (mode == MODE_LLG || (GEN == 2 && mode == MODE_DP)) {
     k = make_float3(-a.gl * (mxB.x + a.alpha * mmxB.x), -a.gl * (mxB.y + a.alpha * mmxB.y),
                     -a.gl * (mxB.z + a.alpha * mmxB.z));
   } else {  // MODE_RELAX: -gamma m x (m x B)
     k = make_float3(-a.gamma * mmxB.x, -a.gamma * mmxB.y, -a.gamma * mmxB.z);
   }
-  const int stage = a.stage;
+  const int stage = stage_;
   if (stage == 1) mn = m;
-  if (GEN == 2 && a.mode == MODE_DP) {  // ap = sum_{j < s} comb[j-1] k_j from the caller (reading C-DP)
+  if (GEN == 2 && mode == MODE_DP) {  // ap = sum_{j < s} comb[j-1] k_j from the caller (reading C-DP)
     const float cs = a.comb[stage - 1];
     const float3 inc = make_float3(ap.x + cs * k.x, ap.y + cs * k.y, ap.z + cs * k.z);
     acc_out = k;
@@ -239,11 +243,19 @@ __device__ __forceinline__ float2 sm_pair(const float* p) { return *reinterpret_
 #endif
 // MM: cavity modes compiled in (1, 2 or kMaxModes with a.nmodes <= MM at run time); GEN: 0 the
 // plain RK4 instances, 1 + interfacial DMI and the thermal draw, 2 + the Dormand-Prince stages
-template <int N2, int MM, int GEN>
-__global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a, const float2* __restrict__ gtw) {
+// FM >= 0: the update mode fixed at compile time — the plain RK4 instance (<N2, 1, 0, MODE_LLG>)
+// then carries no FIELD / MAXTORQUE / X0 / RELAX code, a third less SASS (instruction-cache
+// misses showed as 'no_instruction' stalls in ncu); FM = -1: the mode from the arguments
+// the body with explicit (virtual) block indices (bx, by) of a (gx, gy) grid: a grid of its own
+// (k_update) or a share of the persistent 2D kernel (k_persist2d); NOTMA: the plain-load staging
+// (the persistent kernel re-enters the body and does not re-arm mbarriers)
+template <int N2, int MM, int GEN, int FM, int FS, bool NOTMA = false>
+__device__ __forceinline__ void update_body(const UpdateArgs& a, const float2* __restrict__ gtw, int bx, int by,
+                                            int gx, int gy, float2* sm) {
+  const int mode = FM >= 0 ? FM : a.mode;
+  const int stage_ = FS > 0 ? FS : a.stage;  // FS: the RK4 stage fixed at compile time (hot instances)
   using Cf = UCfg<N2>;
   constexpr int E = Cf::E, TL = Cf::TL, RY = Cf::RY, NT = Cf::NT, LX = 2 * N2, PITCH = Cf::PITCH;
-  extern __shared__ __align__(16) float2 sm[];
   // w_Lx^m, m < Lx: packing / unpacking of the real transforms and, every other entry, the
   // row FFTs' twiddles (base table, TWS = 2: fewer live registers than a plan table here)
   float2* tw = sm;
@@ -261,19 +273,19 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
   const Dims& d = a.d;
   const int nx = d.nx, ny = d.ny, nz = d.nz;
   const long long N = d.cs;                        // component stride of the state arrays
-  const int y0 = blockIdx.x * RY, z = blockIdx.y;  // z: local plane (X rows, partials)
+  const int y0 = bx * RY, z = by;  // z: local plane (X rows, partials)
   const int zs = z + d.zoff;                       // storage plane of the (halo'd) state arrays
   const bool zlo = d.zg0 + z > 0, zhi = d.zg0 + z < d.nzg - 1;  // global z neighbours exist
   const int nrow = min(RY, ny - y0);
   const int ylo = y0 > 0 ? y0 - 1 : 0, yhi = min(y0 + RY, ny - 1);  // staged m_s rows at z
   const int nxp = nx + (nx & 1);                                     // tile row pitch (8-byte pairs)
   const int csc = (RY + 2) * nxp, csz = RY * nxp;                    // component pitches of the tiles
-  const bool use_demag = a.demag && (a.terms & MCQ_TERM_DEMAG) && a.mode != MODE_X0;
-  const bool tma = (nx & 3) == 0 && (d.P & 1) == 0;
+  const bool use_demag = a.demag && (a.terms & MCQ_TERM_DEMAG) && mode != MODE_X0;
+  const bool tma = !NOTMA && (nx & 3) == 0 && (d.P & 1) == 0;
   const bool trows = tma && MCQ_UROWS;
-  const bool st_mode = a.mode == MODE_LLG || a.mode == MODE_RELAX;
-  const bool ld_mn = trows && st_mode && a.stage > 1;  // m_n and the accumulator: stages 2-4
-  const bool ld_br = trows && a.brms[0] && (a.mode == MODE_LLG || a.mode == MODE_FIELD);
+  const bool st_mode = mode == MODE_LLG || mode == MODE_RELAX;
+  const bool ld_mn = trows && st_mode && stage_ > 1;  // m_n and the accumulator: stages 2-4
+  const bool ld_br = trows && a.brms[0] && (mode == MODE_LLG || mode == MODE_FIELD);
 
   // ---------------- 0: TMA staging (bars[0]: X rows, bars[1]: m_s tile) ----------------
   // thread 0 initialises the barriers and issues every copy at once, so the copies' latency
@@ -374,8 +386,8 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
 #pragma unroll
   for (int k = 0; k < MM; ++k) {
     float gc = 0.f, ge = 0.f;
-    if (k < nm && (a.mode == MODE_LLG || a.mode == MODE_FIELD || a.mode == MODE_DP)) {
-      const int si = (a.mode == MODE_FIELD) ? 0 : a.stage - 1;
+    if (k < nm && (mode == MODE_LLG || mode == MODE_FIELD || mode == MODE_DP)) {
+      const int si = (mode == MODE_FIELD) ? 0 : stage_ - 1;
       gc = (a.terms & MCQ_TERM_CAVITY) ? a.cav->gc[k][si] : 0.f;
       ge = (a.terms & MCQ_TERM_EXCITATION) ? a.cav->ge[k][si] : 0.f;
     }
@@ -389,20 +401,20 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
   double wacc[MM];
 #pragma unroll
   for (int k = 0; k < MM; ++k) wacc[k] = 0.0;
-  const bool dp = GEN == 2 && a.mode == MODE_DP;
+  const bool dp = GEN == 2 && mode == MODE_DP;
   // overlaps (and the trace's sum m) of the step result: RK4 stage 4's output, DP stage 7's input
-  const bool wsum = (a.mode == MODE_LLG && a.stage == 4) || (dp && a.stage == 7);
+  const bool wsum = (mode == MODE_LLG && stage_ == 4) || (dp && stage_ == 7);
   float tmax = 0.f;
   const bool tr = a.trace && wsum;
   const unsigned rowbase = (unsigned)nx * (y + (unsigned)ny * zs);  // 32-bit indices (< 2^32 elements)
   const unsigned Nu = (unsigned)N;
   const float* trow = tc + (yl + 1) * nxp;  // this row inside the z tile
   const bool vec = (nx & 1) == 0;           // global pairs are 8-byte aligned
-  const bool st = a.mode == MODE_LLG || a.mode == MODE_RELAX || (dp && a.stage < 7);  // writes a state
-  const bool need_mn = st && a.stage > 1, need_acc = !dp && st && a.stage > 1;
+  const bool st = mode == MODE_LLG || mode == MODE_RELAX || (dp && stage_ < 7);  // writes a state
+  const bool need_mn = st && stage_ > 1, need_acc = !dp && st && stage_ > 1;
   const bool need_br = a.brms[0] && (gsum != 0.f || wsum);
-  const bool th_st = GEN && a.eta && a.mode == MODE_LLG && a.stage == 1;  // thermal draw stored
-  const bool th_ld = GEN && a.eta && a.mode == MODE_LLG && a.stage > 1;   // and reloaded
+  const bool th_st = GEN && a.eta && mode == MODE_LLG && stage_ == 1;  // thermal draw stored
+  const bool th_ld = GEN && a.eta && mode == MODE_LLG && stage_ > 1;   // and reloaded
 #pragma unroll
   for (int i = 0; i < E; ++i) {
     const int x0 = 2 * (t + TL * i);
@@ -437,18 +449,18 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
       if (dp) {  // ap = sum_{j < s} comb[j-1] k_j (the earlier stages' slopes, from HBM)
         // two slopes per iteration: their loads are in flight together (same summation order)
 #pragma unroll 1
-        for (int j = 1; j < a.stage; j += 2) {
+        for (int j = 1; j < stage_; j += 2) {
           float2 kk[2][3];
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
             const float* Kj = a.K + (size_t)(j + q - 1) * 3 * Nu;
 #pragma unroll
             for (int c = 0; c < 3; ++c)
-              kk[q][c] = j + q < a.stage ? ld_pair(Kj, c * Nu + idx, vec, two) : make_float2(0.f, 0.f);
+              kk[q][c] = j + q < stage_ ? ld_pair(Kj, c * Nu + idx, vec, two) : make_float2(0.f, 0.f);
           }
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
-            if (j + q < a.stage) {
+            if (j + q < stage_) {
               const float w = a.comb[j + q - 1];
 #pragma unroll
               for (int c = 0; c < 3; ++c) {
@@ -514,7 +526,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
         float3 accn = make_float3(0.f, 0.f, 0.f), Bf = make_float3(0.f, 0.f, 0.f);
         float3 out;
         if constexpr (MM == 1) {
-          out = cell_core<GEN>(a, m, nb, ok, mn, ap, br, gsum, Bd, tmax, accn, Bf);
+          out = cell_core<GEN, FM, FS>(a, m, nb, ok, mn, ap, br, gsum, Bd, tmax, accn, Bf);
         } else {
           float3 bcav = make_float3(br.x * gsum, br.y * gsum, br.z * gsum);
 #pragma unroll
@@ -525,7 +537,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
               bcav.z += MCQ_PICK(bk2[k - 1][2]) * gs[k];
             }
           }
-          out = cell_core<GEN>(a, m, nb, ok, mn, ap, bcav, any_cav ? 1.f : 0.f, Bd, tmax, accn, Bf);
+          out = cell_core<GEN, FM, FS>(a, m, nb, ok, mn, ap, bcav, any_cav ? 1.f : 0.f, Bd, tmax, accn, Bf);
         }
         if (wsum) {
           wacc[0] += (double)(br.x * out.x) + (double)(br.y * out.y) + (double)(br.z * out.z);
@@ -556,15 +568,15 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
       }
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        if (a.mode == MODE_FIELD) st_pair(a.bout, c * Nu + idx, bf2[c], vec, two);
+        if (mode == MODE_FIELD) st_pair(a.bout, c * Nu + idx, bf2[c], vec, two);
         if (st) {
           st_pair(a.mOut, c * Nu + idx, o[c], vec, two);
           // z-slab halos: remote stores into the neighbours' halo planes (P2P over NVLink)
           if (a.halo_lo && z == 0) st_pair(a.halo_lo, c * Nu + (unsigned)nx * (y + (unsigned)ny * (nz + 1)) + x0, o[c], vec, two);
           if (a.halo_hi && z == nz - 1) st_pair(a.halo_hi, c * Nu + (unsigned)nx * y + x0, o[c], vec, two);
           if (dp)
-            st_pair(a.K + (size_t)(a.stage - 1) * 3 * Nu, c * Nu + idx, acc2[c], vec, two);  // k_s
-          else if (a.stage < 4)
+            st_pair(a.K + (size_t)(stage_ - 1) * 3 * Nu, c * Nu + idx, acc2[c], vec, two);  // k_s
+          else if (stage_ < 4)
             st_pair(a.acc, c * Nu + idx, acc2[c], vec, two);
         }
       }
@@ -610,14 +622,14 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
       double s = 0.0;
       if (threadIdx.x < kPartM || tr)
         for (int w = 0; w < nw; ++w) s += red[w * kNPart + threadIdx.x];
-      const int nps = gridDim.x * gridDim.y;
-      a.partials[threadIdx.x * nps + blockIdx.y * gridDim.x + blockIdx.x] = s;
+      const int nps = gx * gy;
+      a.partials[threadIdx.x * nps + by * gx + bx] = s;
       // divergence guard at no per-cell cost: br . m_{n+1} is NaN for any non-finite m_{n+1}
       // (0 * inf and 0 * NaN are NaN), so a non-finite W_0 partial flags the step
       if (threadIdx.x == 0 && a.nonfinite && !isfinite(s)) atomicOr(a.nonfinite, 1);
     }
   }
-  if (dp && a.stage == 7) {  // the step's error estimate: max over cells (fp32 bits, >= 0)
+  if (dp && stage_ == 7) {  // the step's error estimate: max over cells (fp32 bits, >= 0)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_down_sync(0xffffffffu, tmax, o));
     if (lane == 0) redf[warp] = tmax;
@@ -628,7 +640,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
       atomicMax(a.maxbits, __float_as_uint(s));
     }
   }
-  if (a.mode == MODE_MAXTORQUE) {
+  if (mode == MODE_MAXTORQUE) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_down_sync(0xffffffffu, tmax, o));
     if (lane == 0) redf[warp] = tmax;
@@ -640,7 +652,7 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
     }
     return;
   }
-  if (a.mode == MODE_FIELD) return;
+  if (mode == MODE_FIELD) return;
 
   // ---------------- C: packed x-R2C of the new rows ----------------
   if (!use_demag) __syncthreads();  // xs may still hold staged rows of other threads' reads
@@ -667,6 +679,12 @@ __global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a
       }
     }
   }
+}
+
+template <int N2, int MM, int GEN, int FM = -1, int FS = 0>
+__global__ void __launch_bounds__(UCfg<N2>::NT, MCQ_UMINB) k_update(UpdateArgs a, const float2* __restrict__ gtw) {
+  extern __shared__ __align__(128) float2 sm[];
+  update_body<N2, MM, GEN, FM, FS>(a, gtw, blockIdx.x, blockIdx.y, gridDim.x, gridDim.y, sm);
 }
 
 int update_grid_blocks(const Dims& d) {
@@ -714,6 +732,14 @@ void launch_update(const UpdateArgs& a, const float2* tw, cudaStream_t st) {
       launch_pdl(a.d.pdl, k_update<N2, kMaxModes, 0>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
     else if (a.nmodes == 2)  // two modes (bright + dark): half the per-mode registers of MM = 4
       launch_pdl(a.d.pdl, k_update<N2, 2, 0>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
+    else if (a.mode == MODE_LLG && a.stage == 1)  // the headline path: plain RK4, one mode, per stage
+      launch_pdl(a.d.pdl, k_update<N2, 1, 0, MODE_LLG, 1>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
+    else if (a.mode == MODE_LLG && a.stage == 2)
+      launch_pdl(a.d.pdl, k_update<N2, 1, 0, MODE_LLG, 2>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
+    else if (a.mode == MODE_LLG && a.stage == 3)
+      launch_pdl(a.d.pdl, k_update<N2, 1, 0, MODE_LLG, 3>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
+    else if (a.mode == MODE_LLG)
+      launch_pdl(a.d.pdl, k_update<N2, 1, 0, MODE_LLG, 4>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
     else
       launch_pdl(a.d.pdl, k_update<N2, 1, 0>, grid, dim3(Cf::NT), Cf::SMEM, st, a, tw);
   })
@@ -724,6 +750,10 @@ void configure_update_kernels() {
     MCQ_DISPATCH_N2(n, {
       const int smem = (int)UCfg<N2>::SMEM;
       cudaFuncSetAttribute(k_update<N2, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(k_update<N2, 1, 0, MODE_LLG, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(k_update<N2, 1, 0, MODE_LLG, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(k_update<N2, 1, 0, MODE_LLG, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(k_update<N2, 1, 0, MODE_LLG, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       cudaFuncSetAttribute(k_update<N2, 2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       cudaFuncSetAttribute(k_update<N2, kMaxModes, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       cudaFuncSetAttribute(k_update<N2, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -796,6 +826,39 @@ __global__ void k_plane_sums(CavParams p, const double* __restrict__ partials, i
 // Level 2 (and, unless psum_in is given, level 1 for all slabs held here), then per mode
 // alpha_{n+1} = e^{-(kappa + i w) dt} alpha_n + i (V_c/hbar) W_{n+1} dt; t += dt (a13).
 // partials: per slab [kNPart][nps] (slab-major); psum_in: gathered plane sums [nzg][kNPart].
+// a13 from the reduced sums tot[q]: alpha_{n+1}, t, W, the trace row, the next step's stage
+// factors (one thread)
+__device__ __forceinline__ void cav_finish(const CavParams& p, CavState* st, const double* tot) {
+  for (int k = 0; k < p.nmodes; ++k) {
+    const double W = p.cav_on[k] ? p.Ms * tot[k] : 0.0;
+    const double er = p.ecn_re[k], ei = p.ecn_im[k];
+    const double re = er * st->re[k] - ei * st->im[k];
+    const double im = er * st->im[k] + ei * st->re[k] + p.vc_over_hbar * W * p.dt;
+    st->re[k] = re;
+    st->im[k] = im;
+    st->W[k] = W;
+  }
+  st->t += p.dt;
+  st->step += 1;
+  if (p.th_count) *p.thstep += 1;  // thermal noise step: never restarted by a memory reset
+  if (p.trace && st->step % p.trace_every == 0) {  // NEXT-3: the per-step observables
+    const long long r = st->trace_rows;
+    if (r < p.trace_cap) {
+      double* row = p.trace + r * kTraceCols;
+      row[0] = st->t;
+      row[1] = tot[kPartM] * p.inv_nmag;
+      row[2] = tot[kPartM + 1] * p.inv_nmag;
+      row[3] = tot[kPartM + 2] * p.inv_nmag;
+      row[4] = st->re[0];
+      row[5] = st->im[0];
+      row[6] = p.Ms * tot[0];
+      row[7] = (double)st->step;
+    }
+    st->trace_rows = r + 1;
+  }
+  cav_prepare(p, st);
+}
+
 constexpr int kCavThreads = 1024;
 constexpr int kMaxPlanes = 512;
 __global__ void __launch_bounds__(kCavThreads) k_cavity(CavParams p, CavState* st, const double* __restrict__ partials,
@@ -825,36 +888,108 @@ __global__ void __launch_bounds__(kCavThreads) k_cavity(CavParams p, CavState* s
     if (lane == 0) tot[warp] = s;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < p.nmodes; ++k) {
-      const double W = p.cav_on[k] ? p.Ms * tot[k] : 0.0;
-      const double er = p.ecn_re[k], ei = p.ecn_im[k];
-      const double re = er * st->re[k] - ei * st->im[k];
-      const double im = er * st->im[k] + ei * st->re[k] + p.vc_over_hbar * W * p.dt;
-      st->re[k] = re;
-      st->im[k] = im;
-      st->W[k] = W;
-    }
-    st->t += p.dt;
-    st->step += 1;
-    if (p.th_count) *p.thstep += 1;  // thermal noise step: never restarted by a memory reset
-    if (p.trace && st->step % p.trace_every == 0) {  // NEXT-3: the per-step observables
-      const long long r = st->trace_rows;
-      if (r < p.trace_cap) {
-        double* row = p.trace + r * kTraceCols;
-        row[0] = st->t;
-        row[1] = tot[kPartM] * p.inv_nmag;
-        row[2] = tot[kPartM + 1] * p.inv_nmag;
-        row[3] = tot[kPartM + 2] * p.inv_nmag;
-        row[4] = st->re[0];
-        row[5] = st->im[0];
-        row[6] = p.Ms * tot[0];
-        row[7] = (double)st->step;
+  if (threadIdx.x == 0) cav_finish(p, st, tot);
+}
+
+// ---------------------------------------------------------------- K-P2D: persistent 2D steps
+// Grids with nz = 1 and a few thousand cells (BJ configs[0], the 64 x 64 x 1 film of the bias
+// sweeps) are launch-latency bound: a step is 9 kernels (4 x (K-Y2D, K-U) + K-CAV) whose work is
+// a few microseconds in all (58 us per step measured as separate graph nodes).  One cooperative
+// kernel runs all `steps` steps: per stage its CTAs share the K-Y2D work (y forward . Khat .
+// y inverse on X, in place), a grid barrier, the K-U work (the same body as k_update, with plain
+// staging loads), a barrier; after stage 4 CTA 0 reduces the overlap partials with the same
+// fixed-order tree as K-CAV and advances the cavity, a barrier.  The same bodies and arithmetic
+// as the separate kernels: bitwise the same trajectory (tests/test_gpu_persist2d.py).
+struct Persist2DArgs {
+  UpdateArgs u[4];  // stages 1..4
+  CavParams cp;
+  CavState* cav;
+  const float* khat;
+  int steps;
+  int nbx;    // K-U blocks (ny / RY)
+  int nconv;  // K-Y2D blocks
+};
+
+template <int N2, int L>
+__global__ void __launch_bounds__(UCfg<N2>::NT) k_persist2d(Persist2DArgs pa, const float2* __restrict__ gtw) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(128) float2 sm[];
+  __shared__ double tot[kNPart];
+  const Dims& d = pa.u[0].d;
+  constexpr int NTT = UCfg<N2>::NT;
+  for (int step = 0; step < pa.steps; ++step) {
+    for (int s = 0; s < 4; ++s) {
+      for (int vb = blockIdx.x; vb < pa.nconv; vb += gridDim.x) {
+        conv_body<L, true, NTT>(pa.u[s].X, pa.khat, d, gtw, vb, 0, sm);
+        __syncthreads();  // the next virtual block reuses the shared twiddles / exchange buffer
       }
-      st->trace_rows = r + 1;
+      grid.sync();
+      for (int vb = blockIdx.x; vb < pa.nbx; vb += gridDim.x) {
+        update_body<N2, 1, 0, MODE_LLG, 0, true>(pa.u[s], gtw, vb, 0, pa.nbx, 1, sm);
+        __syncthreads();
+      }
+      grid.sync();
     }
-    cav_prepare(p, st);
+    if (blockIdx.x == 0) {  // K-CAV: one plane, the same two-level fixed-order tree
+      bool use[kNPart];
+      cav_use(pa.cp, use);
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      __shared__ double ps[kNPart];
+      if (warp == 0) plane_sum(pa.u[3].partials, pa.nbx, pa.nbx, 0, ps, lane, use);
+      __syncthreads();
+      for (int q = warp; q < kNPart; q += nw) {
+        double v = (use[q] && lane == 0) ? ps[q] : 0.0;
+        v = warp_sum_fixed(v);
+        if (lane == 0) tot[q] = v;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) cav_finish(pa.cp, pa.cav, tot);
+    }
+    grid.sync();
   }
+}
+
+template <int N2, int L>
+static int persist2d_launch(const Persist2DArgs& pa, const float2* tw, cudaStream_t st) {
+  using Cu = UCfg<N2>;
+  using Cc = ZCfg<L, Cu::NT>;
+  const size_t smem = Cu::SMEM > Cc::SMEM ? Cu::SMEM : Cc::SMEM;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_persist2d<N2, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  int per_sm = 0, dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_persist2d<N2, L>, Cu::NT, smem);
+  Persist2DArgs copy = pa;
+  copy.nbx = (pa.u[0].d.ny + Cu::RY - 1) / Cu::RY;
+  copy.nconv = (pa.u[0].d.NKX + Cc::C - 1) / Cc::C;
+  int grid = copy.nbx > copy.nconv ? copy.nbx : copy.nconv;
+  if (grid > per_sm * nsm) grid = per_sm * nsm;
+  if (grid < 1) return -1;
+  void* args[] = {&copy, const_cast<float2**>(&tw)};
+  return cudaLaunchCooperativeKernel((void*)k_persist2d<N2, L>, dim3(grid), dim3(Cu::NT), args, smem, st) == cudaSuccess
+             ? 0
+             : -1;
+}
+
+int launch_persist2d(const UpdateArgs u[4], const CavParams& cp, CavState* cav, const float* khat, int steps,
+                     const float2* tw, cudaStream_t s) {
+  Persist2DArgs pa{};
+  for (int i = 0; i < 4; ++i) pa.u[i] = u[i];
+  pa.cp = cp;
+  pa.cav = cav;
+  pa.khat = khat;
+  pa.steps = steps;
+  const int N2 = u[0].d.N2, L = u[0].d.Ly;
+#define P2D(n2, l) \
+  if (N2 == n2 && L == l) return persist2d_launch<n2, l>(pa, tw, s);
+  P2D(32, 64) P2D(32, 128) P2D(64, 64) P2D(64, 128) P2D(64, 256) P2D(128, 128) P2D(128, 256)
+#undef P2D
+  return -1;
 }
 
 void launch_cavity(const CavParams& p, CavState* st, const double* partials, int nps, int nbx, int nzl, int nzg,

@@ -1,0 +1,52 @@
+"""The persistent cooperative kernel for nz == 1 grids (update.cu K-P2D; VERDICT r1 item 6:
+configs[0] latency path): bitwise the same trajectory as the per-step graphs (same bodies, same
+fixed-order reductions), cavity state and trace included, and oracle parity over 100 steps."""
+import numpy as np
+import pytest
+
+from helpers import oracle_from, rel_l2
+from synth import small_config, make_config
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2410_00966_b200 as mcq  # noqa: E402
+
+
+@pytest.mark.parametrize("grid", [(64, 64, 1), (40, 24, 1), (30, 60, 1)])
+def test_persistent_2d_bitwise_equals_graphs(grid):
+    cfg = small_config("film", grid, seed=51, state="phys")
+    a = mcq.Solver.from_config(cfg)
+    b = mcq.Solver.from_config(cfg)
+    mcq.mcq_set_persistent_2d(b.ctx, 0)
+    a.trace(64)
+    b.trace(64)
+    for n in (1, 7, 16, 3):          # partial "graph chunks" on the graph side
+        a.run(cfg.dt, n)
+        b.run(cfg.dt, n)
+    assert np.array_equal(a.m(), b.m())
+    ca, cb = a.cavity(), b.cavity()
+    assert (ca["re_alpha"], ca["im_alpha"], ca["W"], ca["step"]) == (cb["re_alpha"], cb["im_alpha"], cb["W"], cb["step"])
+    assert np.array_equal(a.trace(), b.trace())
+    a.close()
+    b.close()
+
+
+def test_persistent_2d_configs0_100_steps_parity():
+    cfg = make_config(0)
+    s = mcq.Solver.from_config(cfg)
+    ref = oracle_from(cfg)
+    s.run(cfg.dt, 100)
+    ref.run(cfg.dt, 100)
+    assert rel_l2(s.m(), ref.m.reshape(-1, 3)) < 1e-4
+    a = ref.mem.alpha()
+    cav = s.cavity()
+    assert abs(complex(cav["re_alpha"], cav["im_alpha"]) - a) <= 1e-4 * max(abs(a), 1e-12)
+    # one kernel launch per call (plus the stage-factor kernel), not 9 per step
+    n0 = mcq.mcq_kernel_launches(s.ctx)
+    s.run(cfg.dt, 50)
+    assert mcq.mcq_kernel_launches(s.ctx) - n0 == 2
+    s.close()

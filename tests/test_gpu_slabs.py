@@ -110,6 +110,13 @@ def test_loopback_launch_count_and_layout():
     s.run(cfg.dt, 11)
     s.sync()
     assert mcq.mcq_kernel_launches(s.ctx) - n0 == 1 + 11 * (4 * 4 * (3 + 1) + 1)
+    # overlapped schedule: K-Y and K-YI one launch per component (each component's transpose
+    # runs on the side stream during the next one's pass)
+    mcq.mcq_set_slab_overlap(s.ctx, 1)
+    n0 = mcq.mcq_kernel_launches(s.ctx)
+    s.run(cfg.dt, 11)
+    s.sync()
+    assert mcq.mcq_kernel_launches(s.ctx) - n0 == 1 + 11 * (4 * 4 * (3 + 1 + 3 + 1) + 1)
     s.close()
     one.close()
 
@@ -125,3 +132,19 @@ def test_slab_argument_validation():
     with pytest.raises(mcq.MCQError) as e:
         mcq.mcq_create(g, c, 1e5, 1e-11, 0.01, dist={"rank": 2, "world": 2, "nccl_id": bytes(128)})
     assert e.value.code == -1
+
+
+@pytest.mark.parametrize("grid,slabs", [((16, 12, 8), 4), ((16, 6, 100), 5)])
+def test_overlapped_slab_schedule_is_bitwise_the_serial_one(grid, slabs):
+    """The side-stream schedule (per-component y passes, transposes overlapped: the NCCL default)
+    gives the same bits as one slab."""
+    cfg = small_config("sphere", grid, seed=9, state="phys")
+    one = mcq.Solver.from_config(cfg)
+    lb = _loop(cfg, slabs)
+    mcq.mcq_set_slab_overlap(lb.ctx, 1)
+    one.run(cfg.dt, 13)
+    lb.run(cfg.dt, 13)
+    assert np.array_equal(one.m(), lb.m())
+    assert one.cavity()["re_alpha"] == lb.cavity()["re_alpha"]
+    one.close()
+    lb.close()
