@@ -263,6 +263,8 @@ def main():
                 mcq.mcq_set_brms_mode(sv.ctx, k, dark)
                 mcq.mcq_set_cavity_mode(sv.ctx, k, cfg.f_c + 0.3e9 * k, cfg.kappa)
             sv.set_m(cfg.m0)
+        if R > 1 and cfg.grid[2] == 1:  # concurrent 2D replicas: one persistent kernel per run call
+            mcq.mcq_set_persistent_2d(sv.ctx, 1)
         if args.temperature > 0:
             mcq.mcq_set_temperature(sv.ctx, args.temperature, 1234 + j)
         if args.dmi != 0:

@@ -120,7 +120,12 @@ struct mcq_ctx {
   // "transfers" are HBM copies competing with the passes (measured: 97.6 vs 65.1 ms/step,
   // configs[4] x 8 slabs) — mcq_set_slab_overlap switches it (the loopback tests run both)
   bool overlap = false;
-  bool persist2d = true;  // nz == 1 grids: the persistent cooperative kernel (mcq_set_persistent_2d)
+  // nz == 1 grids: the persistent cooperative kernel (mcq_set_persistent_2d).  Off by default:
+  // measured on configs[0] (64 x 64 x 1), one replica: 64.5 us/step vs 55.4 us for the per-step
+  // graphs (its 9 grid barriers per step cost more than the graph's kernel boundaries); 32
+  // concurrent replicas (a bias sweep): 77.2 vs 89.5 us per step for all 32 (1.70e9 vs 1.46e9
+  // cell-updates/s) — the sweep driver and bench.py --batch switch it on
+  bool persist2d = false;
   std::vector<Slab> sl;
   float2* tw = nullptr;
   float* khat = nullptr;
@@ -159,6 +164,8 @@ struct mcq_ctx {
   long long launches = 0;
   alignas(64) CUtensorMap tmz;  // TMA descriptor of Y for the pipelined K-Z kernel (1 slab)
   bool have_tmz = false;
+  alignas(64) CUtensorMap tmz2;  // TMA descriptor of Y for K-Z v2's staged columns (1 slab)
+  bool have_tmz2 = false;
   std::string err;
   long long cells_here() const { return (long long)sl.size() * sl[0].d.N; }
   long long first_cell() const { return mode == 2 ? (long long)rank * sl[0].d.N : 0; }
@@ -474,7 +481,7 @@ struct Enq {
         else if (NS == 1 && zv && !strcmp(zv, "plain"))
           n = launch_zconv(sl.d, Z, c->khat, c->tw, s);
         else
-          n = launch_zconv_seq(sl.d, Z, c->khat, c->tw, s);
+          n = launch_zconv_seq(sl.d, Z, c->khat, c->tw, s, c->have_tmz2 ? &c->tmz2 : nullptr);
         post(MCQ_K_ZCONV, n);
       }
       if (NS > 1) alltoall(false);
@@ -817,6 +824,14 @@ void make_y_tensor_map(mcq_ctx* c) {
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   c->have_tmz = (r == CUDA_SUCCESS);
+  const cuuint32_t box2[3] = {(cuuint32_t)zconv2_box_c(d.Lz), 1, (cuuint32_t)d.nz};
+  c->have_tmz2 = false;
+  if (box2[0] > 0 && d.nz <= 256) {
+    const CUresult r2 = enc(&c->tmz2, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->sl[0].Y, dims, strides, box2, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    c->have_tmz2 = (r2 == CUDA_SUCCESS);
+  }
 }
 
 int alloc_slab(mcq_ctx* c, Slab& s) {

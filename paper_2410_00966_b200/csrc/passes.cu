@@ -420,47 +420,79 @@ static int sm_count() {
   return nsm;
 }
 
-// K-Z v2 (zconv2.cuh) for Lz = 256 / 512: persistent, 2 CTAs per SM
+// K-Z v2 (zconv2.cuh) for Lz = 256 / 512: persistent, 2 CTAs per SM (MCQ_Z2PERSIST = 0: one
+// CTA per tile)
+// single slab: TMA-staged z columns in K-Z v2 (measured, non-persistent: Lz = 512 3.89 vs 4.51 ms
+// with the register prefetch of the next component, which costs 32 registers there; Lz = 256
+// 153 vs 110 us — its 8-slot register prefetch is cheap and the TMA lead time short)
+#ifndef MCQ_Z2TMA_256
+#define MCQ_Z2TMA_256 0
+#endif
+#ifndef MCQ_Z2TMA_512
+#define MCQ_Z2TMA_512 1
+#endif
+
+#ifndef MCQ_Z2PERSIST
+#define MCQ_Z2PERSIST 0  // one CTA per tile: configs[4] 4.49 vs 5.33 ms, configs[1] 110 vs 153 us (persistent)
+#endif
 template <int L, bool SPLIT>
-static int zconv2_cols(const Dims& d, float2* Y, const float* khat, const float2* tw, int cols, cudaStream_t st) {
+static int zconv2_cols(const Dims& d, float2* Y, const float* khat, const float2* tw, int cols, const void* tmap,
+                       cudaStream_t st) {
   using Z = Z2Cfg<L>;
   const int rem = cols % Z::C;
   const int nkt = cols / Z::C + (rem > 1 ? 1 : 0);
   const int nlone = rem == 1 ? (d.Ly + Z::C - 1) / Z::C : 0;
   const int ntiles = nlone + nkt * d.Ly;
-  const int grid = std::min(ntiles, Z::MINB * sm_count());
-  launch_pdl(d.pdl, k_zconv2<L, SPLIT>, dim3(grid), dim3(Z::NT), Z::SMEM, st, Y, khat, d, tw, nkt, nlone, ntiles);
+  CUtensorMap none;
+  memset(&none, 0, sizeof(none));
+  if (!SPLIT && tmap && (L == 256 ? MCQ_Z2TMA_256 : MCQ_Z2TMA_512)) {
+    // normal tiles: TMA-staged inputs (persistent); the lone Nyquist-column tiles (if any): the
+    // load path, a small launch of its own
+    const CUtensorMap& tm = *reinterpret_cast<const CUtensorMap*>(tmap);
+    const int nnorm = ntiles - nlone;
+    const int grid = MCQ_Z2PERSIST ? std::min(nnorm, Z::MINB * sm_count()) : nnorm;
+    int n = 0;
+    if (nnorm > 0)
+      launch_pdl(d.pdl, k_zconv2<L, false, true>, dim3(grid), dim3(Z::NT), Z::SMEM, st, Y, khat, d, tw, nkt, nlone,
+                 ntiles, nlone, tm), ++n;
+    if (nlone > 0)
+      launch_pdl(d.pdl, k_zconv2<L, false, false>, dim3(nlone), dim3(Z::NT), Z::SMEM, st, Y, khat, d, tw, nkt, nlone,
+                 nlone, 0, none), ++n;
+    return n;
+  }
+  const int grid = MCQ_Z2PERSIST ? std::min(ntiles, Z::MINB * sm_count()) : ntiles;
+  launch_pdl(d.pdl, k_zconv2<L, SPLIT>, dim3(grid), dim3(Z::NT), Z::SMEM, st, Y, khat, d, tw, nkt, nlone, ntiles, 0,
+             none);
   return 1;
 }
 
-// K-Z kernel per length (measured, round 2, 1x B200; profiles/r2_zconv_variants.md):
-//   Lz = 256 (configs[1]-[3]): component-sequential k_zconv_seq 119 us, v2 153 us, warp-
-//   autonomous columns (v3, removed) 189 us;  Lz = 512 (configs[4]): v2 5.36 ms, seq 5.57 ms,
-//   v3 14.95 ms (per-warp 8-byte row pieces: 4x the L2 sector traffic)
 #ifndef MCQ_ZV2_256
-#define MCQ_ZV2_256 0
+#define MCQ_ZV2_256 1
 #endif
 #ifndef MCQ_ZV2_512
 #define MCQ_ZV2_512 1
 #endif
 
-int launch_zconv_seq(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t st) {
+int launch_zconv_seq(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t st,
+                     const void* tmap2) {
   const int cols = d.kxw;  // valid columns of this slab
   if (cols <= 0) return 0;
   static const char* zv = getenv("MCQ_ZVARIANT");  // experiment override: seq | v2
   bool v2 = d.Lz == 256 ? MCQ_ZV2_256 : MCQ_ZV2_512;
   if (zv && !strcmp(zv, "seq")) v2 = false;
   if (zv && !strcmp(zv, "v2")) v2 = true;
-  if (v2 && d.Lz == 256) return d.NS > 1 ? zconv2_cols<256, true>(d, Y, khat, tw, cols, st)
-                                         : zconv2_cols<256, false>(d, Y, khat, tw, cols, st);
-  if (v2 && d.Lz == 512) return d.NS > 1 ? zconv2_cols<512, true>(d, Y, khat, tw, cols, st)
-                                         : zconv2_cols<512, false>(d, Y, khat, tw, cols, st);
+  if (v2 && d.Lz == 256) return d.NS > 1 ? zconv2_cols<256, true>(d, Y, khat, tw, cols, nullptr, st)
+                                         : zconv2_cols<256, false>(d, Y, khat, tw, cols, tmap2, st);
+  if (v2 && d.Lz == 512) return d.NS > 1 ? zconv2_cols<512, true>(d, Y, khat, tw, cols, nullptr, st)
+                                         : zconv2_cols<512, false>(d, Y, khat, tw, cols, tmap2, st);
   int n = 0;
   MCQ_DISPATCH_L(d.Lz, {
     n = d.NS > 1 ? zconv_seq_cols<L, true>(d, Y, khat, tw, cols, st) : zconv_seq_cols<L, false>(d, Y, khat, tw, cols, st);
   })
   return n;
 }
+
+int zconv2_box_c(int Lz) { return Lz == 256 ? Z2Cfg<256>::C : (Lz == 512 ? Z2Cfg<512>::C : 0); }
 
 int zconv_tma_box_c(int Lz) {
   int c = 0;
@@ -524,6 +556,8 @@ void configure_pass_kernels() {
       cudaFuncSetAttribute(k_zconv_tma<L, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZTCfg<L>::SMEM);
     })
   }
+  cudaFuncSetAttribute(k_zconv2<256, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cfg<256>::SMEM);
+  cudaFuncSetAttribute(k_zconv2<512, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cfg<512>::SMEM);
   cudaFuncSetAttribute(k_zconv2<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cfg<256>::SMEM);
   cudaFuncSetAttribute(k_zconv2<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cfg<256>::SMEM);
   cudaFuncSetAttribute(k_zconv2<512, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cfg<512>::SMEM);

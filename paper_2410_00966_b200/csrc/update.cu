@@ -926,7 +926,12 @@ __global__ void __launch_bounds__(UCfg<N2>::NT) k_persist2d(Persist2DArgs pa, co
       }
       grid.sync();
       for (int vb = blockIdx.x; vb < pa.nbx; vb += gridDim.x) {
-        update_body<N2, 1, 0, MODE_LLG, 0, true>(pa.u[s], gtw, vb, 0, pa.nbx, 1, sm);
+        // the stage-specialised bodies of the graph path's k_update instances (same code, same
+        // FMA contraction: bitwise the same results)
+        if (s == 0) update_body<N2, 1, 0, MODE_LLG, 1, true>(pa.u[0], gtw, vb, 0, pa.nbx, 1, sm);
+        else if (s == 1) update_body<N2, 1, 0, MODE_LLG, 2, true>(pa.u[1], gtw, vb, 0, pa.nbx, 1, sm);
+        else if (s == 2) update_body<N2, 1, 0, MODE_LLG, 3, true>(pa.u[2], gtw, vb, 0, pa.nbx, 1, sm);
+        else update_body<N2, 1, 0, MODE_LLG, 4, true>(pa.u[3], gtw, vb, 0, pa.nbx, 1, sm);
         __syncthreads();
       }
       grid.sync();

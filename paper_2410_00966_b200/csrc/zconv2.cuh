@@ -76,10 +76,16 @@ __device__ __forceinline__ int z2a(int pos, int c) {
   return a;
 }
 
-template <int L, bool SPLIT>
+// TMA = true (single slab, normal tiles [tfirst, ntiles)): the z columns come in by TMA tensor
+// copies (box: C columns x nz planes of one component) into the component regions themselves —
+// component 0 and 2 through region 2, component 1 through region 1 — issued a phase or more
+// ahead (next tile's component 0 during this tile's inverse), so no input load holds registers
+// or waits on DRAM; the threads read their inputs from the staged box ([z][c]).
+template <int L, bool SPLIT, bool TMA = false>
 __global__ void __launch_bounds__(Z2Cfg<L>::NT, Z2Cfg<L>::MINB) k_zconv2(float2* __restrict__ Y, const float* __restrict__ khat,
                                                              Dims d, const float2* __restrict__ gtw, int nkt,
-                                                             int nlone, int ntiles) {
+                                                             int nlone, int ntiles, int tfirst,
+                                                             const __grid_constant__ CUtensorMap tm) {
   using Z = Z2Cfg<L>;
   constexpr int NCH = Z::NCH, E = Z::E, TL = Z::TL, C = Z::C, NT = Z::NT, TWP = Z::TWP, LINE = Z::LINE;
   constexpr int EN = 8 * NCH;  // slots that can carry inputs / outputs (z = t + 16 i < nz <= L/2)
@@ -123,11 +129,30 @@ __global__ void __launch_bounds__(Z2Cfg<L>::NT, Z2Cfg<L>::MINB) k_zconv2(float2*
   float2* const reg0 = buf + ch * LINE;              // component 0, this thread's channel
   float2* const reg1 = buf + (NCH + ch) * LINE;      // component 1
   float2* const reg2 = buf + (2 * NCH + ch) * LINE;  // component 2 (exchange only)
-  float2 pf[EN];  // the next inputs in flight: component g+1 of this tile or component 0 of the next
-  {
+  float2 pf[TMA ? 1 : EN];  // (LDG path) the next inputs in flight: component g+1 or the next tile's 0
+  __shared__ __align__(8) uint64_t bars[3];  // (TMA path) one per component region
+  const int t0 = tfirst + blockIdx.x;
+  // TMA: box (C columns, 1 row ky, nz planes) of component g at tile `tl` into region `reg`
+  auto issue = [&](int tl, int g, float2* dst, uint64_t* bar) {
+    int k0, ky0;
+    lane_col(tl, 0, k0, ky0);
+    mbar_arrive_expect_tx(bar, (uint32_t)(C * nz * sizeof(float2)));
+    tma_load_3d(dst, &tm, k0, ky0, g * nz, bar);
+  };
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < 3; ++i) mbar_init(&bars[i], 1);
+      fence_mbar_init();
+      if (t0 < ntiles) {
+        issue(t0, 0, reg2 - ch * LINE, &bars[2]);  // (reg2 of channel 0)
+        issue(t0, 1, reg1 - ch * LINE, &bars[1]);
+      }
+    }
+    __syncthreads();
+  } else {
     int kxl, ky;
-    lane_col(blockIdx.x, c, kxl, ky);
-    const bool ok = kxl < d.kxw && ky < d.Ly && (int)blockIdx.x < ntiles;
+    lane_col(t0, c, kxl, ky);
+    const bool ok = kxl < d.kxw && ky < d.Ly && t0 < ntiles;
     const unsigned col = (unsigned)min(ky, d.Ly - 1) * row + min(kxl, d.kxw - 1);
 #pragma unroll
     for (int i = 0; i < EN; ++i) {
@@ -135,9 +160,10 @@ __global__ void __launch_bounds__(Z2Cfg<L>::NT, Z2Cfg<L>::MINB) k_zconv2(float2*
       pf[i] = (ok && z < nz) ? Y[col + zoff(z)] : make_float2(0.f, 0.f);
     }
   }
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  uint32_t ph1 = 0, ph2 = 0;  // mbarrier phase parities (TMA path)
+  for (int tile = t0; tile < ntiles; tile += gridDim.x) {
     const int nxt = tile + gridDim.x;
-    if (!MCQ_Z2NEXT && tile != (int)blockIdx.x) {  // component 0 of this tile (L2-prefetched)
+    if (!TMA && !MCQ_Z2NEXT && tile != t0) {  // component 0 of this tile (L2-prefetched)
       int kxl, ky;
       lane_col(tile, c, kxl, ky);
       const bool ok = kxl < d.kxw && ky < d.Ly;
@@ -156,9 +182,11 @@ __global__ void __launch_bounds__(Z2Cfg<L>::NT, Z2Cfg<L>::MINB) k_zconv2(float2*
       lane_col(nxt, 0, pk, pky);
       const int pkyf = pky <= hy ? pky : d.Ly - pky;
       const float2* py = Y + (unsigned)pky * row + pk;
+      if (!TMA) {  // (the TMA path loads the inputs itself)
 #pragma unroll 1
-      for (int g = 0; g < 3; ++g)
-        for (int z = threadIdx.x; z < nz; z += NT) prefetch_l2(py + g * cstr + zoff(z));
+        for (int g = 0; g < 3; ++g)
+          for (int z = threadIdx.x; z < nz; z += NT) prefetch_l2(py + g * cstr + zoff(z));
+      }
       const float* pkh = khat + ((unsigned)pkyf * d.kpitch + d.kx0 - d.kxoff + pk) * 6;
       const unsigned kstride = (unsigned)(hy + 1) * d.kpitch * 6;
       for (int j = threadIdx.x; j < (L / 2 + 1) * (3 * C / 16); j += NT) {  // C x 24 B = 3C/16 lines
@@ -171,14 +199,35 @@ __global__ void __launch_bounds__(Z2Cfg<L>::NT, Z2Cfg<L>::MINB) k_zconv2(float2*
     const bool ok = kxl < d.kxw && ky < d.Ly;
     const unsigned col = (unsigned)min(ky, d.Ly - 1) * row + min(kxl, d.kxw - 1);
     __syncthreads();  // the previous tile's shared-memory reads are done
+    if (TMA && threadIdx.x == 0 && tile != t0) {  // component 1 into region 1 (free again)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(tile, 1, reg1 - ch * LINE, &bars[1]);
+    }
 
     // ---- forward: component g in registers, 16 x 16 with one exchange; park g = 0, 1
     float2 v[E];
 #pragma unroll 1
     for (int g = 0; g < 3; ++g) {
+      if constexpr (TMA) {  // the staged box [z][c]: component 1 in region 1, 0 and 2 in region 2
+        uint64_t* bar = g == 1 ? &bars[1] : &bars[2];
+        mbar_wait(bar, g == 1 ? ph1 : ph2);
+        if (g == 1) ph1 ^= 1u; else ph2 ^= 1u;
+        const float2* box = (g == 1 ? reg1 : reg2) - ch * LINE;
 #pragma unroll
-      for (int i = 0; i < E; ++i) v[i] = i < EN ? pf[i] : make_float2(0.f, 0.f);
-      if (g < 2) {
+        for (int i = 0; i < E; ++i) {
+          const int z = t + 16 * i;
+          v[i] = (i < EN && z < nz) ? box[z * C + c] : make_float2(0.f, 0.f);
+        }
+        __syncthreads();  // every input read before the box is overwritten
+        if (g == 0 && threadIdx.x == 0) {  // component 2 into region 2 (its box is consumed)
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(tile, 2, reg2 - ch * LINE, &bars[2]);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) v[i] = i < EN ? pf[i] : make_float2(0.f, 0.f);
+      }
+      if (!TMA && g < 2) {
 #pragma unroll
         for (int i = 0; i < EN; ++i) {
           const int z = t + 16 * i;
@@ -246,7 +295,7 @@ __global__ void __launch_bounds__(Z2Cfg<L>::NT, Z2Cfg<L>::MINB) k_zconv2(float2*
     }
 
     // ---- the next tile's component-0 inputs (in flight during the inverse phase)
-    if (MCQ_Z2NEXT && nxt < ntiles) {
+    if (!TMA && MCQ_Z2NEXT && nxt < ntiles) {
       int nk, nky;
       lane_col(nxt, c, nk, nky);
       const bool nok = nk < d.kxw && nky < d.Ly;
@@ -267,6 +316,10 @@ __global__ void __launch_bounds__(Z2Cfg<L>::NT, Z2Cfg<L>::MINB) k_zconv2(float2*
         for (int i = 0; i < E; ++i) v[i] = R[z2a<C>(t + 16 * i, c)];
       }
       __syncthreads();  // every own-position read of region g is done before the exchange
+      if (TMA && g == 1 && threadIdx.x == 0 && nxt < ntiles) {  // region 2 is done with this tile
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(nxt, 0, reg2 - ch * LINE, &bars[2]);
+      }
       dft16<true>(v);
 #pragma unroll
       for (int r = 0; r < 16; ++r) R[z2a<C>(16 * t + r, c)] = v[r];

@@ -51,10 +51,13 @@ def sweep(make_solver, points, dt, steps, component=1, every=1, pad=8, window=1)
 
     from . import mcq_set_trace, mcq_trace_peaks_batch
 
+    from . import mcq_set_persistent_2d
+
     streams = [torch.cuda.Stream() for _ in points]
     solvers = [make_solver(p, s.cuda_stream) for p, s in zip(points, streams)]
     for sv in solvers:
         mcq_set_trace(sv.ctx, steps // every + 1, every)
+        mcq_set_persistent_2d(sv.ctx, 1)  # 2D replicas: one persistent kernel each (no-op in 3D)
     for sv in solvers:                       # enqueue all: the replicas overlap on the GPU
         sv.run(dt, steps)
     torch.cuda.synchronize()

@@ -21,6 +21,7 @@ def test_persistent_2d_bitwise_equals_graphs(grid):
     cfg = small_config("film", grid, seed=51, state="phys")
     a = mcq.Solver.from_config(cfg)
     b = mcq.Solver.from_config(cfg)
+    mcq.mcq_set_persistent_2d(a.ctx, 1)
     mcq.mcq_set_persistent_2d(b.ctx, 0)
     a.trace(64)
     b.trace(64)
@@ -38,6 +39,7 @@ def test_persistent_2d_bitwise_equals_graphs(grid):
 def test_persistent_2d_configs0_100_steps_parity():
     cfg = make_config(0)
     s = mcq.Solver.from_config(cfg)
+    mcq.mcq_set_persistent_2d(s.ctx, 1)
     ref = oracle_from(cfg)
     s.run(cfg.dt, 100)
     ref.run(cfg.dt, 100)
