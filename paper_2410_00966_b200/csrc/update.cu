@@ -32,6 +32,9 @@
 
 namespace mcq {
 
+#ifndef MCQ_UPLAN
+#define MCQ_UPLAN 1  // K-U row FFTs read a per-plan twiddle table (0: the strided base table)
+#endif
 template <int N2>
 struct UCfg {
 #ifndef MCQ_UE_BIG
@@ -52,7 +55,11 @@ struct UCfg {
   // staged m_s tile (floats, nx <= N2 cells per row): [3][RY+2][nx] at z, [3][RY][nx] at z-1, z+1
   static constexpr int TILE_C = 3 * (RY + 2) * N2;
   static constexpr int TILE_Z = 3 * RY * N2;
-  static constexpr size_t XS_BYTES = (size_t)(2 * N2 + 3 * RY * PITCH) * sizeof(float2);
+  // the row FFTs' per-plan twiddle table (regfft.cuh: R factors of a butterfly class contiguous,
+  // 16-byte loads) and the packing twiddles w_Lx^n, n < N2, then the X rows / exchange buffer
+  static constexpr int PLAN = MCQ_UPLAN ? ((reg_tw_size<N2, E>() + 1) & ~1) : 0;
+  static constexpr int TWB = MCQ_UPLAN ? N2 : 2 * N2;  // base table entries
+  static constexpr size_t XS_BYTES = (size_t)(PLAN + TWB + 3 * RY * PITCH) * sizeof(float2);
   // + the CTA's rows of m_n, the RK4 accumulator and the B_rms map ([3][RY][nx] each, TMA path),
   // so every HBM read of the kernel is in flight while phase A runs
   static constexpr size_t SMEM = XS_BYTES + (size_t)(TILE_C + (MCQ_UROWS ? 5 : 2) * TILE_Z) * sizeof(float);
@@ -256,10 +263,11 @@ __device__ __forceinline__ void update_body(const UpdateArgs& a, const float2* _
   const int stage_ = FS > 0 ? FS : a.stage;  // FS: the RK4 stage fixed at compile time (hot instances)
   using Cf = UCfg<N2>;
   constexpr int E = Cf::E, TL = Cf::TL, RY = Cf::RY, NT = Cf::NT, LX = 2 * N2, PITCH = Cf::PITCH;
-  // w_Lx^m, m < Lx: packing / unpacking of the real transforms and, every other entry, the
-  // row FFTs' twiddles (base table, TWS = 2: fewer live registers than a plan table here)
-  float2* tw = sm;
-  float2* xs = sm + LX;  // [3][RY][PITCH]: X rows (staged by TMA), then the FFT exchange buffer
+  // the row FFTs' plan table (16-byte twiddle loads at immediate offsets; the strided base
+  // table it replaces had 2-4-way bank conflicts in the late stages) and w_Lx^n for the packing
+  float2* ptw = sm;                // row-FFT plan table (MCQ_UPLAN)
+  float2* tw = sm + Cf::PLAN;       // w_Lx^m, m < TWB
+  float2* xs = tw + Cf::TWB;        // [3][RY][PITCH]: X rows (staged by TMA), then the FFT exchange buffer
   float* tc = reinterpret_cast<float*>(reinterpret_cast<char*>(sm) + Cf::XS_BYTES);  // [3][RY+2][nx]
   float* tzm = tc + Cf::TILE_C;                                                       // [3][RY][nx]
   float* tzp = tzm + Cf::TILE_Z;
@@ -320,7 +328,20 @@ __device__ __forceinline__ void update_body(const UpdateArgs& a, const float2* _
       if (ld_br) tma_load_1d(tbr + c * csz, a.brms[0] + c * N + rows, bz, &bars[1]);
     }
   }
-  for (int m = threadIdx.x; m < LX; m += NT) tw[m] = gtw[m * (kTwMax / LX)];
+  {  // twiddle table: every load in flight at once (a serial load -> store loop was the top stall
+     // of the N2 = 512 instance, ncu r2t: 8 dependent L2 round trips per CTA)
+    constexpr int TWB = Cf::TWB, NL = (TWB + NT - 1) / NT;
+    float2 w[NL];
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+      const int m = threadIdx.x + j * NT;
+      w[j] = (m < TWB) ? __ldg(gtw + m * (kTwMax / LX)) : make_float2(0.f, 0.f);
+    }
+    if constexpr (MCQ_UPLAN) reg_tw_build<N2, E, NT>(ptw, gtw);
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+      if (threadIdx.x + j * NT < TWB) tw[threadIdx.x + j * NT] = w[j];
+  }
   pdl_wait();
   __syncthreads();
   if (!tma) {  // fallback (unaligned rows): cooperative coalesced loads into the same layout
@@ -369,7 +390,8 @@ __device__ __forceinline__ void update_body(const UpdateArgs& a, const float2* _
       }
     }
     __syncthreads();  // the staged rows are read before the FFT reuses the buffer
-    reg_fft<N2, E, 3, true, 2>(v, xs, A, tw, t);
+    if constexpr (MCQ_UPLAN) reg_fft<N2, E, 3, true, 0>(v, xs, A, ptw, t);
+    else reg_fft<N2, E, 3, true, 2>(v, xs, A, tw, t);
   } else {
 #pragma unroll
     for (int c = 0; c < 3; ++c)
@@ -656,7 +678,8 @@ __device__ __forceinline__ void update_body(const UpdateArgs& a, const float2* _
 
   // ---------------- C: packed x-R2C of the new rows ----------------
   if (!use_demag) __syncthreads();  // xs may still hold staged rows of other threads' reads
-  reg_fft<N2, E, 3, false, 2>(v, xs, A, tw, t);
+  if constexpr (MCQ_UPLAN) reg_fft<N2, E, 3, false, 0>(v, xs, A, ptw, t);
+  else reg_fft<N2, E, 3, false, 2>(v, xs, A, tw, t);
   // X_k = (Z_k + conj Z_{N-k})/2 - i/2 w^k (Z_k - conj Z_{N-k}); partners via shared memory
 #pragma unroll
   for (int c = 0; c < 3; ++c)

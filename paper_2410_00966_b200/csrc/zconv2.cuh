@@ -35,8 +35,12 @@ namespace mcq {
 #ifndef MCQ_Z2C
 #define MCQ_Z2C 16  // kx columns per tile at Lz = 256 (half that at Lz = 512)
 #endif
+#ifndef MCQ_Z2TMAST
+#define MCQ_Z2TMAST 1  // TMA path: the outputs leave through TMA tensor stores of the component boxes
+#endif
 #ifndef MCQ_Z2KB
-#define MCQ_Z2KB 8  // Khat multiply: points per batch of loads in flight
+#define MCQ_Z2KB 0  // Khat multiply: points per batch of loads in flight (0: 8 at Lz = 256, 4 at 512 —
+                    // 8 spilled there, at the 128-register cap of two CTAs per SM)
 #endif
 #ifndef MCQ_Z2NEXT
 #define MCQ_Z2NEXT 1  // load the next tile's component 0 into registers during the inverse phase
@@ -89,16 +93,30 @@ __global__ void __launch_bounds__(Z2Cfg<L>::NT, Z2Cfg<L>::MINB) k_zconv2(float2*
   using Z = Z2Cfg<L>;
   constexpr int NCH = Z::NCH, E = Z::E, TL = Z::TL, C = Z::C, NT = Z::NT, TWP = Z::TWP, LINE = Z::LINE;
   constexpr int EN = 8 * NCH;  // slots that can carry inputs / outputs (z = t + 16 i < nz <= L/2)
+  constexpr int KLN = 3 * C / 16 + 2;  // 128-byte lines a Khat row segment (C x 24 bytes) can touch
   extern __shared__ __align__(128) float2 sm[];
   float2* twf = sm;                   // [ch][k][TWP]: w_L^{r (NCH k + ch)}
   float2* twi = sm + NCH * 16 * TWP;  // [ch][k][TWP]: w_L^{-k (NCH r + ch)}
   float2* buf = sm + Z::TWN;          // [component][channel][LINE]
   pdl_trigger();
-  for (int e = threadIdx.x; e < NCH * 256; e += NT) {
-    const int ch = e >> 8, k = (e >> 4) & 15, r = e & 15;
-    const int ef = (r * (NCH * k + ch)) % L, ei = (k * (NCH * r + ch)) % L;
-    twf[(ch * 16 + k) * TWP + r] = gtw[ef * (kTwMax / L)];
-    twi[(ch * 16 + k) * TWP + r] = cconj(gtw[ei * (kTwMax / L)]);
+  {  // all of a thread's table loads in flight at once (one L2 round trip per CTA, not four)
+    constexpr int NE = (NCH * 256 + NT - 1) / NT;
+    float2 wf[NE], wi[NE];
+#pragma unroll
+    for (int j = 0; j < NE; ++j) {
+      const int e = threadIdx.x + j * NT, ch = e >> 8, k = (e >> 4) & 15, r = e & 15;
+      const int ef = (r * (NCH * k + ch)) % L, ei = (k * (NCH * r + ch)) % L;
+      wf[j] = e < NCH * 256 ? __ldg(gtw + ef * (kTwMax / L)) : make_float2(0.f, 0.f);
+      wi[j] = e < NCH * 256 ? __ldg(gtw + ei * (kTwMax / L)) : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int j = 0; j < NE; ++j) {
+      const int e = threadIdx.x + j * NT, ch = e >> 8, k = (e >> 4) & 15, r = e & 15;
+      if (e < NCH * 256) {
+        twf[(ch * 16 + k) * TWP + r] = wf[j];
+        twi[(ch * 16 + k) * TWP + r] = cconj(wi[j]);
+      }
+    }
   }
   __syncthreads();
   pdl_wait();
@@ -189,8 +207,8 @@ __global__ void __launch_bounds__(Z2Cfg<L>::NT, Z2Cfg<L>::MINB) k_zconv2(float2*
       }
       const float* pkh = khat + ((unsigned)pkyf * d.kpitch + d.kx0 - d.kxoff + pk) * 6;
       const unsigned kstride = (unsigned)(hy + 1) * d.kpitch * 6;
-      for (int j = threadIdx.x; j < (L / 2 + 1) * (3 * C / 16); j += NT) {  // C x 24 B = 3C/16 lines
-        const int kzf = j / (3 * C / 16), q = j - kzf * (3 * C / 16);
+      for (int j = threadIdx.x; j < (L / 2 + 1) * KLN; j += NT) {  // C x 24 B: <= KLN lines
+        const int kzf = j / KLN, q = j - kzf * KLN;
         prefetch_l2(pkh + kzf * kstride + q * 32);
       }
     }
@@ -198,6 +216,19 @@ __global__ void __launch_bounds__(Z2Cfg<L>::NT, Z2Cfg<L>::MINB) k_zconv2(float2*
     lane_col(tile, c, kxl, ky);
     const bool ok = kxl < d.kxw && ky < d.Ly;
     const unsigned col = (unsigned)min(ky, d.Ly - 1) * row + min(kxl, d.kxw - 1);
+    if (tile == t0 && tile >= nlone) {  // this tile's Khat rows into L2 (needed after 3 transforms)
+      const int pkyf = ky <= hy ? ky : d.Ly - ky;
+      int k0, ky0;
+      lane_col(tile, 0, k0, ky0);
+      const int kyf0 = ky0 <= hy ? ky0 : d.Ly - ky0;
+      const float* pkh = khat + ((unsigned)kyf0 * d.kpitch + d.kx0 - d.kxoff + k0) * 6;
+      const unsigned kstride = (unsigned)(hy + 1) * d.kpitch * 6;
+      (void)pkyf;
+      for (int j = threadIdx.x; j < (L / 2 + 1) * KLN; j += NT) {
+        const int kzf = j / KLN, q = j - kzf * KLN;
+        prefetch_l2(pkh + kzf * kstride + q * 32);
+      }
+    }
     __syncthreads();  // the previous tile's shared-memory reads are done
     if (TMA && threadIdx.x == 0 && tile != t0) {  // component 1 into region 1 (free again)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -266,7 +297,7 @@ __global__ void __launch_bounds__(Z2Cfg<L>::NT, Z2Cfg<L>::MINB) k_zconv2(float2*
       const int kyf = ky <= hy ? ky : d.Ly - ky;
       const float sy = ky <= hy ? 1.f : -1.f;
       const float2* kb = reinterpret_cast<const float2*>(khat) + ((unsigned)kyf * d.kpitch + kx - d.kxoff) * 3;
-      constexpr int KB = MCQ_Z2KB;
+      constexpr int KB = MCQ_Z2KB > 0 ? MCQ_Z2KB : (NCH == 2 ? 4 : 8);
 #pragma unroll
       for (int b = 0; b < E; b += KB) {
         float2 kk[KB][3];
@@ -317,6 +348,7 @@ __global__ void __launch_bounds__(Z2Cfg<L>::NT, Z2Cfg<L>::MINB) k_zconv2(float2*
       }
       __syncthreads();  // every own-position read of region g is done before the exchange
       if (TMA && g == 1 && threadIdx.x == 0 && nxt < ntiles) {  // region 2 is done with this tile
+        if (MCQ_Z2TMAST) tma_store_wait_read();  // (and the TMA store of component 2 has read it)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         issue(nxt, 0, reg2 - ch * LINE, &bars[2]);
       }
@@ -349,7 +381,24 @@ __global__ void __launch_bounds__(Z2Cfg<L>::NT, Z2Cfg<L>::MINB) k_zconv2(float2*
         for (int i = 0; i < E; ++i)
           if ((i < 8) == (ch == 0)) v[i] = add2(v[i], Pr[z2a<C>(t + 16 * i, c)]);
       }
-      if (ok) {
+      if constexpr (TMA && MCQ_Z2TMAST) {
+        // the finished planes into the component's box [z][c] (channel-0 block of region g, read
+        // by nobody any more once every thread has passed the barrier), one TMA tensor store
+        __syncthreads();
+        float2* box = R - ch * LINE;
+#pragma unroll
+        for (int i = 0; i < EN; ++i) {
+          const int z = t + 16 * i;
+          if ((NCH == 1 || (i < 8) == (ch == 0)) && z < nz) box[z * C + c] = v[i];
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          int k0, ky0;
+          lane_col(tile, 0, k0, ky0);
+          tma_store_3d(&tm, box, k0, ky0, g * nz);
+        }
+      } else if (ok) {
 #pragma unroll
         for (int i = 0; i < EN; ++i) {
           const int z = t + 16 * i;
@@ -357,7 +406,9 @@ __global__ void __launch_bounds__(Z2Cfg<L>::NT, Z2Cfg<L>::MINB) k_zconv2(float2*
         }
       }
     }
+    if (TMA && MCQ_Z2TMAST && threadIdx.x == 0) tma_store_wait_read();  // boxes reusable next tile
   }
+  if (TMA && MCQ_Z2TMAST && threadIdx.x == 0) tma_store_wait_all();
 }
 
 }  // namespace mcq
