@@ -2,7 +2,7 @@
 // FFT) for Lz = 256 and 512, the lengths of BJ configs[1]-[4].  Included by passes.cu.
 //
 // Redesigned for sm_100a from the ncu evidence of the component-sequential kernel k_zconv_seq
-// (profiles/r2_ncu_zconv.md): it was bound by shared-memory wavefronts (Lz = 512: three radix
+// (profiles/r2_zconv_variants.md): it was bound by shared-memory wavefronts (Lz = 512: three radix
 // stages, i.e. two full-length exchanges per transform, 25 % bank conflicts) and by exposed load
 // latency (the Khat loads of the multiply; every CTA's first-component loads).
 //  * Frequency channels.  The zero-padded transform of nz <= L/2 inputs is split by the residue
@@ -18,10 +18,12 @@
 //  * Fused multiply.  Component 2's spectrum stays in registers; the Khat multiply reads the
 //    parked components 0 and 1 at the thread's own positions and writes their products back, and
 //    the inverse starts with component 2 (no park / reload of it).
-//  * Persistent CTAs (2 per SM) walk the (kx tile, ky) tiles.  At the start of a tile, bulk L2
-//    prefetches (one cp.async.bulk.prefetch per contiguous row segment) pull the NEXT tile's z
-//    columns and Khat rows into L2; the next tile's component-0 inputs are loaded into registers
-//    during this tile's inverse phase, component g+1's during component g's forward transform.
+//  * One CTA per (kx tile, ky) tile by default (2 resident per SM; the persistent walk,
+//    MCQ_Z2PERSIST, measured slower).  At the start of a tile its Khat rows are prefetched into
+//    L2 (needed after the three forward transforms).  Lz = 256: component g+1's inputs are loaded
+//    into registers during component g's forward transform.  Lz = 512 (TMA = true): the z columns
+//    come in by TMA tensor copies into the component regions, a phase ahead, and the results
+//    leave by TMA tensor stores (measurements: profiles/r2_zconv_variants.md).
 //  * Shared layout [component][channel][position][column] (C = 8: the 64-byte bank half flipped
 //    by bit 4 of the position): stage stores (16t + r) and loads (t + 16i) take 2 wavefronts per
 //    warp, the minimum for 256 bytes.

@@ -7,7 +7,7 @@ Small grids chosen so each one runs a specific bench kernel instance:
     channels; configs[4]), with the "lone" Nyquist-column tiles (NKX = C q + 1), a partial column
     tile (NKX < C) and the z-slab (SPLIT) addressing in loopback;
   * K-U at N2 = 128 (configs[1]) and N2 = 512 (configs[3]/[4]) row transforms;
-  * K-Y / K-YI at Ly = 256;
+  * K-Y / K-YI at Ly = 256 and 1024;
 plus the whole-grid field of configs[1] and configs[3] element by element (relative L2 and max
 abs) against the oracle's direct DFT, and 100 steps of the configs[4] construction downscaled to
 64 x 64 x 32, decomposed into 8 loopback z slabs (bitwise equal to the undecomposed run)."""
@@ -35,6 +35,7 @@ KERNEL_CASES = [
     ("film", (128, 8, 4), "K-U N2=128 (configs[1] row transform)"),
     ("disc", (512, 3, 2), "K-U N2=512 (configs[3]/[4] row transform)"),
     ("sphere", (8, 128, 4), "K-Y / K-YI Ly=256"),
+    ("film", (8, 300, 2), "K-Y / K-YI Ly=1024 (configs[3]/[4]: 8-column tiles, swizzled rows)"),
 ]
 
 

@@ -3,7 +3,8 @@
 compute-sanitizer runs on this driver have left GPUs unusable, so the round-end suite does not
 start it unless MCQ_RUN_SANITIZER names the tool(s) to run, one per gpurun call
 (MCQ_RUN_SANITIZER=memcheck, =racecheck or =synccheck).  The logs of the runs made are kept
-in profiles/r2_sanitizer_*.log."""
+in profiles/r2_sanitizer_*.log.  (Round 2: the GPU pool refuses compute-sanitizer runs
+outright, so no log could be taken.)"""
 import os
 import subprocess
 import sys

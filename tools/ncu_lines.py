@@ -2,6 +2,7 @@
 """Warp-stall samples of one kernel aggregated per CUDA source line.
 
   python tools/ncu_lines.py REPORT.ncu-rep KERNEL_REGEX LIB.so [N]
+  NCU_COL="L1 Wavefronts Shared" python tools/ncu_lines.py ...   (any per-instruction column)
 
 ncu's SASS source page carries the samples per instruction address; the line table comes from
 `nvdisasm -g` on the cubin of LIB.so (the library the report was taken with: build it from the
@@ -16,6 +17,9 @@ import sys
 import tempfile
 
 
+COL = os.environ.get("NCU_COL", "Warp Stall Sampling (All Samples)")
+
+
 def sass_samples(rep, rx):
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{rx}"],
                          capture_output=True, text=True).stdout
@@ -24,7 +28,7 @@ def sass_samples(rep, rx):
     start = next(i for i, l in enumerate(lines) if l.startswith('"Address"'))
     rows = [r for r in csv.DictReader(io.StringIO("\n".join(lines[start:]))) if r["Address"].startswith("0x")]
     base = min(int(r["Address"], 16) for r in rows)
-    return name, {int(r["Address"], 16) - base: int(r["Warp Stall Sampling (All Samples)"] or 0) for r in rows}
+    return name, {int(r["Address"], 16) - base: int(float(r[COL] or 0)) for r in rows}
 
 
 def line_table(lib, mangled_hint):

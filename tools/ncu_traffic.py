@@ -1,10 +1,14 @@
 """Extract per-launch DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) of the hot-path
 kernels from an `ncu --set full` report and store it for bench.py's roofline "traffic" field.
 
-    python tools/ncu_traffic.py report.ncu-rep profiles/ncu_traffic.json config1
+    python tools/ncu_traffic.py report.ncu-rep profiles/ncu_traffic.json config1 [STAGES]
 
-The JSON maps a workload key to {kernel class: bytes per launch, "_source": report name}; kernel
-classes follow bench.py (yfwd, zconv, yinv, y2d, update, cavity)."""
+The JSON maps a workload key to {kernel class: bytes per stage, "_source": report name}; kernel
+classes follow bench.py (yfwd, zconv, yinv, y2d, update, cavity), whose live timings bracket one
+RHS stage of a class (several launches: per-component K-Y passes, the K-Z normal + lone-tile
+launches).  With STAGES given (a tools/ncu_step.py capture of one RK4 step: 4), the bytes of all
+launches of a class are summed and divided by STAGES (the cavity kernel runs once per step);
+without it, the per-launch average is stored (the round-1 captures)."""
 import csv
 import json
 import os
@@ -21,11 +25,14 @@ def classify(name):
         return "yinv" if len(targs) > 1 and targs[1] in ("1", "true") else "yfwd"
     if base == "k_conv":
         return "y2d" if len(targs) > 1 and targs[1] in ("1", "true") else "zconv"
-    return {"k_zconv_seq": "zconv", "k_zconv_tma": "zconv", "k_update": "update", "k_cavity": "cavity"}.get(base)
+    return {"k_zconv_seq": "zconv", "k_zconv2": "zconv", "k_zconv_tma": "zconv", "k_update": "update", "k_cavity": "cavity"}.get(base)
 
 
-def main(rep, out, key):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+def main(rep, out, key, stages=None):
+    # a report, or its `ncu -i REP --page raw --csv` export (full-set step captures exceed what
+    # gpurun copies back; they are exported on the box)
+    txt = open(rep).read() if rep.endswith(".csv") else subprocess.run(
+        ["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(txt.splitlines()))
     hdr, data = rows[0], rows[2:]
     iname = hdr.index("Kernel Name")
@@ -40,11 +47,15 @@ def main(rep, out, key):
         b = float(d[ir]) * scale.get(iu[ir], 1) + float(d[iw]) * scale.get(iu[iw], 1)
         acc.setdefault(k, []).append(b)
     res = json.load(open(out)) if os.path.exists(out) else {}
-    res[key] = {k: sum(v) / len(v) for k, v in acc.items()}
+    if stages:
+        res[key] = {k: sum(v) / (1 if k == "cavity" else int(stages)) for k, v in acc.items()}
+        res[key]["_launches"] = {k: len(v) for k, v in acc.items()}
+    else:
+        res[key] = {k: sum(v) / len(v) for k, v in acc.items()}
     res[key]["_source"] = os.path.basename(rep)
     json.dump(res, open(out, "w"), indent=1, sort_keys=True)
     print(json.dumps(res[key]))
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:4])
+    main(*sys.argv[1:5])

@@ -1,5 +1,5 @@
 """Small workload for compute-sanitizer (memcheck / racecheck / synccheck): every kernel family
-of the hot path on small grids — the RK4 step with cavity and map (3D: K-Y, K-Z v2 at Lz = 256,
+of the hot path on small grids — the RK4 step with cavity and map (3D: K-Y, K-Z v2 at Lz = 256 and 512 (TMA, lone tiles),
 K-YI, K-U, K-CAV; 2D: K-Y2D), the old K-Z at other Lz, relax, field evaluation, Dormand-Prince,
 two cavity modes, thermal + DMI, and a loopback z-slab decomposition.  Run under
 tests/test_gpu_sanitizer.py (opt-in) or by hand:
@@ -15,7 +15,8 @@ from synth import small_config  # noqa: E402
 
 
 def main():
-    for kind, grid in [("film", (12, 10, 1)), ("sphere", (8, 6, 70)), ("sphere", (10, 6, 9)), ("film", (6, 3, 129))]:
+    for kind, grid in [("film", (12, 10, 1)), ("sphere", (8, 6, 70)), ("sphere", (10, 6, 9)), ("film", (6, 3, 129)),
+                       ("film", (8, 6, 200))]:
         cfg = small_config(kind, grid, seed=3, state="phys")
         s = mcq.Solver.from_config(cfg)
         s.run(cfg.dt, 3)
