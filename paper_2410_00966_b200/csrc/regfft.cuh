@@ -11,8 +11,8 @@
 // Thread t runs butterflies b = t + q*TL (q < E/R) whose inputs are exactly its positions
 // p_{q + r E/R}; in the last stage (Ns R = L) the outputs land on the same positions.
 // Twiddles come from a per-plan table in shared memory (reg_tw_build): for every stage with
-// Ns > 1 the R factors w_{Ns R}^{r k} of butterfly class k are contiguous, so a butterfly reads
-// them with R/2 16-byte loads at immediate offsets from one base address.
+// Ns > 1 the R factors w_{Ns R}^{r k} of butterfly class k are read with R/2 16-byte loads at
+// immediate offsets (stride Ns pairs) from one base address (reg_tw_slot).
 #pragma once
 #include "common.cuh"  // kTwMax
 #include "fft.cuh"
@@ -45,6 +45,18 @@ __host__ __device__ constexpr int reg_tw_size() {
   return s < 2 ? 2 : s;
 }
 
+// Slot of factor r of class k in a stage's block.  MCQ_TWSOA: pairs (2 r2, 2 r2 + 1) of all
+// classes side by side — [r2][k][2] — so the 16-byte loads of a warp's consecutive classes are
+// consecutive (the [k][r] layout put them R * 8 bytes apart: 59 % of K-U's excess shared
+// wavefronts at configs[4], ncu r2h); [k][r] otherwise.
+#ifndef MCQ_TWSOA
+#define MCQ_TWSOA 1
+#endif
+template <int R, int Ns>
+__host__ __device__ constexpr int reg_tw_slot(int k, int r) {
+  return MCQ_TWSOA ? ((r >> 1) * Ns + k) * 2 + (r & 1) : k * R + r;
+}
+
 // Fill the plan table from the global fp64-generated table gtw[m] = exp(-2 pi i m / kTwMax)
 // (stage Ns, radix R, class k < Ns, factor r < R: w_{Ns R}^{r k}).  Caller synchronises.
 template <int L, int E, int NT, int Ns = 1, int OFF = 0>
@@ -55,7 +67,7 @@ __device__ __forceinline__ void reg_tw_build(float2* st, const float2* __restric
 #pragma unroll
       for (int j = 0; j < (Ns * R + NT - 1) / NT; ++j) {
         const int e = threadIdx.x + j * NT;
-        if (e < Ns * R) st[OFF + e] = gtw[((e & (R - 1)) * (e / R)) * (kTwMax / (Ns * R))];
+        if (e < Ns * R) st[OFF + reg_tw_slot<R, Ns>(e / R, e & (R - 1))] = gtw[((e & (R - 1)) * (e / R)) * (kTwMax / (Ns * R))];
       }
     }
     reg_tw_build<L, E, NT, Ns * R, OFF + (Ns > 1 ? Ns * R : 0)>(st, gtw);
@@ -81,10 +93,10 @@ __device__ __forceinline__ void reg_stage(float2 (&v)[NLT][E], float2* __restric
       // twiddles depend only on the butterfly, so all NLT lines of the thread share them
       float2 w[R];
       if constexpr (Ns > 1 && TWS == 0) {  // plan table: R/2 16-byte loads from one base
-        const float4* w4 = reinterpret_cast<const float4*>(st + reg_tw_off<L, E>(Ns) + k * R);
+        const float4* w4 = reinterpret_cast<const float4*>(st + reg_tw_off<L, E>(Ns) + reg_tw_slot<R, Ns>(k, 0));
 #pragma unroll
         for (int r2 = 0; r2 < R / 2; ++r2) {
-          const float4 p = w4[r2];
+          const float4 p = w4[MCQ_TWSOA ? r2 * Ns : r2];
           w[2 * r2] = make_float2(p.x, INV ? -p.y : p.y);
           w[2 * r2 + 1] = make_float2(p.z, INV ? -p.w : p.w);
         }

@@ -21,8 +21,10 @@ COL = os.environ.get("NCU_COL", "Warp Stall Sampling (All Samples)")
 
 
 def sass_samples(rep, rx):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{rx}"],
-                         capture_output=True, text=True).stdout
+    # a report, or its `ncu -i REP --page source --csv` export (taken on the GPU box when the
+    # report is too large to bring back)
+    out = open(rep).read() if rep.endswith(".csv") else subprocess.run(
+        ["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{rx}"], capture_output=True, text=True).stdout
     lines = out.splitlines()
     name = lines[0].split('","')[1].rstrip('",') if lines else "?"
     start = next(i for i, l in enumerate(lines) if l.startswith('"Address"'))
