@@ -32,6 +32,13 @@
 
 namespace mcq {
 
+#ifndef MCQ_UZG
+#define MCQ_UZG 1  // N2 >= 256: the exchange stencil's z neighbours read from HBM / L2 at the cell
+                   // update instead of TMA-staged tiles — 12 KB less shared memory per CTA at N2 = 512,
+                   // so 5 CTAs per SM fit instead of 4 (ncu r2l: shared memory was K-U's occupancy
+                   // limit; configs[4] K-U 2241 -> 2181 us).  At N2 = 128 registers limit occupancy
+                   // and the late loads only add latency (67.3 -> 70.1 us): staged there.
+#endif
 #ifndef MCQ_UPLAN
 #define MCQ_UPLAN 1  // K-U row FFTs read a per-plan twiddle table (0: the strided base table)
 #endif
@@ -62,7 +69,8 @@ struct UCfg {
   static constexpr size_t XS_BYTES = (size_t)(PLAN + TWB + 3 * RY * PITCH) * sizeof(float2);
   // + the CTA's rows of m_n, the RK4 accumulator and the B_rms map ([3][RY][nx] each, TMA path),
   // so every HBM read of the kernel is in flight while phase A runs
-  static constexpr size_t SMEM = XS_BYTES + (size_t)(TILE_C + (MCQ_UROWS ? 5 : 2) * TILE_Z) * sizeof(float);
+  static constexpr bool UZG = MCQ_UZG && N2 >= 256;  // z neighbours from HBM / L2, not staged
+  static constexpr size_t SMEM = XS_BYTES + (size_t)(TILE_C + ((MCQ_UROWS ? 3 : 0) + (UZG ? 0 : 2)) * TILE_Z) * sizeof(float);
 };
 
 __device__ __forceinline__ float3 cross3(float3 a, float3 b) {
@@ -270,8 +278,8 @@ __device__ __forceinline__ void update_body(const UpdateArgs& a, const float2* _
   float2* xs = tw + Cf::TWB;        // [3][RY][PITCH]: X rows (staged by TMA), then the FFT exchange buffer
   float* tc = reinterpret_cast<float*>(reinterpret_cast<char*>(sm) + Cf::XS_BYTES);  // [3][RY+2][nx]
   float* tzm = tc + Cf::TILE_C;                                                       // [3][RY][nx]
-  float* tzp = tzm + Cf::TILE_Z;
-  float* tmn = tzp + Cf::TILE_Z;  // [3][RY][nx]: m_n, acc, B_rms rows (TMA path)
+  float* tzp = tzm + (Cf::UZG ? 0 : Cf::TILE_Z);
+  float* tmn = tzp + (Cf::UZG ? 0 : Cf::TILE_Z);  // [3][RY][nx]: m_n, acc, B_rms rows (TMA path)
   float* tap = tmn + Cf::TILE_Z;
   float* tbr = tap + Cf::TILE_Z;
   __shared__ __align__(8) uint64_t bars[2];
@@ -313,14 +321,15 @@ __device__ __forceinline__ void update_body(const UpdateArgs& a, const float2* _
           tma_load_1d(xs + (c * RY + r) * PITCH, a.X + ((size_t)(c * nz + z) * ny + y0 + r) * d.P, bx, &bars[0]);
     }
     const uint32_t bc = (uint32_t)(yhi - ylo + 1) * nx * 4, bz = (uint32_t)nrow * nx * 4;
-    mbar_arrive_expect_tx(&bars[1], 3 * (bc + (zlo ? bz : 0) + (zhi ? bz : 0) + (ld_mn ? 2 * bz : 0) +
+    const bool stz = !Cf::UZG;  // z-neighbour rows staged
+    mbar_arrive_expect_tx(&bars[1], 3 * (bc + (stz && zlo ? bz : 0) + (stz && zhi ? bz : 0) + (ld_mn ? 2 * bz : 0) +
                                          (ld_br ? bz : 0)));
     const long long rows = ((long long)zs * ny + y0) * nx;  // the CTA's rows at z (contiguous)
     for (int c = 0; c < 3; ++c) {
       const float* src = a.mS + c * N;
       tma_load_1d(tc + c * csc + (ylo - (y0 - 1)) * nx, src + ((long long)zs * ny + ylo) * nx, bc, &bars[1]);
-      if (zlo) tma_load_1d(tzm + c * csz, src + ((long long)(zs - 1) * ny + y0) * nx, bz, &bars[1]);
-      if (zhi) tma_load_1d(tzp + c * csz, src + ((long long)(zs + 1) * ny + y0) * nx, bz, &bars[1]);
+      if (stz && zlo) tma_load_1d(tzm + c * csz, src + ((long long)(zs - 1) * ny + y0) * nx, bz, &bars[1]);
+      if (stz && zhi) tma_load_1d(tzp + c * csz, src + ((long long)(zs + 1) * ny + y0) * nx, bz, &bars[1]);
       if (ld_mn) {
         tma_load_1d(tmn + c * csz, a.mN + c * N + rows, bz, &bars[1]);
         tma_load_1d(tap + c * csz, a.acc + c * N + rows, bz, &bars[1]);
@@ -356,11 +365,12 @@ __device__ __forceinline__ void update_body(const UpdateArgs& a, const float2* _
         const int r = e / nx, x = e - r * nx;
         tc[c * csc + (ylo - (y0 - 1) + r) * nxp + x] = src[((long long)zs * ny + ylo) * nx + e];
       }
-      for (int e = threadIdx.x; e < nrow * nx; e += NT) {
-        const int r = e / nx, x = e - r * nx;
-        if (zlo) tzm[c * csz + r * nxp + x] = src[((long long)(zs - 1) * ny + y0) * nx + e];
-        if (zhi) tzp[c * csz + r * nxp + x] = src[((long long)(zs + 1) * ny + y0) * nx + e];
-      }
+      if (!Cf::UZG)
+        for (int e = threadIdx.x; e < nrow * nx; e += NT) {
+          const int r = e / nx, x = e - r * nx;
+          if (zlo) tzm[c * csz + r * nxp + x] = src[((long long)(zs - 1) * ny + y0) * nx + e];
+          if (zhi) tzp[c * csz + r * nxp + x] = src[((long long)(zs + 1) * ny + y0) * nx + e];
+        }
     }
     __syncthreads();
   }
@@ -458,8 +468,14 @@ __device__ __forceinline__ void update_body(const UpdateArgs& a, const float2* _
         mc[c] = sm_pair(r + x0);
         ym[c] = y > 0 ? sm_pair(r - nxp + x0) : mc[c];
         yp[c] = y < ny - 1 ? sm_pair(r + nxp + x0) : mc[c];
-        zm[c] = zlo ? sm_pair(tzm + c * csz + yl * nxp + x0) : mc[c];
-        zp[c] = zhi ? sm_pair(tzp + c * csz + yl * nxp + x0) : mc[c];
+        if constexpr (Cf::UZG) {
+          const unsigned pl = (unsigned)nx * ny;  // plane stride (the halo planes of a slab included)
+          zm[c] = zlo ? ld_pair(a.mS, c * Nu + idx - pl, vec, two) : mc[c];
+          zp[c] = zhi ? ld_pair(a.mS, c * Nu + idx + pl, vec, two) : mc[c];
+        } else {
+          zm[c] = zlo ? sm_pair(tzm + c * csz + yl * nxp + x0) : mc[c];
+          zp[c] = zhi ? sm_pair(tzp + c * csz + yl * nxp + x0) : mc[c];
+        }
         xl[c] = x0 > 0 ? r[x0 - 1] : 0.f;
         xr[c] = x0 + 2 < nx ? r[x0 + 2] : 0.f;
         const int so = c * csz + yl * nxp + x0;  // staged rows (TMA path)
