@@ -39,6 +39,10 @@ namespace mcq {
                    // limit; configs[4] K-U 2241 -> 2181 us).  At N2 = 128 registers limit occupancy
                    // and the late loads only add latency (67.3 -> 70.1 us): staged there.
 #endif
+#ifndef MCQ_UYG
+#define MCQ_UYG 0  // N2 >= 256: the y neighbours from L2 too (the tile then holds the CTA's own rows
+                   // only; measured slower: configs[4] K-U 2221 vs 2187 us, also with 6 CTAs/SM)
+#endif
 #ifndef MCQ_UPLAN
 #define MCQ_UPLAN 1  // K-U row FFTs read a per-plan twiddle table (0: the strided base table)
 #endif
@@ -60,7 +64,9 @@ struct UCfg {
   static constexpr int P0 = N2 + (N2 >= 16 ? N2 / 16 : 1);
   static constexpr int PITCH = P0 + (P0 & 1);
   // staged m_s tile (floats, nx <= N2 cells per row): [3][RY+2][nx] at z, [3][RY][nx] at z-1, z+1
-  static constexpr int TILE_C = 3 * (RY + 2) * N2;
+  static constexpr bool UYG = MCQ_UYG && N2 >= 256;  // y neighbours from HBM / L2: no halo rows
+  static constexpr int HY = UYG ? 0 : 1;             // halo rows above / below the CTA's rows
+  static constexpr int TILE_C = 3 * (RY + 2 * HY) * N2;
   static constexpr int TILE_Z = 3 * RY * N2;
   // the row FFTs' per-plan twiddle table (regfft.cuh: R factors of a butterfly class contiguous,
   // 16-byte loads) and the packing twiddles w_Lx^n, n < N2, then the X rows / exchange buffer
@@ -293,9 +299,10 @@ __device__ __forceinline__ void update_body(const UpdateArgs& a, const float2* _
   const int zs = z + d.zoff;                       // storage plane of the (halo'd) state arrays
   const bool zlo = d.zg0 + z > 0, zhi = d.zg0 + z < d.nzg - 1;  // global z neighbours exist
   const int nrow = min(RY, ny - y0);
-  const int ylo = y0 > 0 ? y0 - 1 : 0, yhi = min(y0 + RY, ny - 1);  // staged m_s rows at z
+  constexpr int HY = Cf::HY;
+  const int ylo = y0 > 0 ? y0 - HY : 0, yhi = min(y0 + RY - 1 + HY, ny - 1);  // staged m_s rows at z
   const int nxp = nx + (nx & 1);                                     // tile row pitch (8-byte pairs)
-  const int csc = (RY + 2) * nxp, csz = RY * nxp;                    // component pitches of the tiles
+  const int csc = (RY + 2 * HY) * nxp, csz = RY * nxp;               // component pitches of the tiles
   const bool use_demag = a.demag && (a.terms & MCQ_TERM_DEMAG) && mode != MODE_X0;
   const bool tma = !NOTMA && (nx & 3) == 0 && (d.P & 1) == 0;
   const bool trows = tma && MCQ_UROWS;
@@ -327,7 +334,7 @@ __device__ __forceinline__ void update_body(const UpdateArgs& a, const float2* _
     const long long rows = ((long long)zs * ny + y0) * nx;  // the CTA's rows at z (contiguous)
     for (int c = 0; c < 3; ++c) {
       const float* src = a.mS + c * N;
-      tma_load_1d(tc + c * csc + (ylo - (y0 - 1)) * nx, src + ((long long)zs * ny + ylo) * nx, bc, &bars[1]);
+      tma_load_1d(tc + c * csc + (ylo - (y0 - HY)) * nx, src + ((long long)zs * ny + ylo) * nx, bc, &bars[1]);
       if (stz && zlo) tma_load_1d(tzm + c * csz, src + ((long long)(zs - 1) * ny + y0) * nx, bz, &bars[1]);
       if (stz && zhi) tma_load_1d(tzp + c * csz, src + ((long long)(zs + 1) * ny + y0) * nx, bz, &bars[1]);
       if (ld_mn) {
@@ -363,7 +370,7 @@ __device__ __forceinline__ void update_body(const UpdateArgs& a, const float2* _
       const float* src = a.mS + c * N;
       for (int e = threadIdx.x; e < (yhi - ylo + 1) * nx; e += NT) {
         const int r = e / nx, x = e - r * nx;
-        tc[c * csc + (ylo - (y0 - 1) + r) * nxp + x] = src[((long long)zs * ny + ylo) * nx + e];
+        tc[c * csc + (ylo - (y0 - HY) + r) * nxp + x] = src[((long long)zs * ny + ylo) * nx + e];
       }
       if (!Cf::UZG)
         for (int e = threadIdx.x; e < nrow * nx; e += NT) {
@@ -440,7 +447,7 @@ __device__ __forceinline__ void update_body(const UpdateArgs& a, const float2* _
   const bool tr = a.trace && wsum;
   const unsigned rowbase = (unsigned)nx * (y + (unsigned)ny * zs);  // 32-bit indices (< 2^32 elements)
   const unsigned Nu = (unsigned)N;
-  const float* trow = tc + (yl + 1) * nxp;  // this row inside the z tile
+  const float* trow = tc + (yl + HY) * nxp;  // this row inside the z tile
   const bool vec = (nx & 1) == 0;           // global pairs are 8-byte aligned
   const bool st = mode == MODE_LLG || mode == MODE_RELAX || (dp && stage_ < 7);  // writes a state
   const bool need_mn = st && stage_ > 1, need_acc = !dp && st && stage_ > 1;
@@ -466,8 +473,13 @@ __device__ __forceinline__ void update_body(const UpdateArgs& a, const float2* _
       for (int c = 0; c < 3; ++c) {
         const float* r = trow + c * csc;
         mc[c] = sm_pair(r + x0);
-        ym[c] = y > 0 ? sm_pair(r - nxp + x0) : mc[c];
-        yp[c] = y < ny - 1 ? sm_pair(r + nxp + x0) : mc[c];
+        if constexpr (Cf::UYG) {
+          ym[c] = y > 0 ? ld_pair(a.mS, c * Nu + idx - nx, vec, two) : mc[c];
+          yp[c] = y < ny - 1 ? ld_pair(a.mS, c * Nu + idx + nx, vec, two) : mc[c];
+        } else {
+          ym[c] = y > 0 ? sm_pair(r - nxp + x0) : mc[c];
+          yp[c] = y < ny - 1 ? sm_pair(r + nxp + x0) : mc[c];
+        }
         if constexpr (Cf::UZG) {
           const unsigned pl = (unsigned)nx * ny;  // plane stride (the halo planes of a slab included)
           zm[c] = zlo ? ld_pair(a.mS, c * Nu + idx - pl, vec, two) : mc[c];
