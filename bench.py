@@ -378,6 +378,8 @@ def main():
     pk = peaks()
     achieved = ab[top] / (prof[top][0] * 1e-3) / 1e9
     step_bytes = step_alg_bytes(L, cfg.grid, cfg.brms_map is not None, ns)
+    if not slab and args.loopback > 1:  # every slab's launches run on this GPU in one step
+        step_bytes *= ns
     traffic, traffic_src = ncu_traffic(args.config, top) if (world == 1 and args.loopback <= 1) else (None, None)
     ms_step = ms_max / args.steps
     # resident working set of one replica: 4 state arrays, X, Y, Khat (+ map), vs the 126 MB L2
@@ -408,7 +410,8 @@ def main():
             "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": pk["hbm_gbs"],
                          "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
                          "traffic_source": (f"profiles/ncu_traffic.json from {traffic_src} (ncu --set full, dram "
-                                            f"bytes read+write per launch; summary profiles/r1_final_ncu_full.txt)"
+                                            f"bytes read+write per RHS stage of this kernel class, i.e. per timed 'launch' here; "
+                                            f"summary profiles/r2_final_ncu.md)"
                                             if traffic_src else None),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("_fallback") else "fallback",
                          "alg_bytes_per_launch": ab[top], "ms_per_launch": prof[top][0]},
