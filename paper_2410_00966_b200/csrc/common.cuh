@@ -201,9 +201,10 @@ void configure_pass_kernels();
 // comp < 0: all three components in one launch; 0..2: that component only
 int launch_yfwd(const Dims& d, const float2* X, float2* Y, const float2* tw, cudaStream_t s, int comp = -1);
 int launch_zconv(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t s);
-// tmap2: CUtensorMap over Y with box (zconv2_box_c(Lz), 1, nz) for the TMA-staged K-Z v2, or nullptr
+// tmap2: CUtensorMaps for the TMA-staged K-Z: Y with boxes (zconv2_box_c(Lz), 1, nz) for v2 and
+// (16, 1, nz) for v3 at Lz = 512, then Khat for v3 (valid iff khat_map), or nullptr
 int launch_zconv_seq(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t s,
-                     const void* tmap2 = nullptr);
+                     const void* tmap2 = nullptr, bool khat_map = false);
 int zconv2_box_c(int Lz);
 int zconv_tma_box_c(int Lz);  // kx columns per K-Z tile of the TMA-pipelined variant
 int launch_zconv_tma(const Dims& d, const void* tmap /* CUtensorMap over Y */, float2* Y, const float* khat,

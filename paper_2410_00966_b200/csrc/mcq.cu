@@ -164,8 +164,10 @@ struct mcq_ctx {
   long long launches = 0;
   alignas(64) CUtensorMap tmz;  // TMA descriptor of Y for the pipelined K-Z kernel (1 slab)
   bool have_tmz = false;
-  alignas(64) CUtensorMap tmz2;  // TMA descriptor of Y for K-Z v2's staged columns (1 slab)
+  alignas(64) CUtensorMap tmz2[3];  // TMA descriptors for K-Z (1 slab): Y with box (zconv2_box_c, 1,
+                                    // nz) for v2, (16, 1, nz) for v3 (Lz = 512); Khat for v3
   bool have_tmz2 = false;
+  bool have_tmk = false;  // tmz2[2] (K-Z v3 needs it)
   std::string err;
   long long cells_here() const { return (long long)sl.size() * sl[0].d.N; }
   long long first_cell() const { return mode == 2 ? (long long)rank * sl[0].d.N : 0; }
@@ -481,7 +483,7 @@ struct Enq {
         else if (NS == 1 && zv && !strcmp(zv, "plain"))
           n = launch_zconv(sl.d, Z, c->khat, c->tw, s);
         else
-          n = launch_zconv_seq(sl.d, Z, c->khat, c->tw, s, c->have_tmz2 ? &c->tmz2 : nullptr);
+          n = launch_zconv_seq(sl.d, Z, c->khat, c->tw, s, c->have_tmz2 ? c->tmz2 : nullptr, c->have_tmk);
         post(MCQ_K_ZCONV, n);
       }
       if (NS > 1) alltoall(false);
@@ -827,10 +829,24 @@ void make_y_tensor_map(mcq_ctx* c) {
   const cuuint32_t box2[3] = {(cuuint32_t)zconv2_box_c(d.Lz), 1, (cuuint32_t)d.nz};
   c->have_tmz2 = false;
   if (box2[0] > 0 && d.nz <= 256) {
-    const CUresult r2 = enc(&c->tmz2, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->sl[0].Y, dims, strides, box2, es,
+    const cuuint32_t box3[3] = {16, 1, (cuuint32_t)d.nz};
+    const CUresult r2 = enc(&c->tmz2[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->sl[0].Y, dims, strides, box2, es,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    c->have_tmz2 = (r2 == CUDA_SUCCESS);
+    const CUresult r3 = enc(&c->tmz2[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->sl[0].Y, dims, strides, box3, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    // Khat [kz][ky][kpitch][6] fp32 as (6 kpitch, Ly/2 + 1, Lz/2 + 1), box (96, 1, 129)
+    const cuuint64_t kd[3] = {(cuuint64_t)6 * d.kpitch, (cuuint64_t)d.Ly / 2 + 1, (cuuint64_t)d.Lz / 2 + 1};
+    const cuuint64_t ks[2] = {(cuuint64_t)6 * d.kpitch * 4, (cuuint64_t)6 * d.kpitch * 4 * (d.Ly / 2 + 1)};
+    const cuuint32_t kb[3] = {96, 1, 129};
+    CUresult rk = CUDA_ERROR_INVALID_VALUE;
+    if (d.Lz == 512 && c->khat && d.kpitch % 2 == 0)
+      rk = enc(&c->tmz2[2], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, c->khat, kd, ks, kb, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rk != CUDA_SUCCESS) memset(&c->tmz2[2], 0, sizeof(CUtensorMap));
+    c->have_tmz2 = (r2 == CUDA_SUCCESS && r3 == CUDA_SUCCESS);
+    c->have_tmk = (rk == CUDA_SUCCESS);
   }
 }
 

@@ -27,6 +27,7 @@
 #include "tma.cuh"
 #include "conv.cuh"
 #include "zconv2.cuh"
+#include "zconv3.cuh"
 
 namespace mcq {
 
@@ -39,12 +40,15 @@ namespace mcq {
 #ifndef MCQ_YNT
 #define MCQ_YNT 256  // target threads per CTA in K-Y / K-YI
 #endif
+#ifndef MCQ_YCMIN
+#define MCQ_YCMIN 8  // fewest kx columns per K-Y / K-YI CTA (64-byte row segments; sets C at L = 1024)
+#endif
 template <int L, int CW = 0>
 struct PassCfg {  // single-component passes (K-Y, K-YI)
   static constexpr int E = L < MCQ_YE ? L : MCQ_YE;
   static constexpr int TL = L / E;
   static constexpr int C0 = MCQ_YNT / TL;
-  static constexpr int C = CW > 0 ? CW : (C0 < 8 ? 8 : (C0 > 64 ? 64 : C0));
+  static constexpr int C = CW > 0 ? CW : (C0 < MCQ_YCMIN ? MCQ_YCMIN : (C0 > 64 ? 64 : C0));
   static constexpr int NT = C * TL;
   static constexpr int TWN = pass_twn<L, E>();  // twiddle table (complex)
   static constexpr size_t SMEM = (size_t)(TWN + (TL > 1 ? L * C : 0)) * sizeof(float2);
@@ -435,9 +439,13 @@ static int sm_count() {
 #ifndef MCQ_Z2PERSIST
 #define MCQ_Z2PERSIST 0  // one CTA per tile: configs[4] 4.49 vs 5.33 ms, configs[1] 110 vs 153 us (persistent)
 #endif
+#ifndef MCQ_Z3
+#define MCQ_Z3 1  // Lz = 512 (single slab): K-Z v3 (zconv3.cuh); 0: v2 with TMA-staged columns
+#endif
+
 template <int L, bool SPLIT>
 static int zconv2_cols(const Dims& d, float2* Y, const float* khat, const float2* tw, int cols, const void* tmap,
-                       cudaStream_t st) {
+                       cudaStream_t st, bool khat_map = false) {
   using Z = Z2Cfg<L>;
   const int rem = cols % Z::C;
   const int nkt = cols / Z::C + (rem > 1 ? 1 : 0);
@@ -445,6 +453,24 @@ static int zconv2_cols(const Dims& d, float2* Y, const float* khat, const float2
   const int ntiles = nlone + nkt * d.Ly;
   CUtensorMap none;
   memset(&none, 0, sizeof(none));
+  if (L == 512 && !SPLIT && tmap && khat_map && MCQ_Z3 && d.nz <= 256 && d.kxoff == 0) {
+    // K-Z v3 (zconv3.cuh): 16-column tiles, persistent, one CTA per SM; the lone Nyquist column
+    // (NKX = 16 q + 1) by v2's lone-tile launch.  tmap: [v2 box, v3 box, Khat]
+    const CUtensorMap* tm3 = reinterpret_cast<const CUtensorMap*>(tmap) + 1;
+    const int rem3 = cols % Z3Cfg::C;
+    const int nkt3 = cols / Z3Cfg::C + (rem3 > 1 ? 1 : 0);
+    const int nt3 = nkt3 * d.Ly;
+    int n = 0;
+    if (nt3 > 0)
+      launch_pdl(d.pdl, k_zconv3, dim3(std::min(nt3, sm_count())), dim3(Z3Cfg::NT), Z3Cfg::SMEM, st, Y, khat, d, tw,
+                 nkt3, nt3, tm3[0], tm3[1]), ++n;
+    if (rem3 == 1) {
+      const int nl = (d.Ly + Z::C - 1) / Z::C;
+      launch_pdl(d.pdl, k_zconv2<L, false, false>, dim3(nl), dim3(Z::NT), Z::SMEM, st, Y, khat, d, tw, nkt, nl, nl, 0,
+                 none), ++n;
+    }
+    return n;
+  }
   if (!SPLIT && tmap && (L == 256 ? MCQ_Z2TMA_256 : MCQ_Z2TMA_512)) {
     // normal tiles: TMA-staged inputs (persistent); the lone Nyquist-column tiles (if any): the
     // load path, a small launch of its own
@@ -474,7 +500,7 @@ static int zconv2_cols(const Dims& d, float2* Y, const float* khat, const float2
 #endif
 
 int launch_zconv_seq(const Dims& d, float2* Y, const float* khat, const float2* tw, cudaStream_t st,
-                     const void* tmap2) {
+                     const void* tmap2, bool khat_map) {
   const int cols = d.kxw;  // valid columns of this slab
   if (cols <= 0) return 0;
   static const char* zv = getenv("MCQ_ZVARIANT");  // experiment override: seq | v2
@@ -484,7 +510,7 @@ int launch_zconv_seq(const Dims& d, float2* Y, const float* khat, const float2* 
   if (v2 && d.Lz == 256) return d.NS > 1 ? zconv2_cols<256, true>(d, Y, khat, tw, cols, nullptr, st)
                                          : zconv2_cols<256, false>(d, Y, khat, tw, cols, tmap2, st);
   if (v2 && d.Lz == 512) return d.NS > 1 ? zconv2_cols<512, true>(d, Y, khat, tw, cols, nullptr, st)
-                                         : zconv2_cols<512, false>(d, Y, khat, tw, cols, tmap2, st);
+                                         : zconv2_cols<512, false>(d, Y, khat, tw, cols, tmap2, st, khat_map);
   int n = 0;
   MCQ_DISPATCH_L(d.Lz, {
     n = d.NS > 1 ? zconv_seq_cols<L, true>(d, Y, khat, tw, cols, st) : zconv_seq_cols<L, false>(d, Y, khat, tw, cols, st);
@@ -562,6 +588,7 @@ void configure_pass_kernels() {
   cudaFuncSetAttribute(k_zconv2<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cfg<256>::SMEM);
   cudaFuncSetAttribute(k_zconv2<512, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cfg<512>::SMEM);
   cudaFuncSetAttribute(k_zconv2<512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cfg<512>::SMEM);
+  cudaFuncSetAttribute(k_zconv3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z3Cfg::SMEM);
   cudaGetLastError();
 }
 

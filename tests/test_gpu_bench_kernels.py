@@ -3,9 +3,10 @@ full size real"; BJ north_star acceptance: fp32 field within 1e-5 relative L2 pe
 total, m after fixed steps within 1e-4).
 
 Small grids chosen so each one runs a specific bench kernel instance:
-  * K-Z v2 (zconv2.cuh) at Lz = 256 (one channel; configs[1]-[3]) and Lz = 512 (two frequency
-    channels; configs[4]), with the "lone" Nyquist-column tiles (NKX = C q + 1), a partial column
-    tile (NKX < C) and the z-slab (SPLIT) addressing in loopback;
+  * K-Z v2 (zconv2.cuh) at Lz = 256 (one channel; configs[1]-[3]) and K-Z v3 (zconv3.cuh) at
+    Lz = 512 (two frequency channels in registers; configs[4]), with the "lone" Nyquist-column
+    tiles (NKX = C q + 1), partial column tiles (NKX < C) and v2's z-slab (SPLIT) addressing at
+    Lz = 512 in loopback;
   * K-U at N2 = 128 (configs[1]) and N2 = 512 (configs[3]/[4]) row transforms;
   * K-Y / K-YI at Ly = 256 and 1024;
 plus the whole-grid field of configs[1] and configs[3] element by element (relative L2 and max
@@ -28,10 +29,12 @@ import paper_2410_00966_b200 as mcq  # noqa: E402
 # (kind, grid, what it instantiates)
 KERNEL_CASES = [
     ("disc", (16, 6, 100), "K-Z v2 Lz=256, NKX=17: 1 full 16-column tile + lone tiles"),
-    ("film", (8, 6, 200), "K-Z v2 Lz=512 (2 channels), NKX=9: 1 full 8-column tile + lone tiles"),
-    ("sphere", (8, 10, 200), "K-Z v2 Lz=512, masked"),
+    ("film", (8, 6, 200), "K-Z v3 Lz=512 (2 channels), NKX=9: one partial 16-column tile"),
+    ("sphere", (8, 10, 200), "K-Z v3 Lz=512, masked"),
     ("film", (4, 5, 70), "K-Z v2 Lz=256, NKX=5 < C: one partial tile per ky"),
-    ("film", (6, 3, 129), "K-Z v2 Lz=512 with nz = 129 (zero inputs of the channel transforms)"),
+    ("film", (6, 3, 129), "K-Z v3 Lz=512 with nz = 129 (zero inputs of the channel transforms)"),
+    ("film", (16, 6, 200), "K-Z v3 Lz=512, NKX=17: one 16-column tile + v2's lone tiles"),
+    ("disc", (40, 8, 150), "K-Z v3 Lz=512, NKX=65: 4 tiles per ky + lone tiles, masked"),
     ("film", (128, 8, 4), "K-U N2=128 (configs[1] row transform)"),
     ("disc", (512, 3, 2), "K-U N2=512 (configs[3]/[4] row transform)"),
     ("sphere", (8, 128, 4), "K-Y / K-YI Ly=256"),
