@@ -165,7 +165,7 @@ struct mcq_ctx {
   alignas(64) CUtensorMap tmz;  // TMA descriptor of Y for the pipelined K-Z kernel (1 slab)
   bool have_tmz = false;
   alignas(64) CUtensorMap tmz2[3];  // TMA descriptors for K-Z (1 slab): Y with box (zconv2_box_c, 1,
-                                    // nz) for v2, (16, 1, nz) for v3 (Lz = 512); Khat for v3
+                                    // nz) for v2, (16, 1, nz) for v3 (Lz = 256, 512); Khat for v3
   bool have_tmz2 = false;
   bool have_tmk = false;  // tmz2[2] (K-Z v3 needs it)
   std::string err;
@@ -841,7 +841,7 @@ void make_y_tensor_map(mcq_ctx* c) {
     const cuuint64_t ks[2] = {(cuuint64_t)6 * d.kpitch * 4, (cuuint64_t)6 * d.kpitch * 4 * (d.Ly / 2 + 1)};
     const cuuint32_t kb[3] = {96, 1, 129};
     CUresult rk = CUDA_ERROR_INVALID_VALUE;
-    if (d.Lz == 512 && c->khat && d.kpitch % 2 == 0)
+    if ((d.Lz == 512 || d.Lz == 256) && c->khat && d.kpitch % 2 == 0)
       rk = enc(&c->tmz2[2], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, c->khat, kd, ks, kb, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (rk != CUDA_SUCCESS) memset(&c->tmz2[2], 0, sizeof(CUtensorMap));

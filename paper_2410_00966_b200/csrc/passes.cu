@@ -442,6 +442,10 @@ static int sm_count() {
 #ifndef MCQ_Z3
 #define MCQ_Z3 1  // Lz = 512 (single slab): K-Z v3 (zconv3.cuh); 0: v2 with TMA-staged columns
 #endif
+#ifndef MCQ_Z3_256
+#define MCQ_Z3_256 0  // Lz = 256 (single slab): K-Z v3 (parity-tested, measured slower: 126.6 vs 105.6
+                      // us at configs[1] — one channel leaves v2 no hand-over to save); 0: v2
+#endif
 
 template <int L, bool SPLIT>
 static int zconv2_cols(const Dims& d, float2* Y, const float* khat, const float2* tw, int cols, const void* tmap,
@@ -453,17 +457,18 @@ static int zconv2_cols(const Dims& d, float2* Y, const float* khat, const float2
   const int ntiles = nlone + nkt * d.Ly;
   CUtensorMap none;
   memset(&none, 0, sizeof(none));
-  if (L == 512 && !SPLIT && tmap && khat_map && MCQ_Z3 && d.nz <= 256 && d.kxoff == 0) {
-    // K-Z v3 (zconv3.cuh): 16-column tiles, persistent, one CTA per SM; the lone Nyquist column
-    // (NKX = 16 q + 1) by v2's lone-tile launch.  tmap: [v2 box, v3 box, Khat]
+  if (!SPLIT && tmap && khat_map && (L == 512 ? MCQ_Z3 : MCQ_Z3_256) && d.nz <= L / 2 && d.kxoff == 0) {
+    // K-Z v3 (zconv3.cuh): 16-column tiles, persistent, MINB CTAs per SM; the lone Nyquist
+    // column (NKX = 16 q + 1) by v2's lone-tile launch.  tmap: [v2 box, v3 box, Khat]
+    using Z3 = Z3Cfg<L>;
     const CUtensorMap* tm3 = reinterpret_cast<const CUtensorMap*>(tmap) + 1;
-    const int rem3 = cols % Z3Cfg::C;
-    const int nkt3 = cols / Z3Cfg::C + (rem3 > 1 ? 1 : 0);
+    const int rem3 = cols % Z3::C;
+    const int nkt3 = cols / Z3::C + (rem3 > 1 ? 1 : 0);
     const int nt3 = nkt3 * d.Ly;
     int n = 0;
     if (nt3 > 0)
-      launch_pdl(d.pdl, k_zconv3, dim3(std::min(nt3, sm_count())), dim3(Z3Cfg::NT), Z3Cfg::SMEM, st, Y, khat, d, tw,
-                 nkt3, nt3, tm3[0], tm3[1]), ++n;
+      launch_pdl(d.pdl, k_zconv3<L>, dim3(std::min(nt3, Z3::MINB * sm_count())), dim3(Z3::NT), Z3::SMEM, st, Y, khat,
+                 d, tw, nkt3, nt3, tm3[0], tm3[1]), ++n;
     if (rem3 == 1) {
       const int nl = (d.Ly + Z::C - 1) / Z::C;
       launch_pdl(d.pdl, k_zconv2<L, false, false>, dim3(nl), dim3(Z::NT), Z::SMEM, st, Y, khat, d, tw, nkt, nl, nl, 0,
@@ -508,7 +513,7 @@ int launch_zconv_seq(const Dims& d, float2* Y, const float* khat, const float2* 
   if (zv && !strcmp(zv, "seq")) v2 = false;
   if (zv && !strcmp(zv, "v2")) v2 = true;
   if (v2 && d.Lz == 256) return d.NS > 1 ? zconv2_cols<256, true>(d, Y, khat, tw, cols, nullptr, st)
-                                         : zconv2_cols<256, false>(d, Y, khat, tw, cols, tmap2, st);
+                                         : zconv2_cols<256, false>(d, Y, khat, tw, cols, tmap2, st, khat_map);
   if (v2 && d.Lz == 512) return d.NS > 1 ? zconv2_cols<512, true>(d, Y, khat, tw, cols, nullptr, st)
                                          : zconv2_cols<512, false>(d, Y, khat, tw, cols, tmap2, st, khat_map);
   int n = 0;
@@ -588,7 +593,8 @@ void configure_pass_kernels() {
   cudaFuncSetAttribute(k_zconv2<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cfg<256>::SMEM);
   cudaFuncSetAttribute(k_zconv2<512, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cfg<512>::SMEM);
   cudaFuncSetAttribute(k_zconv2<512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cfg<512>::SMEM);
-  cudaFuncSetAttribute(k_zconv3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z3Cfg::SMEM);
+  cudaFuncSetAttribute(k_zconv3<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z3Cfg<256>::SMEM);
+  cudaFuncSetAttribute(k_zconv3<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z3Cfg<512>::SMEM);
   cudaGetLastError();
 }
 

@@ -1,4 +1,4 @@
-// zconv3.cuh — K-Z for Lz = 512 with the column slice held in registers (a3 of SURVEY §8(a):
+// zconv3.cuh — K-Z for Lz = 256 / 512 with the column slice held in registers (a3 of SURVEY §8(a):
 // forward z FFT, Khat multiply, inverse z FFT).  Included by passes.cu; MCQ_Z3 selects it.
 //
 // Same arithmetic as K-Z v2 (zconv2.cuh: frequency channels X[2k + ch] = DFT_256(x[n] w_512^{n ch}),
@@ -25,22 +25,32 @@
 
 namespace mcq {
 
+#ifndef MCQ_Z3MINB256
+#define MCQ_Z3MINB256 2  // Lz = 256: CTAs per SM asked of ptxas (2: the 128-register cap)
+#endif
+template <int L_>
 struct Z3Cfg {
-  static constexpr int L = 512, NCH = 2, C = 16, TL = 16, NT = C * TL;  // 256 threads
-  static constexpr int TWP = 18;                                         // as Z2Cfg
-  static constexpr int TWN = 2 * NCH * 16 * TWP;                         // twf + twi (complex)
-  static constexpr int LINE = 256 * C;                                   // one (channel) exchange block
-  static constexpr int BOX = 3 * 256 * C;                                // one tile's inputs (nz <= 256)
-  static constexpr int KH = 2 * 129 * 3 * C;                             // one tile's Khat ([kz][C][3] float2, 258 rows)
-  static constexpr int REG = BOX > KH ? BOX : KH;                        // a region holds either
-  static constexpr size_t SMEM = (size_t)(TWN + 2 * REG) * sizeof(float2);  // 202 KB
+  static_assert(L_ == 256 || L_ == 512, "K-Z v3: Lz = 256 or 512");
+  static constexpr int L = L_, NCH = L / 256, C = 16, TL = 16, NT = C * TL;  // 256 threads
+  static constexpr int TWP = 18;                                              // as Z2Cfg
+  static constexpr int TWN = 2 * NCH * 16 * TWP;                              // twf + twi (complex)
+  static constexpr int LINE = 256 * C;                                        // one (channel) exchange block
+  static constexpr int BOX = 3 * (L / 2) * C;                                 // one tile's inputs (nz <= L/2)
+  static constexpr int NKB = (L / 2 + 1 + 128) / 129;                         // Khat boxes of 129 kz rows
+  static constexpr int KH = NKB * 129 * 3 * C;                                // one tile's Khat ([kz][C][3] float2)
+  static constexpr int XCH = NCH * LINE;                                      // one component's exchange
+  static constexpr int REG0 = BOX > KH ? BOX : KH;
+  static constexpr int REG = REG0 > XCH ? REG0 : XCH;                         // a region holds any of them
+  static constexpr size_t SMEM = (size_t)(TWN + 2 * REG) * sizeof(float2);   // 207 KB (512), 104 KB (256)
+  static constexpr int MINB = L == 256 ? MCQ_Z3MINB256 : 1;  // 512: up to 255 registers
 };
 
-__global__ void __launch_bounds__(Z3Cfg::NT, 1) k_zconv3(float2* __restrict__ Y, const float* __restrict__ khat,
+template <int L_>
+__global__ void __launch_bounds__(Z3Cfg<L_>::NT, Z3Cfg<L_>::MINB) k_zconv3(float2* __restrict__ Y, const float* __restrict__ khat,
                                                          Dims d, const float2* __restrict__ gtw, int nkt, int ntiles,
                                                          const __grid_constant__ CUtensorMap tm,
                                                          const __grid_constant__ CUtensorMap tmk) {
-  using Z = Z3Cfg;
+  using Z = Z3Cfg<L_>;
   constexpr int L = Z::L, NCH = Z::NCH, C = Z::C, NT = Z::NT, TWP = Z::TWP, LINE = Z::LINE, REG = Z::REG;
   extern __shared__ __align__(128) float2 sm[];
   float2* twf = sm;                   // [ch][k][TWP]: w_L^{r (NCH k + ch)}
@@ -89,7 +99,7 @@ __global__ void __launch_bounds__(Z3Cfg::NT, 1) k_zconv3(float2* __restrict__ Y,
     tile_pos(j, kx0, ky);
     mbar_arrive_expect_tx(&bars[b], (uint32_t)(3 * C * nz * sizeof(float2)));
 #pragma unroll
-    for (int g = 0; g < 3; ++g) tma_load_3d(bufs + b * REG + g * 256 * C, &tm, kx0, ky, g * nz, &bars[b]);
+    for (int g = 0; g < 3; ++g) tma_load_3d(bufs + b * REG + g * (L / 2) * C, &tm, kx0, ky, g * nz, &bars[b]);
   };
   // tile j's Khat rows into region Ks as [kz][C][3] float2 by two TMA tensor copies (tmk: Khat
   // viewed as (6 kpitch floats, Ly/2 + 1, Lz/2 + 1), box (6 C, 1, 129): kz rows 0-128 and 129-257,
@@ -102,9 +112,9 @@ __global__ void __launch_bounds__(Z3Cfg::NT, 1) k_zconv3(float2* __restrict__ Y,
     tile_pos(j, kx0, ky);
     const int kyf = ky <= hy ? ky : d.Ly - ky;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the generic accesses of the region
-    mbar_arrive_expect_tx(&bars[2], 2u * 129 * 6 * C * sizeof(float));
-    tma_load_3d(Ks, &tmk, (d.kx0 - d.kxoff + kx0) * 6, kyf, 0, &bars[2]);
-    tma_load_3d(Ks + 129 * 3 * C, &tmk, (d.kx0 - d.kxoff + kx0) * 6, kyf, 129, &bars[2]);
+    mbar_arrive_expect_tx(&bars[2], (uint32_t)(Z::NKB * 129 * 6 * C * sizeof(float)));
+#pragma unroll
+    for (int q = 0; q < Z::NKB; ++q) tma_load_3d(Ks + q * 129 * 3 * C, &tmk, (d.kx0 - d.kxoff + kx0) * 6, kyf, 129 * q, &bars[2]);
   };
   // Per tile j with its inputs in region b: Khat(j) is staged into region b^1 (free: the previous
   // tile's exchange area) during the forward transforms; once the multiply has read it, the next
@@ -127,31 +137,34 @@ __global__ void __launch_bounds__(Z3Cfg::NT, 1) k_zconv3(float2* __restrict__ Y,
     const bool ok = kxl < d.kxw;
 
     // ---- inputs (z = t + 16 i < nz) into registers; then the buffer is the exchange area
-    float2 X[3][2][16];
+    constexpr int EN = 8 * NCH;  // slots that can carry inputs / outputs (z = t + 16 i < nz <= L/2)
+    float2 X[3][NCH][16];
 #pragma unroll
     for (int g = 0; g < 3; ++g)
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int z = t + 16 * i;
-        X[g][0][i] = z < nz ? B[g * 256 * C + z * C + c] : make_float2(0.f, 0.f);
+        X[g][0][i] = (i < EN && z < nz) ? B[g * (L / 2) * C + z * C + c] : make_float2(0.f, 0.f);
       }
     __syncthreads();
 
     // ---- forward, per component: both channels, one 16 x 16 exchange
 #pragma unroll
     for (int g = 0; g < 3; ++g) {
-      X[g][1][0] = X[g][0][0];
+      if constexpr (NCH == 2) {
+        X[g][NCH - 1][0] = X[g][0][0];
 #pragma unroll
-      for (int i = 1; i < 16; ++i) X[g][1][i] = cmul(X[g][0][i], w32c(i));
-      dft16<false>(X[g][0]);
-      dft16<false>(X[g][1]);
+        for (int i = 1; i < 16; ++i) X[g][NCH - 1][i] = cmul(X[g][0][i], w32c(i));
+      }
 #pragma unroll
-      for (int ch = 0; ch < 2; ++ch)
+      for (int ch = 0; ch < NCH; ++ch) dft16<false>(X[g][ch]);
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
         for (int r = 0; r < 16; ++r) B[ch * LINE + (16 * t + r) * C + c] = X[g][ch][r];
       __syncthreads();
 #pragma unroll
-      for (int ch = 0; ch < 2; ++ch) {
+      for (int ch = 0; ch < NCH; ++ch) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) X[g][ch][i] = B[ch * LINE + (t + 16 * i) * C + c];
         const float4* w4 = reinterpret_cast<const float4*>(twf + (ch * 16 + t) * TWP);
@@ -174,7 +187,7 @@ __global__ void __launch_bounds__(Z3Cfg::NT, 1) k_zconv3(float2* __restrict__ Y,
 #pragma unroll
       for (int i = 0; i < 16; ++i)
 #pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
+        for (int ch = 0; ch < NCH; ++ch) {
           const int kz = NCH * (t + 16 * i) + ch;
           const int kzf = i < 8 ? kz : L - kz;  // kz = L/2 (i = 8, t = ch = 0) folds to itself
           const float2* k2 = Ks + (kzf * C + c) * 3;
@@ -197,34 +210,36 @@ __global__ void __launch_bounds__(Z3Cfg::NT, 1) k_zconv3(float2* __restrict__ Y,
     const unsigned col = (unsigned)ky * row + (unsigned)min(kxl, d.kxw - 1);
 #pragma unroll
     for (int g = 0; g < 3; ++g) {
-      dft16<true>(X[g][0]);
-      dft16<true>(X[g][1]);
 #pragma unroll
-      for (int ch = 0; ch < 2; ++ch)
+      for (int ch = 0; ch < NCH; ++ch) dft16<true>(X[g][ch]);
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
         for (int r = 0; r < 16; ++r) B[ch * LINE + (16 * t + r) * C + c] = X[g][ch][r];
       __syncthreads();
 #pragma unroll
-      for (int ch = 0; ch < 2; ++ch) {
+      for (int ch = 0; ch < NCH; ++ch) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) X[g][ch][i] = B[ch * LINE + (t + 16 * i) * C + c];
         const float4* w4 = reinterpret_cast<const float4*>(twi + (ch * 16 + t) * TWP);
 #pragma unroll
         for (int r2 = 0; r2 < 8; ++r2) {
           const float4 p = w4[r2];
-          X[g][ch][2 * r2] = cmul(X[g][ch][2 * r2], make_float2(p.x, p.y));
+          if (NCH == 2 || r2 > 0) X[g][ch][2 * r2] = cmul(X[g][ch][2 * r2], make_float2(p.x, p.y));
           X[g][ch][2 * r2 + 1] = cmul(X[g][ch][2 * r2 + 1], make_float2(p.z, p.w));
         }
         dft16<true>(X[g][ch]);
       }
       __syncthreads();  // the block is rewritten by the next component
+      if constexpr (NCH == 2) {
 #pragma unroll
-      for (int i = 1; i < 16; ++i) X[g][1][i] = cmul(X[g][1][i], cconj(w32c(i)));
+        for (int i = 1; i < 16; ++i) X[g][NCH - 1][i] = cmul(X[g][NCH - 1][i], cconj(w32c(i)));
+      }
       if (ok) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
+        for (int i = 0; i < EN; ++i) {
           const int z = t + 16 * i;
-          if (z < nz) Y[col + g * cstr + (unsigned)z * plane] = add2(X[g][0][i], X[g][1][i]);
+          if (z < nz) Y[col + g * cstr + (unsigned)z * plane] = NCH == 2 ? add2(X[g][0][i], X[g][NCH - 1][i]) : X[g][0][i];
         }
       }
     }
