@@ -25,7 +25,7 @@ def classify(name):
         return "yinv" if len(targs) > 1 and targs[1] in ("1", "true") else "yfwd"
     if base == "k_conv":
         return "y2d" if len(targs) > 1 and targs[1] in ("1", "true") else "zconv"
-    return {"k_zconv_seq": "zconv", "k_zconv2": "zconv", "k_zconv_tma": "zconv", "k_update": "update", "k_cavity": "cavity"}.get(base)
+    return {"k_zconv_seq": "zconv", "k_zconv2": "zconv", "k_zconv3": "zconv", "k_zconv_tma": "zconv", "k_update": "update", "k_cavity": "cavity"}.get(base)
 
 
 def main(rep, out, key, stages=None):
