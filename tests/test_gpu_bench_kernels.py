@@ -35,6 +35,7 @@ KERNEL_CASES = [
     ("film", (6, 3, 129), "K-Z v3 Lz=512 with nz = 129 (zero inputs of the channel transforms)"),
     ("film", (16, 6, 200), "K-Z v3 Lz=512, NKX=17: one 16-column tile + v2's lone tiles"),
     ("disc", (40, 8, 150), "K-Z v3 Lz=512, NKX=65: 4 tiles per ky + lone tiles, masked"),
+    ("film", (6, 4, 256), "K-Z v3 Lz=512 at nz = 256 (configs[4]'s depth: every input slot live)"),
     ("film", (128, 8, 4), "K-U N2=128 (configs[1] row transform)"),
     ("disc", (512, 3, 2), "K-U N2=512 (configs[3]/[4] row transform)"),
     ("sphere", (8, 128, 4), "K-Y / K-YI Ly=256"),
