@@ -92,6 +92,10 @@ struct Slab {
   double* partials = nullptr;                       // into ctx partials (loopback) or own (NCCL)
   int nparts = 0;                                   // K-U CTAs of one stage (nbx * nz)
   double* psum = nullptr;                           // NCCL: this rank's plane sums [nz][kNPart]
+  // z slabs: TMA descriptors for K-Z v3 in the [v2, v3, Khat] convention of mcq_ctx::tmz2 — [1]:
+  // the received blocks R as 4D (KXS, Ly, nzl, 3 NS), [2]: this slab's Khat ([0] unused)
+  alignas(64) CUtensorMap tm3[3];
+  bool have_tm3 = false;
 };
 
 }  // namespace
@@ -449,7 +453,7 @@ struct Enq {
       wait(s, 4);
       for (auto& sl : c->sl) {
         pre(MCQ_K_ZCONV);
-        const int n = launch_zconv_seq(sl.d, sl.R, c->khat, c->tw, s);
+        const int n = launch_zconv_seq(sl.d, sl.R, c->khat, c->tw, s, sl.have_tm3 ? sl.tm3 : nullptr, sl.have_tm3);
         post(MCQ_K_ZCONV, n);
       }
       record(5, s);
@@ -483,7 +487,8 @@ struct Enq {
         else if (NS == 1 && zv && !strcmp(zv, "plain"))
           n = launch_zconv(sl.d, Z, c->khat, c->tw, s);
         else
-          n = launch_zconv_seq(sl.d, Z, c->khat, c->tw, s, c->have_tmz2 ? c->tmz2 : nullptr, c->have_tmk);
+          n = NS > 1 ? launch_zconv_seq(sl.d, Z, c->khat, c->tw, s, sl.have_tm3 ? sl.tm3 : nullptr, sl.have_tm3)
+                     : launch_zconv_seq(sl.d, Z, c->khat, c->tw, s, c->have_tmz2 ? c->tmz2 : nullptr, c->have_tmk);
         post(MCQ_K_ZCONV, n);
       }
       if (NS > 1) alltoall(false);
@@ -802,9 +807,14 @@ void free_all(mcq_ctx* c) {
 
 // TMA descriptor of Y[3][nz][Ly][P] viewed as a 3D tensor (P, Ly, 3 nz) of 8-byte elements;
 // box (C, 1, nz) = one component's z column block of a K-Z tile (single slab only).
+void make_slab_maps(mcq_ctx* c);
+
 void make_y_tensor_map(mcq_ctx* c) {
   c->have_tmz = false;
-  if (c->NS != 1) return;
+  if (c->NS != 1) {
+    make_slab_maps(c);
+    return;
+  }
   const Dims& d = c->sl[0].d;
   if (d.nz < 2 || d.nz > 256 || !c->sl[0].Y) return;
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
@@ -847,6 +857,48 @@ void make_y_tensor_map(mcq_ctx* c) {
     if (rk != CUDA_SUCCESS) memset(&c->tmz2[2], 0, sizeof(CUtensorMap));
     c->have_tmz2 = (r2 == CUDA_SUCCESS && r3 == CUDA_SUCCESS);
     c->have_tmk = (rk == CUDA_SUCCESS);
+  }
+}
+
+// z slabs (K-Z v3, SPLIT): per slab, the received blocks R[q][g][zl][ky][KXS] as a 4D tensor
+// (KXS, Ly, nzl, 3 NS); box (16, 1, nzl, 3 NS - 2) with element stride 3 along the last dimension
+// picks component g of every source rank q, so the box lands as [z][c].  And the slab's Khat.
+void make_slab_maps(mcq_ctx* c) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+      cudaGetLastError();
+      return;
+    }
+    enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  for (auto& sl : c->sl) {
+    sl.have_tm3 = false;
+    const Dims& d = sl.d;
+    memset(sl.tm3, 0, sizeof(sl.tm3));
+    // (a box wider than the tensor — KXS < 16 on small slabs — faulted on the device with an
+    // illegal-instruction error: such slabs keep K-Z v2)
+    if (!sl.R || !c->khat || (d.Lz != 512 && d.Lz != 256) || d.nzg > d.Lz / 2 || d.kpitch % 2 || c->NS > 85 ||
+        d.KXS < 16 || 6 * d.kpitch < 96)
+      continue;
+    const cuuint64_t dims[4] = {(cuuint64_t)d.KXS, (cuuint64_t)d.Ly, (cuuint64_t)d.nz, (cuuint64_t)3 * c->NS};
+    const cuuint64_t strides[3] = {(cuuint64_t)d.KXS * 8, (cuuint64_t)d.Ly * d.KXS * 8,
+                                   (cuuint64_t)d.nz * d.Ly * d.KXS * 8};
+    const cuuint32_t box[4] = {16, 1, (cuuint32_t)d.nz, (cuuint32_t)(3 * c->NS - 2)};
+    const cuuint32_t es[4] = {1, 1, 1, 3};
+    const CUresult r = enc(&sl.tm3[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, sl.R, dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const cuuint64_t kd[3] = {(cuuint64_t)6 * d.kpitch, (cuuint64_t)d.Ly / 2 + 1, (cuuint64_t)d.Lz / 2 + 1};
+    const cuuint64_t ks[2] = {(cuuint64_t)6 * d.kpitch * 4, (cuuint64_t)6 * d.kpitch * 4 * (d.Ly / 2 + 1)};
+    const cuuint32_t kb[3] = {96, 1, 129};
+    const cuuint32_t kes[3] = {1, 1, 1};
+    const CUresult rk = enc(&sl.tm3[2], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, c->khat, kd, ks, kb, kes,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    sl.have_tm3 = (r == CUDA_SUCCESS && rk == CUDA_SUCCESS);
   }
 }
 

@@ -442,6 +442,9 @@ static int sm_count() {
 #ifndef MCQ_Z3
 #define MCQ_Z3 1  // Lz = 512 (single slab): K-Z v3 (zconv3.cuh); 0: v2 with TMA-staged columns
 #endif
+#ifndef MCQ_Z3_SPLIT
+#define MCQ_Z3_SPLIT 1  // z slabs (received kx-slab blocks, 4D TMA boxes): K-Z v3 too
+#endif
 #ifndef MCQ_Z3_256
 #define MCQ_Z3_256 0  // Lz = 256 (single slab): K-Z v3 (parity-tested, measured slower: 126.6 vs 105.6
                       // us at configs[1] — one channel leaves v2 no hand-over to save); 0: v2
@@ -457,7 +460,7 @@ static int zconv2_cols(const Dims& d, float2* Y, const float* khat, const float2
   const int ntiles = nlone + nkt * d.Ly;
   CUtensorMap none;
   memset(&none, 0, sizeof(none));
-  if (!SPLIT && tmap && khat_map && (L == 512 ? MCQ_Z3 : MCQ_Z3_256) && d.nz <= L / 2 && d.kxoff == 0) {
+  if (tmap && khat_map && (L == 512 ? MCQ_Z3 : MCQ_Z3_256) && d.nzg <= L / 2 && (!SPLIT || MCQ_Z3_SPLIT)) {
     // K-Z v3 (zconv3.cuh): 16-column tiles, persistent, MINB CTAs per SM; the lone Nyquist
     // column (NKX = 16 q + 1) by v2's lone-tile launch.  tmap: [v2 box, v3 box, Khat]
     using Z3 = Z3Cfg<L>;
@@ -467,11 +470,11 @@ static int zconv2_cols(const Dims& d, float2* Y, const float* khat, const float2
     const int nt3 = nkt3 * d.Ly;
     int n = 0;
     if (nt3 > 0)
-      launch_pdl(d.pdl, k_zconv3<L>, dim3(std::min(nt3, Z3::MINB * sm_count())), dim3(Z3::NT), Z3::SMEM, st, Y, khat,
-                 d, tw, nkt3, nt3, tm3[0], tm3[1]), ++n;
+      launch_pdl(d.pdl, k_zconv3<L, SPLIT>, dim3(std::min(nt3, Z3::MINB * sm_count())), dim3(Z3::NT), Z3::SMEM, st,
+                 Y, khat, d, tw, nkt3, nt3, tm3[0], tm3[1]), ++n;
     if (rem3 == 1) {
       const int nl = (d.Ly + Z::C - 1) / Z::C;
-      launch_pdl(d.pdl, k_zconv2<L, false, false>, dim3(nl), dim3(Z::NT), Z::SMEM, st, Y, khat, d, tw, nkt, nl, nl, 0,
+      launch_pdl(d.pdl, k_zconv2<L, SPLIT, false>, dim3(nl), dim3(Z::NT), Z::SMEM, st, Y, khat, d, tw, nkt, nl, nl, 0,
                  none), ++n;
     }
     return n;
@@ -512,9 +515,9 @@ int launch_zconv_seq(const Dims& d, float2* Y, const float* khat, const float2* 
   bool v2 = d.Lz == 256 ? MCQ_ZV2_256 : MCQ_ZV2_512;
   if (zv && !strcmp(zv, "seq")) v2 = false;
   if (zv && !strcmp(zv, "v2")) v2 = true;
-  if (v2 && d.Lz == 256) return d.NS > 1 ? zconv2_cols<256, true>(d, Y, khat, tw, cols, nullptr, st)
+  if (v2 && d.Lz == 256) return d.NS > 1 ? zconv2_cols<256, true>(d, Y, khat, tw, cols, tmap2, st, khat_map)
                                          : zconv2_cols<256, false>(d, Y, khat, tw, cols, tmap2, st, khat_map);
-  if (v2 && d.Lz == 512) return d.NS > 1 ? zconv2_cols<512, true>(d, Y, khat, tw, cols, nullptr, st)
+  if (v2 && d.Lz == 512) return d.NS > 1 ? zconv2_cols<512, true>(d, Y, khat, tw, cols, tmap2, st, khat_map)
                                          : zconv2_cols<512, false>(d, Y, khat, tw, cols, tmap2, st, khat_map);
   int n = 0;
   MCQ_DISPATCH_L(d.Lz, {
@@ -595,6 +598,8 @@ void configure_pass_kernels() {
   cudaFuncSetAttribute(k_zconv2<512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cfg<512>::SMEM);
   cudaFuncSetAttribute(k_zconv3<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z3Cfg<256>::SMEM);
   cudaFuncSetAttribute(k_zconv3<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z3Cfg<512>::SMEM);
+  cudaFuncSetAttribute(k_zconv3<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z3Cfg<256>::SMEM);
+  cudaFuncSetAttribute(k_zconv3<512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z3Cfg<512>::SMEM);
   cudaGetLastError();
 }
 

@@ -45,7 +45,10 @@ struct Z3Cfg {
   static constexpr int MINB = L == 256 ? MCQ_Z3MINB256 : 1;  // 512: up to 255 registers
 };
 
-template <int L_>
+// SPLIT (z slabs): the received kx-slab blocks R[source rank][component][zl][ky][KXS]; tm is then a
+// 4D map (KXS, Ly, nzl, 3 NS) read with element stride 3 along its last dimension from q = g, so a
+// component's box still lands as [z][c] (z = rank * nzl + zl); stores use zconv2.cuh's zoff.
+template <int L_, bool SPLIT = false>
 __global__ void __launch_bounds__(Z3Cfg<L_>::NT, Z3Cfg<L_>::MINB) k_zconv3(float2* __restrict__ Y, const float* __restrict__ khat,
                                                          Dims d, const float2* __restrict__ gtw, int nkt, int ntiles,
                                                          const __grid_constant__ CUtensorMap tm,
@@ -83,8 +86,14 @@ __global__ void __launch_bounds__(Z3Cfg<L_>::NT, Z3Cfg<L_>::MINB) k_zconv3(float
   __syncthreads();
   pdl_wait();
   const int c = threadIdx.x % C, t = threadIdx.x / C;
-  const int nz = d.nz, hy = d.Ly / 2;
-  const unsigned row = d.KXS, plane = (unsigned)d.Ly * row, cstr = (unsigned)nz * plane;
+  const int nz = d.nzg, nzl = d.nz, hy = d.Ly / 2;  // global planes (the transform's inputs), this slab's
+  const unsigned row = d.KXS, plane = (unsigned)d.Ly * row, cstr = (unsigned)nzl * plane;
+  const float inv_nzl = 1.f / (float)nzl;
+  auto zoff = [&](int z) -> unsigned {  // offset of global plane z (zconv2.cuh)
+    unsigned a = (unsigned)z * plane;
+    if constexpr (SPLIT) a += (unsigned)(2 * nzl * __float2int_rz(((float)z + 0.5f) * inv_nzl)) * plane;
+    return a;
+  };
   const unsigned kzs = (unsigned)(hy + 1) * d.kpitch * 3;  // Khat stride between kz rows (float2 units)
   const float inv_nkt = 1.f / (float)nkt;
   // first column and row of tile j: rows ky and Ly - ky back to back (same folded Khat rows);
@@ -99,7 +108,12 @@ __global__ void __launch_bounds__(Z3Cfg<L_>::NT, Z3Cfg<L_>::MINB) k_zconv3(float
     tile_pos(j, kx0, ky);
     mbar_arrive_expect_tx(&bars[b], (uint32_t)(3 * C * nz * sizeof(float2)));
 #pragma unroll
-    for (int g = 0; g < 3; ++g) tma_load_3d(bufs + b * REG + g * (L / 2) * C, &tm, kx0, ky, g * nz, &bars[b]);
+    for (int g = 0; g < 3; ++g) {
+      if constexpr (SPLIT)
+        tma_load_4d(bufs + b * REG + g * (L / 2) * C, &tm, kx0, ky, 0, g, &bars[b]);
+      else
+        tma_load_3d(bufs + b * REG + g * (L / 2) * C, &tm, kx0, ky, g * nz, &bars[b]);
+    }
   };
   // tile j's Khat rows into region Ks as [kz][C][3] float2 by two TMA tensor copies (tmk: Khat
   // viewed as (6 kpitch floats, Ly/2 + 1, Lz/2 + 1), box (6 C, 1, 129): kz rows 0-128 and 129-257,
@@ -239,7 +253,7 @@ __global__ void __launch_bounds__(Z3Cfg<L_>::NT, Z3Cfg<L_>::MINB) k_zconv3(float
 #pragma unroll
         for (int i = 0; i < EN; ++i) {
           const int z = t + 16 * i;
-          if (z < nz) Y[col + g * cstr + (unsigned)z * plane] = NCH == 2 ? add2(X[g][0][i], X[g][NCH - 1][i]) : X[g][0][i];
+          if (z < nz) Y[col + g * cstr + zoff(z)] = NCH == 2 ? add2(X[g][0][i], X[g][NCH - 1][i]) : X[g][0][i];
         }
       }
     }

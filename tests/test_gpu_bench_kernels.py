@@ -78,10 +78,13 @@ def test_bench_kernel_instances(kind, grid, what):
 
 
 @pytest.mark.parametrize("kind,grid,slabs", [("disc", (16, 6, 100), 4), ("film", (8, 6, 200), 5),
-                                             ("film", (6, 3, 129), 3)])
+                                             ("film", (6, 3, 129), 3), ("disc", (64, 8, 150), 2),
+                                             ("film", (64, 6, 256), 4)])
 def test_zconv2_split_addressing_bitwise(kind, grid, slabs):
-    """The SPLIT instance (z slabs: source-rank blocks, kx slabs per rank) gives bit-identical
-    results to the single-slab instance."""
+    """The SPLIT instances (z slabs: source-rank blocks, kx slabs per rank) give bit-identical
+    results to the single-slab instance: K-Z v2 SPLIT for narrow kx slabs, K-Z v3 SPLIT (4D TMA
+    boxes over the received blocks) at Lz = 512 once a kx slab is >= 16 columns wide
+    (64 x 8 x 150 in 2 slabs, 64 x 6 x 256 in 4)."""
     cfg = small_config(kind, grid, seed=32, state="phys")
     one = mcq.Solver.from_config(cfg)
     many = mcq.Solver.from_config(cfg, dist={"rank": -1, "world": slabs})
